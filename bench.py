@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py -- TernaryNet ternary conv3d / FCN throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the hot path over BASELINE.json configs[1] (C1): the
+int8 ternary codes 1x64x64x128x128 are packed (A1, tn_pack_i8) and convolved
+with 64x64x3x3x3 ternary filters with the fused integer-threshold requant (A2-A4,
+tn_conv3d_requant).  `value` = effective GMAC/s (out voxels x K x C x 27 per
+step, all ranks) with inputs resident in HBM.  The same JSON line carries:
+  roofline     -- the conv kernel's achieved rate vs its binding peak
+  e2e          -- the same metric through the C ABI with host buffers (H2D of
+                  the codes + D2H of the packed output inside the timed region)
+  fcn          -- FCN voxels/s (A1-A9): configs[3] (8 CT-like volumes
+                  128x256x256, sharded one volume at a time across ranks)
+  cpu_baseline -- the oracle (oracle/, untuned) on a bounded sample of C1
+  clocks       -- NVML SM clocks and throttle reasons sampled during timing
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own C1 replica
+(weak scaling, no data-path collective; BASELINE configs shard by volume), max
+device time over ranks.  `--impl reference` times the CPU oracle instead
+(rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+C1 = synth.CONFIGS["C1"]
+C1_MACS = 64 * 128 * 128 * 64 * 64 * 27          # out voxels x K x C x 27 = 115,964,116,992
+FCN_MACS_PER_VOXEL = 45360
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--fcn-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fcn", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    """Samples SM clock and throttle reasons every 5 ms on a background thread."""
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._names = {}
+        if self.ok:
+            for name in ("GpuIdle", "ApplicationsClocksSetting", "SwPowerCap", "HwSlowdown", "SyncBoost",
+                         "SwThermalSlowdown", "HwThermalSlowdown", "HwPowerBrakeSlowdown", "DisplayClockSetting"):
+                v = getattr(self.nv, "nvmlClocksEventReason" + name, None) or \
+                    getattr(self.nv, "nvmlClocksThrottleReason" + name, None)
+                if v:
+                    self._names[v] = name
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self._names.items():
+                    if r & bit and name != "GpuIdle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_c1_sample(x, w, lo, hi, planes: int):
+    """Oracle conv3d + requant over output planes [0, planes) of C1 (input planes [0, planes+1))."""
+    import oracle
+    xs = np.ascontiguousarray(x[:, :, :planes + 1])
+    acc = oracle.conv3d(xs, w)[:, :, :planes]
+    oracle.requant(np.ascontiguousarray(acc), lo, hi)
+    return planes * 128 * 128 * 64 * 64 * 27
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    x, w, lo, hi = synth.conv_config("C1")
+    planes = 2
+    for _ in range(args.warmup):
+        oracle_c1_sample(x, w, lo, hi, planes)
+    times = []
+    macs = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = time.perf_counter()
+        macs += oracle_c1_sample(x, w, lo, hi, planes)
+        times.append(time.perf_counter() - s)
+    tot = time.perf_counter() - t0
+    value = macs / tot / 1e9
+    line = {
+        "impl": "reference", "metric": "ternary conv3d effective GMAC/s (C1, fused requant)",
+        "value": value, "unit": "GMAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 + requant (BASELINE configs[1])",
+                   "sample": f"output planes [0,{planes}) of 64 per step"},
+        "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"oracle conv3d+requant, {planes} of 64 output planes of C1 per step"},
+        "e2e": {"value": value, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1801_09449_b200 as tn
+
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    tnpk = os.path.join(ROOT, "profiles", "PEAKS_TN.json")
+    tn_peaks = json.load(open(tnpk)) if os.path.exists(tnpk) else {}
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # ---- C1 inputs (same seeds on every rank: replicas)
+    x, w, lo, hi = synth.conv_config("C1")
+    x_host = torch.from_numpy(x).pin_memory()
+    x_d = x_host.to(dev)
+    w_d = torch.from_numpy(w).to(dev)
+    lo_d, hi_d = torch.from_numpy(lo).to(dev), torch.from_numpy(hi).to(dev)
+    xd = tn.dims(*x.shape)
+    g = tn.geom(1, 1, 1)
+    wp = tn.tn_pack_weights(w_d)
+    xp = tn.packed_empty(*x.shape, device=dev)
+    yp = tn.packed_empty(1, 64, 64, 128, 128, device=dev)
+    yp_host = torch.empty(yp.shape, dtype=torch.int32).pin_memory()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        tn.tn_pack_i8(x_d, xp)
+        tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+
+    # ---- parity gate (SPEC.md:485 pattern: no number without a passing check)
+    step()
+    torch.cuda.synchronize()
+    parity = "skipped"
+    if rank == 0:
+        import oracle
+        gen = synth.rng(1234)
+        m = 256
+        at = np.stack([np.zeros(m, int), gen.integers(0, 64, m), gen.integers(0, 64, m),
+                       gen.integers(0, 128, m), gen.integers(0, 128, m)], 1).astype(np.int32)
+        acc = oracle.conv3d_at(x, w, at)
+        n_, k_, z_, y_, x_ = at.T
+        ref = np.where(acc >= hi[k_], 1, np.where(acc <= lo[k_], -1, 0))
+        ypn = yp.cpu().numpy().view(np.uint32)
+        sb = (ypn[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
+        mb = (ypn[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
+        got = np.where(mb == 1, np.where(sb == 1, 1, -1), 0)
+        if not np.array_equal(got, ref):
+            print(json.dumps({"error": "parity check failed; refusing to report"}), flush=True)
+            sys.exit(1)
+        parity = "passed (256 sampled outputs vs oracle)"
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps outside the events
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            a, b, c = ev[i]
+            a.record(stream)
+            tn.tn_pack_i8(x_d, xp)
+            b.record(stream)
+            tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+            c.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(c) for a, _, c in ev]
+    conv_ms = [b.elapsed_time(c) for _, b, c in ev]
+    pack_ms = [a.elapsed_time(b) for a, b, _ in ev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * args.steps * C1_MACS / (tot_ms / 1e3) / 1e9
+
+    # ---- e2e through the C ABI with host buffers
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        x_d.copy_(x_host, non_blocking=True)
+        step()
+        yp_host.copy_(yp, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * e2e_steps * C1_MACS / (e2e_ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (the conv)
+    conv_avg_s = float(np.mean(conv_ms)) / 1e3
+    kernel = tn.tn_get_conv_kernel()
+    uses_tc = bool(tn_peaks.get("tc_active_for_c1", False)) and kernel != tn.TN_KERNEL_POPC
+    clocks = clk.summary()
+    if uses_tc:
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        peak = 2.0 * bf16          # int8 dense = 2 x bf16 dense (nominal 4.5 vs 2.25 PFLOP/s)
+        achieved = 2.0 * C1_MACS / conv_avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "2 x MEASURED_PEAKS.bf16_tflops (int8/bf16 nominal ratio)"}
+    else:
+        popc_per_clk = tn_peaks.get("popc_per_clk_per_sm", 16.0)
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        # 2 POPC per 32-lane word pair -> 16 MAC per POPC
+        peak = popc_per_clk * 16 * 148 * mhz * 1e6 / 1e12
+        achieved = C1_MACS / conv_avg_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TMAC/s (POPC pipe)",
+                "frac": achieved / peak, "traffic": tn_peaks.get("c1_conv_dram_bytes"),
+                "peak_source": f"{popc_per_clk} POPC/clk/SM x 16 MAC/POPC x 148 SM x {mhz} MHz"
+                               + (" (measured POPC rate)" if "popc_per_clk_per_sm" in tn_peaks else
+                                  " (assumed POPC rate)")}
+    roof["kernel"] = "tn_conv3d_requant"
+    roof["avg_ms"] = conv_avg_s * 1e3
+    roof["share_of_step"] = float(np.sum(conv_ms) / np.sum(step_ms))
+
+    # ---- FCN voxels/s: configs[3], 8 volumes sharded across ranks
+    fcn = None
+    if not args.no_fcn:
+        fcn = bench_fcn(args, tn, torch, dist, world, rank, dev, stream)
+
+    # ---- cpu baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        t0 = time.perf_counter()
+        m1 = oracle_c1_sample(x, w, lo, hi, 1)
+        dt1 = time.perf_counter() - t0
+        planes = int(max(1, min(63, 12.0 / max(dt1, 1e-3))))
+        t0 = time.perf_counter()
+        mm = oracle_c1_sample(x, w, lo, hi, planes)
+        dt = time.perf_counter() - t0
+        cpu = {"value": mm / dt / 1e9, "unit": "GMAC/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": f"oracle conv3d+requant over output planes [0,{planes}) of C1's 64 ({dt:.1f} s)",
+               "host_cores_visible": cpu_cores()}
+
+    if rank == 0:
+        line = {
+            "metric": "ternary conv3d effective GMAC/s (C1, fused requant)",
+            "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 s1 p1 + fused "
+                                   "integer-threshold requant, P(0)=0.5 act / 0.6 weights (BASELINE configs[1])",
+                       "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
+                       "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
+                       "conv_kernel": {0: "auto", 1: "popc", 2: "tcgen05-i8"}[kernel],
+                       "l2": "256 MiB buffer zeroed between timed steps, outside the events",
+                       "parallelism": f"replicas x{world}", "parity": parity},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GMAC/s", "steps": e2e_steps,
+                    "h2d_bytes_per_step": int(x_host.numel()), "d2h_bytes_per_step": int(yp.numel() * 4)},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+            "pack_ms": float(np.mean(pack_ms)),
+            "fcn": fcn,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
+    cfg = synth.CONFIGS["C3"]
+    p = synth.fcn_params(cfg["seed_params"])
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"],
+                        device=dev)
+    mine = [i for i in range(len(cfg["seeds"])) if i % world == rank]
+    shape = cfg["vol_shape"]
+    vols = [torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][i])).to(dev) for i in mine]
+    ws = net.workspace(shape, dev)
+    logits = torch.empty((1, 2) + shape[2:], dtype=torch.float32, device=dev)
+    for v in vols[:1]:
+        net(v, logits=logits, ws=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.fcn_steps):
+        for v in vols:
+            net(v, logits=logits, ws=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    vox = int(np.prod(shape[2:]))
+    total_vox = args.fcn_steps * len(cfg["seeds"]) * vox
+    return {"metric": "FCN voxels/s", "value": total_vox / (ms / 1e3), "unit": "voxels/s",
+            "config": "C3: 8 CT-like volumes 1x1x128x256x256, one volume per rank at a time (BASELINE configs[3])",
+            "ms_per_batch": ms / args.fcn_steps, "effective_gmacs": total_vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
+            "steps": args.fcn_steps, "gpu_launches_per_volume": 15, "scaling": "strong (fixed batch of 8)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,183 @@
+/*
+ * tn.h -- C ABI of libtn.so, the B200 (sm_100a) TernaryNet inference hot path.
+ *
+ * The calls follow the paper's statement of the problem (Heinrich, Blendowski,
+ * Oktay, "TernaryNet", arXiv 1801.09449; cited PAPER.md:<line>):
+ *   pack ternary tensors into sign / nonzero-mask bitplanes (PAPER.md:118 and
+ *   Fig. 3, :130), convolve them with ternary 3x3x3 filter banks where every
+ *   inner product is Eq. 9's masked Hamming distance,
+ *   requantise the int32 result to ternary with per-channel integer thresholds
+ *   that fold alpha, batch norm and Eq. 6 (PAPER.md:91-95, :130,
+ *   :135), chain these blocks into a U-Net-style FCN with skip concatenation and
+ *   x2 up/down-sampling (Table 1), and finish with a float
+ *   prediction layer.
+ *
+ * Conventions (readings R1-R16):
+ *  - Every pointer is a DEVICE pointer unless documented "host".  Every call is
+ *    asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream).  The caller allocates and owns all memory; the
+ *    library never allocates on the hot path (tn_fcn_create / tn_comm_init are
+ *    setup calls).
+ *  - Ternary codes: int8 in {-1, 0, +1}, logical layout NCDHW (PyTorch order).
+ *  - Packed ternary tensor (reading R3): uint32 [n][d][h][w][2][cw],
+ *    cw = ceil(c/32).  Per voxel the cw SIGN words come first (bit = 1 <=> +1),
+ *    then the cw MASK words (bit = 1 <=> nonzero; reading R2).  Channel ch is
+ *    bit (ch % 32) of word (ch / 32), LSB first.  Zero = (sign 0, mask 0);
+ *    padding lanes are 0.  Byte size: tn_packed_bytes().
+ *  - Packed weights: uint32 [k][27][2][cw] from int8 [k][c][3][3][3]; tap
+ *    t = (dz*3 + dy)*3 + dx.
+ *  - Convolutions are 3x3x3 cross-correlations with zero padding (PyTorch
+ *    semantics).  Output extent per axis: (len + 2*pad - 2*dil - 1)/stride + 1.
+ *  - Requantisation (reading R5): t = +1 if acc >= hi[k]; else -1 if
+ *    acc <= lo[k]; else 0.
+ *  - 16-byte alignment is required for every tensor pointer (128-bit I/O).
+ *
+ * Errors: host-detectable errors return before any work is queued, with text in
+ * tn_last_error().  Device-detected domain errors (a code outside {-1,0,1}, a
+ * NaN/Inf float, a non-canonical packed word) are reported through the caller's
+ * int64 *d_bad: the caller initialises it to INT64_MAX (tn_bad_init() queues
+ * that), the kernel atomicMin()s the first offending flat NCDHW index into it;
+ * outputs are unspecified when *d_bad != INT64_MAX after the stream syncs
+ * ("domain error naming the offending index").  d_bad may be NULL
+ * (no reporting).  CUDA / NCCL failures return TN_ECUDA / TN_ENCCL.  The
+ * library never aborts and never throws across this ABI.
+ */
+#ifndef TN_H_
+#define TN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tn_stream; /* == cudaStream_t */
+
+typedef enum {
+    TN_OK = 0,
+    TN_EINVAL = 1,        /* null pointer, bad enum, k/c < 1, ... */
+    TN_ESHAPE = 2,        /* inconsistent or unsupported extents */
+    TN_EALIGN = 3,        /* pointer not 16-byte aligned */
+    TN_EUNSUPPORTED = 4,  /* valid request this build does not implement */
+    TN_EDOMAIN = 5,       /* reserved (domain errors are reported via d_bad) */
+    TN_ECUDA = 6,
+    TN_ENCCL = 7
+} tn_status;
+
+typedef struct { int32_t n, c, d, h, w; } tn_dims;              /* logical NCDHW            */
+typedef struct { int32_t stride[3], pad[3], dil[3]; } tn_geom;  /* z, y, x; kernel 3x3x3    */
+
+/* ---- sizes and helpers (host) ------------------------------------------- */
+size_t      tn_packed_bytes(tn_dims x);                /* n*d*h*w * 2*ceil(c/32) * 4   */
+size_t      tn_weight_bytes(int32_t k, int32_t c);     /* k * 27 * 2*ceil(c/32) * 4    */
+/* Output dims of a conv of x with k filters; TN_ESHAPE if an extent is < 1.        */
+tn_status   tn_conv_out_dims(tn_dims x, int32_t k, tn_geom g, tn_dims* out /*host*/);
+const char* tn_last_error(void);                       /* thread-local text            */
+const char* tn_version(void);
+/* Queue *d_bad = INT64_MAX on stream. */
+tn_status   tn_bad_init(int64_t* d_bad, tn_stream stream);
+
+/* ---- A1: ternarise and pack (Eq. 6) --- */
+/* x int8 NCDHW codes -> xp packed.  Domain: code not in {-1,0,1}.            */
+tn_status tn_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, tn_stream stream);
+/* x int32 NCDHW codes -> xp packed.  Domain: code not in {-1,0,1}.           */
+tn_status tn_pack_i32(const int32_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, tn_stream stream);
+/* x float NCDHW -> Eq. 6 with folded normalisation (reading R7):
+ * +1 if x > t_hi, -1 if x < t_lo, else 0.  Domain: NaN / Inf.  Needs t_lo <= t_hi. */
+tn_status tn_pack_f32(const float* x, tn_dims xd, float t_lo, float t_hi, uint32_t* xp,
+                      int64_t* d_bad, tn_stream stream);
+/* w int8 [k][c][3][3][3] -> wp [k][27][2][cw].  Domain: code not in {-1,0,1}. */
+tn_status tn_pack_weights(const int8_t* w, int32_t k, int32_t c, uint32_t* wp, int64_t* d_bad,
+                          tn_stream stream);
+/* xp packed -> x int8 NCDHW.  Domain: sign bit on a zero, or a padding lane set
+ * (reported at the voxel's channel c-1 index).                               */
+tn_status tn_unpack(const uint32_t* xp, tn_dims xd, int8_t* x, int64_t* d_bad, tn_stream stream);
+
+/* ---- A2/A3/A5: ternary conv3d, Eq. 9 (dilation :135) ---- */
+/* y int32 channel-last [n][do][ho][wo][k] (reading R14).                     */
+tn_status tn_conv3d(const uint32_t* xp, tn_dims xd, const uint32_t* wp, int32_t k, tn_geom g,
+                    int32_t* y, tn_stream stream);
+/* A4 fused: yp packed [n][do][ho][wo][2][ceil(k/32)]; lo, hi int32 [k].      */
+tn_status tn_conv3d_requant(const uint32_t* xp, tn_dims xd, const uint32_t* wp, int32_t k,
+                            tn_geom g, const int32_t* lo, const int32_t* hi, uint32_t* yp,
+                            tn_stream stream);
+/* A4 standalone: y int32 channel-last [n][d][h][w][k] (yd.c == k) -> yp packed. */
+tn_status tn_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int32_t* hi,
+                     uint32_t* yp, tn_stream stream);
+
+/* ---- A6: conv over [upsample_x2(a) | b] concatenation */
+/* A convolution whose input is the channel concatenation of nseg (1 or 2)
+ * packed segments, each optionally nearest-x2 upsampled (reading R10).  The
+ * conv-input extents are the segments' common extents after upsampling.  The
+ * conv is the sum of per-segment convs with the segment's slice of the filter
+ * bank (channel order = segment order).  Exactly one of y (int32 channel-last)
+ * or yp (packed, needs lo/hi) must be non-NULL.  All segments must have the
+ * same ceil(c/32) in this build (TN_EUNSUPPORTED otherwise).                 */
+typedef struct {
+    const uint32_t* xp;   /* packed segment; if upsample, at LOW resolution      */
+    tn_dims d;            /* its dims (low-resolution dims if upsample)          */
+    int32_t upsample;     /* 0 = none, 1 = nearest x2 in z, y and x              */
+    const uint32_t* wp;   /* packed weights of this segment [k][27][2][ceil(d.c/32)] */
+} tn_segment;
+tn_status tn_conv3d_seg(const tn_segment* segs /*host array*/, int32_t nseg, int32_t k,
+                        tn_geom g, const int32_t* lo, const int32_t* hi, int32_t* y,
+                        uint32_t* yp, tn_stream stream);
+
+/* ---- A7: first layer -- Eq. 6 on the float input fused with a conv from 1
+ * channel and the requant epilogue (reading R7).
+ * x float [n][1][d][h][w]; wp packed [k][27][2][1]; yp packed.  Domain: NaN/Inf. */
+tn_status tn_conv3d_first(const float* x, tn_dims xd, float t_lo, float t_hi, const uint32_t* wp,
+                          int32_t k, tn_geom g, const int32_t* lo, const int32_t* hi,
+                          uint32_t* yp, int64_t* d_bad, tn_stream stream);
+
+/* ---- A8: prediction, 1x1x1 float conv (reading R12) --- */
+/* tp packed [n][d][h][w][2][1] (td.c <= 32); w float [nclass][td.c]; b float
+ * [nclass]; logits float NCDHW [n][nclass][d][h][w].  Sum order: b, then c
+ * ascending, fp32.                                                            */
+tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
+                     int32_t nclass, float* logits, tn_stream stream);
+
+/* ---- A9: the ternary FCN (Table 1 analogue, reading R9) ------------------- */
+/* A layer table entry.  Layers run in table order; src[] refers to earlier
+ * entries (or -1 = the network input, which requires kind TN_LAYER_FIRST).    */
+enum { TN_LAYER_FIRST = 1, TN_LAYER_CONV = 2 };
+typedef struct {
+    int32_t kind;            /* TN_LAYER_FIRST (float input, 1 channel) or TN_LAYER_CONV */
+    int32_t c_out;
+    int32_t stride;          /* 1 or 2 in all three axes; pad = dil               */
+    int32_t dil;             /* >= 1                                              */
+    int32_t nseg;            /* 1 or 2 input segments (concatenated in this order) */
+    int32_t src[2];          /* producing layer index, or -1 for the input        */
+    int32_t upsample[2];     /* nearest x2 of that segment                        */
+    const uint32_t* wp[2];   /* packed weights per segment (borrowed)             */
+    const int32_t* lo;       /* [c_out] (borrowed)                                */
+    const int32_t* hi;       /* [c_out] (borrowed)                                */
+} tn_layer;
+typedef struct tn_fcn tn_fcn;
+/* layers: host array, copied.  pred_w [nclass][c_out of the last layer] and
+ * pred_b [nclass] are device pointers (borrowed).  t_lo/t_hi: Eq. 6 input band. */
+tn_status tn_fcn_create(const tn_layer* layers, int32_t n_layers, float t_lo, float t_hi,
+                        const float* pred_w, const float* pred_b, int32_t nclass, tn_fcn** out);
+size_t    tn_fcn_workspace_bytes(const tn_fcn* net, tn_dims xd);
+/* x float [n][1][d][h][w] -> logits float [n][nclass][d][h][w]. */
+tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
+                         size_t ws_bytes, int64_t* d_bad, tn_stream stream);
+void      tn_fcn_destroy(tn_fcn* net);
+
+/* Internal-activation access for debugging and per-layer parity: after a
+ * tn_fcn_forward on the same ws, returns the device pointer and dims of layer
+ * i's packed output inside ws (NULL if out of range).                        */
+const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* ws, int32_t i,
+                                    tn_dims* out_dims /*host*/);
+
+/* Kernel selection for the ternary conv (both exact; parity tests run both).
+ * TN_KERNEL_AUTO picks per shape.  Host, process-wide.                        */
+enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2 };
+tn_status tn_set_conv_kernel(int32_t which);
+int32_t   tn_get_conv_kernel(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_H_ */

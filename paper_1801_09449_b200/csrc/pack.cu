@@ -1,0 +1,356 @@
+// pack.cu -- A1 ternarise-and-pack, unpack, standalone A4 requant, A8 prediction.
+//
+// Packed layout (include/tn.h, reading R3): uint32 [n][d][h][w][2][cw]; per voxel
+// cw sign words (bit = +1) then cw mask words (bit = nonzero); channel c is bit
+// c%32 of word c/32.  Encoding: PAPER.md:118 ("2 bits per entry that encode the
+// sign and value") and Fig. 3, mask = nonzero (reading R2).
+//
+// All kernels here are HBM-bound streaming kernels: one thread per voxel (or per
+// 4 voxels for the vectorised packers), coalesced along the innermost axis.
+#include "tn_internal.cuh"
+
+#include <climits>
+
+namespace tn {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void report_bad(int64_t* d_bad, int64_t idx) {
+    if (d_bad != nullptr && idx != LLONG_MAX)
+        atomicMin(reinterpret_cast<long long*>(d_bad), static_cast<long long>(idx));
+}
+
+// ----------------------------------------------------------------------------
+// Integer / float codes NCDHW -> packed.  VPT consecutive voxels per thread
+// (vector loads along the contiguous DHW axis), CW words per plane held in
+// registers and written as one 8/16/32-byte store per voxel.
+// ----------------------------------------------------------------------------
+template <typename T> struct Vec4;
+template <> struct Vec4<int8_t>  { using type = char4; };
+template <> struct Vec4<int32_t> { using type = int4; };
+template <> struct Vec4<float>   { using type = float4; };
+
+template <typename T>
+struct Classify;
+template <> struct Classify<int8_t> {
+    float t_lo, t_hi;
+    __device__ __forceinline__ int operator()(int8_t v, bool& ok) const {
+        ok = (v >= -1 && v <= 1);
+        return v;
+    }
+};
+template <> struct Classify<int32_t> {
+    float t_lo, t_hi;
+    __device__ __forceinline__ int operator()(int32_t v, bool& ok) const {
+        ok = (v >= -1 && v <= 1);
+        return v;
+    }
+};
+template <> struct Classify<float> {
+    float t_lo, t_hi;
+    // Eq. 6 with folded normalisation thresholds (reading R7).
+    __device__ __forceinline__ int operator()(float v, bool& ok) const {
+        ok = isfinite(v);
+        return v > t_hi ? 1 : (v < t_lo ? -1 : 0);
+    }
+};
+
+template <int CW>
+__device__ __forceinline__ void store_voxel(uint32_t* dst, const uint32_t (&s)[CW], const uint32_t (&m)[CW]) {
+    if constexpr (CW == 1) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(s[0], m[0]);
+    } else if constexpr (CW == 2) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(s[0], s[1], m[0], m[1]);
+    } else if constexpr (CW == 4) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(s[0], s[1], s[2], s[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(m[0], m[1], m[2], m[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) { dst[j] = s[j]; dst[CW + j] = m[j]; }
+    }
+}
+
+template <typename T, int CW, int VPT>
+__global__ void __launch_bounds__(kThreads)
+pack_kernel(const T* __restrict__ x, int C, int64_t DHW, int64_t total, Classify<T> cls,
+            uint32_t* __restrict__ xp, int64_t* d_bad) {
+    const int64_t g0 = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) * VPT;
+    if (g0 >= total) return;
+    const int64_t n = g0 / DHW;
+    const int64_t v0 = g0 - n * DHW;
+    const T* xb = x + n * C * DHW + v0;
+    uint32_t s[VPT][CW], m[VPT][CW];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) { s[i][j] = 0u; m[i][j] = 0u; }
+    int64_t bad = LLONG_MAX;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+        const int cend = min(C, 32 * (j + 1));
+        for (int c = 32 * j; c < cend; ++c) {
+            T vals[VPT];
+            if constexpr (VPT == 4) {
+                auto q = *reinterpret_cast<const typename Vec4<T>::type*>(xb + c * DHW);
+                vals[0] = q.x; vals[1] = q.y; vals[2] = q.z; vals[3] = q.w;
+            } else {
+                vals[0] = xb[c * DHW];
+            }
+            const uint32_t bit = 1u << (c & 31);
+#pragma unroll
+            for (int i = 0; i < VPT; ++i) {
+                bool ok;
+                const int t = cls(vals[i], ok);
+                if (!ok) {
+                    const int64_t idx = (n * C + c) * DHW + v0 + i;
+                    bad = min(bad, idx);
+                    continue;
+                }
+                m[i][j] |= (t != 0) ? bit : 0u;
+                s[i][j] |= (t == 1) ? bit : 0u;
+            }
+        }
+    }
+    report_bad(d_bad, bad);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        if (g0 + i < total) store_voxel<CW>(xp + (g0 + i) * 2 * CW, s[i], m[i]);
+    }
+}
+
+// Generic fallback: one thread per (voxel, word); any C.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+pack_generic_kernel(const T* __restrict__ x, int C, int cw, int64_t DHW, int64_t total,
+                    Classify<T> cls, uint32_t* __restrict__ xp, int64_t* d_bad) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    if (t >= total * cw) return;
+    const int64_t g = t / cw;
+    const int j = static_cast<int>(t - g * cw);
+    const int64_t n = g / DHW;
+    const int64_t v = g - n * DHW;
+    uint32_t s = 0, m = 0;
+    int64_t bad = LLONG_MAX;
+    const int cend = min(C, 32 * (j + 1));
+    for (int c = 32 * j; c < cend; ++c) {
+        bool ok;
+        const int64_t idx = (n * C + c) * DHW + v;
+        const int q = cls(x[idx], ok);
+        if (!ok) { bad = min(bad, idx); continue; }
+        const uint32_t bit = 1u << (c & 31);
+        m |= (q != 0) ? bit : 0u;
+        s |= (q == 1) ? bit : 0u;
+    }
+    report_bad(d_bad, bad);
+    xp[g * 2 * cw + j] = s;
+    xp[g * 2 * cw + cw + j] = m;
+}
+
+template <typename T>
+cudaError_t pack_dispatch(const T* x, tn_dims xd, Classify<T> cls, uint32_t* xp, int64_t* d_bad,
+                          cudaStream_t st) {
+    const int64_t DHW = static_cast<int64_t>(xd.d) * xd.h * xd.w;
+    const int64_t total = DHW * xd.n;
+    if (total == 0) return cudaSuccess;
+    const int cw = (xd.c + 31) / 32;
+    const bool vec4 = (DHW % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0);
+#define TN_PACK_CASE(CWV)                                                                    \
+    if (cw == CWV) {                                                                         \
+        if (vec4) {                                                                          \
+            const int64_t nt = (total + 3) / 4;                                              \
+            pack_kernel<T, CWV, 4><<<static_cast<unsigned>((nt + kThreads - 1) / kThreads), \
+                                      kThreads, 0, st>>>(x, xd.c, DHW, total, cls, xp, d_bad); \
+        } else {                                                                             \
+            pack_kernel<T, CWV, 1><<<static_cast<unsigned>((total + kThreads - 1) / kThreads), \
+                                      kThreads, 0, st>>>(x, xd.c, DHW, total, cls, xp, d_bad); \
+        }                                                                                    \
+        return cudaGetLastError();                                                           \
+    }
+    TN_PACK_CASE(1)
+    TN_PACK_CASE(2)
+    TN_PACK_CASE(4)
+#undef TN_PACK_CASE
+    const int64_t nt = total * cw;
+    pack_generic_kernel<T><<<static_cast<unsigned>((nt + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+        x, xd.c, cw, DHW, total, cls, xp, d_bad);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// Weights int8 [K][C][27] -> [K][27][2][CW]; one thread per (k, tap, word).
+// ----------------------------------------------------------------------------
+__global__ void pack_weights_kernel(const int8_t* __restrict__ w, int K, int C, int cw,
+                                    uint32_t* __restrict__ wp, int64_t* d_bad) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= K * 27 * cw) return;
+    const int j = t % cw;
+    const int tap = (t / cw) % 27;
+    const int k = t / (cw * 27);
+    uint32_t s = 0, m = 0;
+    int64_t bad = LLONG_MAX;
+    const int cend = min(C, 32 * (j + 1));
+    for (int c = 32 * j; c < cend; ++c) {
+        const int64_t idx = (static_cast<int64_t>(k) * C + c) * 27 + tap;
+        const int8_t v = w[idx];
+        if (v < -1 || v > 1) { bad = min(bad, idx); continue; }
+        const uint32_t bit = 1u << (c & 31);
+        m |= (v != 0) ? bit : 0u;
+        s |= (v == 1) ? bit : 0u;
+    }
+    report_bad(d_bad, bad);
+    uint32_t* dst = wp + (static_cast<int64_t>(k) * 27 + tap) * 2 * cw;
+    dst[j] = s;
+    dst[cw + j] = m;
+}
+
+// ----------------------------------------------------------------------------
+// Unpack: packed -> int8 NCDHW, with canonical-form validation.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+unpack_kernel(const uint32_t* __restrict__ xp, int C, int cw, int64_t DHW, int64_t total,
+              int8_t* __restrict__ x, int64_t* d_bad) {
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    if (g >= total) return;
+    const int64_t n = g / DHW;
+    const int64_t v = g - n * DHW;
+    const uint32_t* src = xp + g * 2 * cw;
+    int64_t bad = LLONG_MAX;
+    for (int j = 0; j < cw; ++j) {
+        const uint32_t s = src[j], m = src[cw + j];
+        const int cend = min(C, 32 * (j + 1));
+        for (int c = 32 * j; c < cend; ++c) {
+            const int b = c & 31;
+            const uint32_t sb = (s >> b) & 1u, mb = (m >> b) & 1u;
+            const int64_t idx = (n * C + c) * DHW + v;
+            if (sb && !mb) bad = min(bad, idx);
+            x[idx] = static_cast<int8_t>(mb ? (sb ? 1 : -1) : 0);
+        }
+        if (cend < 32 * (j + 1)) {
+            const uint32_t padmask = 0xFFFFFFFFu << (cend & 31);
+            if ((s | m) & padmask) bad = min(bad, (n * C + (C - 1)) * DHW + v);
+        }
+    }
+    report_bad(d_bad, bad);
+}
+
+// ----------------------------------------------------------------------------
+// Standalone requant (A4): int32 channel-last [V][K] -> packed [V][2][cwo].
+// One warp per (voxel, word): lane l owns channel 32*word + l; the sign and
+// mask words are warp ballots.  Reads are coalesced along K.
+// Rule (reading R5): +1 if acc >= hi[k]; else -1 if acc <= lo[k]; else 0.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+requant_kernel(const int32_t* __restrict__ y, int64_t V, int K, int cwo,
+               const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
+               uint32_t* __restrict__ yp) {
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= V * cwo) return;
+    const int64_t v = warp / cwo;
+    const int j = static_cast<int>(warp - v * cwo);
+    const int k = 32 * j + lane;
+    bool pos = false, neg = false;
+    if (k < K) {
+        const int32_t a = y[v * K + k];
+        pos = a >= __ldg(hi + k);
+        neg = !pos && a <= __ldg(lo + k);
+    }
+    const uint32_t s = __ballot_sync(0xFFFFFFFFu, pos);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, pos || neg);
+    if (lane == 0) {
+        yp[v * 2 * cwo + j] = s;
+        yp[v * 2 * cwo + cwo + j] = m;
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Prediction (A8): logits[n][j][v] = b[j] + sum_c w[j][c] * t_c in fp32, c
+// ascending (reading R12).  One thread per voxel; C <= 32.
+// ----------------------------------------------------------------------------
+constexpr int kMaxClass = 8;
+__global__ void __launch_bounds__(kThreads)
+predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t total,
+               const float* __restrict__ w, const float* __restrict__ b, int nclass,
+               float* __restrict__ logits) {
+    __shared__ float sw[kMaxClass * 32];
+    __shared__ float sb[kMaxClass];
+    for (int i = threadIdx.x; i < nclass * C; i += kThreads) sw[i] = w[i];
+    if (threadIdx.x < nclass) sb[threadIdx.x] = b[threadIdx.x];
+    __syncthreads();
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    if (g >= total) return;
+    const uint2 sm = *reinterpret_cast<const uint2*>(tp + g * 2);
+    const int64_t n = g / DHW;
+    const int64_t v = g - n * DHW;
+    for (int j = 0; j < nclass; ++j) {
+        float acc = sb[j];
+        for (int c = 0; c < C; ++c) {
+            const float wv = sw[j * C + c];
+            const bool nz = (sm.y >> c) & 1u;
+            const bool p = (sm.x >> c) & 1u;
+            acc += nz ? (p ? wv : -wv) : 0.0f;
+        }
+        logits[(n * nclass + j) * DHW + v] = acc;
+    }
+}
+
+__global__ void bad_init_kernel(int64_t* d_bad) { *d_bad = LLONG_MAX; }
+
+}  // namespace
+
+cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, cudaStream_t s) {
+    return pack_dispatch<int8_t>(x, xd, Classify<int8_t>{0.f, 0.f}, xp, d_bad, s);
+}
+cudaError_t launch_pack_i32(const int32_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, cudaStream_t s) {
+    return pack_dispatch<int32_t>(x, xd, Classify<int32_t>{0.f, 0.f}, xp, d_bad, s);
+}
+cudaError_t launch_pack_f32(const float* x, tn_dims xd, float t_lo, float t_hi, uint32_t* xp,
+                            int64_t* d_bad, cudaStream_t s) {
+    return pack_dispatch<float>(x, xd, Classify<float>{t_lo, t_hi}, xp, d_bad, s);
+}
+
+cudaError_t launch_pack_weights(const int8_t* w, int k, int c, uint32_t* wp, int64_t* d_bad,
+                                cudaStream_t s) {
+    const int cw = (c + 31) / 32;
+    const int nt = k * 27 * cw;
+    pack_weights_kernel<<<(nt + 127) / 128, 128, 0, s>>>(w, k, c, cw, wp, d_bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const uint32_t* xp, tn_dims xd, int8_t* x, int64_t* d_bad, cudaStream_t s) {
+    const int64_t DHW = static_cast<int64_t>(xd.d) * xd.h * xd.w;
+    const int64_t total = DHW * xd.n;
+    if (total == 0) return cudaSuccess;
+    unpack_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        xp, xd.c, (xd.c + 31) / 32, DHW, total, x, d_bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int32_t* hi,
+                           uint32_t* yp, cudaStream_t s) {
+    const int64_t V = static_cast<int64_t>(yd.n) * yd.d * yd.h * yd.w;
+    if (V == 0) return cudaSuccess;
+    const int cwo = (yd.c + 31) / 32;
+    const int64_t threads = V * cwo * 32;
+    requant_kernel<<<static_cast<unsigned>((threads + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        y, V, yd.c, cwo, lo, hi, yp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
+                           int nclass, float* logits, cudaStream_t s) {
+    const int64_t DHW = static_cast<int64_t>(td.d) * td.h * td.w;
+    const int64_t total = DHW * td.n;
+    if (total == 0) return cudaSuccess;
+    predict_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        tp, td.c, DHW, total, w, b, nclass, logits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bad_init(int64_t* d_bad, cudaStream_t s) {
+    bad_init_kernel<<<1, 1, 0, s>>>(d_bad);
+    return cudaGetLastError();
+}
+
+}  // namespace tn

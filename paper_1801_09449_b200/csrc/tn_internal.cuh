@@ -1,0 +1,93 @@
+// tn_internal.cuh -- internal kernel parameter blocks and helpers for libtn.so.
+// Not part of the ABI (include/tn.h is).  sm_100a only.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/tn.h"
+
+namespace tn {
+
+constexpr int kMaxSeg = 2;
+
+// One input segment of a (possibly concatenated) convolution, in the
+// coordinates of the segment's own buffer.  "Source resolution" is the
+// resolution the buffer is stored at (low resolution if up == 1).
+struct SegDesc {
+    const uint32_t* xp;   // packed [n][D][H][W][2][cw]
+    const uint32_t* wp;   // packed weights [K][27][2][cw]
+    int cw;               // words per bitplane per voxel
+    int D, H, W;          // buffer extents (source resolution)
+    int zbeg;             // global source-resolution z of buffer plane 0 (slabs)
+    int up;               // nearest x2 upsampling of this segment
+};
+
+// A ternary conv launch: output buffer [N][Do][Ho][Wo] covering global output
+// planes [zo_beg, zo_beg + Do).  Conv-input ("ci") coordinates are at the
+// resolution after upsampling; the global ci extents Dci/Hci/Wci define the
+// zero padding.
+struct ConvDesc {
+    SegDesc seg[kMaxSeg];
+    int nseg;
+    int N, K;
+    int s[3], p[3], dl[3];        // z, y, x
+    int Do, Ho, Wo;
+    int zo_beg;
+    int Dci, Hci, Wci;            // global conv-input extents (z, y, x)
+    // outputs: exactly one of y / yp
+    int32_t* y;                   // int32 channel-last [N][Do][Ho][Wo][K]
+    uint32_t* yp;                 // packed [N][Do][Ho][Wo][2][cwo]
+    const int32_t* lo;
+    const int32_t* hi;
+    int cwo;
+};
+
+struct FirstDesc {
+    const float* x;               // [N][1][D][H][W] (buffer), global z of plane 0 = zbeg
+    int D, H, W, zbeg, Dg;        // Dg: global extent in z for padding
+    float t_lo, t_hi;
+    const uint32_t* wp;           // [K][27][2][1]
+    int N, K;
+    int s[3], p[3], dl[3];
+    int Do, Ho, Wo, zo_beg;
+    const int32_t* lo;
+    const int32_t* hi;
+    uint32_t* yp;                 // packed [N][Do][Ho][Wo][2][1]
+    int64_t* d_bad;
+    int64_t bad_base;             // flat index of buffer element 0 in the global tensor
+    int64_t bad_nstride;          // global per-n stride (D_g*H*W)
+};
+
+// Kernel launchers (return cudaGetLastError()).
+cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, cudaStream_t s);
+cudaError_t launch_pack_i32(const int32_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, cudaStream_t s);
+cudaError_t launch_pack_f32(const float* x, tn_dims xd, float t_lo, float t_hi, uint32_t* xp,
+                            int64_t* d_bad, cudaStream_t s);
+cudaError_t launch_pack_weights(const int8_t* w, int k, int c, uint32_t* wp, int64_t* d_bad,
+                                cudaStream_t s);
+cudaError_t launch_unpack(const uint32_t* xp, tn_dims xd, int8_t* x, int64_t* d_bad, cudaStream_t s);
+cudaError_t launch_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int32_t* hi,
+                           uint32_t* yp, cudaStream_t s);
+cudaError_t launch_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
+                           int nclass, float* logits, cudaStream_t s);
+cudaError_t launch_bad_init(int64_t* d_bad, cudaStream_t s);
+
+cudaError_t launch_conv_popc(const ConvDesc& cd, cudaStream_t s);
+cudaError_t launch_conv_first(const FirstDesc& fd, cudaStream_t s);
+
+// tcgen05 implicit-GEMM path; returns cudaErrorNotSupported if the shape is
+// outside what the kernel handles (caller then uses the popc kernel).
+bool        conv_tc_supported(const ConvDesc& cd);
+cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
+
+// Host-side error text.
+void set_error(const char* fmt, ...);
+
+inline int out_extent(int len, int s, int p, int dl) {
+    int span = len + 2 * p - 2 * dl - 1;
+    return span < 0 ? 0 : span / s + 1;
+}
+
+}  // namespace tn

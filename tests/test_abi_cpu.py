@@ -1,0 +1,102 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/tn.h
+declares, and its host-side validation answers without touching a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "tn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(tn_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+@pytest.fixture(scope="module")
+def tn():
+    from paper_1801_09449_b200 import build
+    build.build_library()
+    import paper_1801_09449_b200 as tn
+    return tn
+
+
+def test_library_exports_every_declared_symbol(tn):
+    names = _declared_functions()
+    assert len(names) >= 20
+    raw = ctypes.CDLL(tn.LIB_PATH)
+    for n in names:
+        assert hasattr(raw, n), f"libtn.so does not export {n}"
+    # the binding wraps exactly the declared set
+    assert set(tn.SIGNATURES) == set(names)
+
+
+def test_sizes_and_out_dims(tn):
+    assert tn.lib.tn_packed_bytes(tn.dims(1, 64, 64, 128, 128)) == 1048576 * 16
+    assert tn.lib.tn_packed_bytes(tn.dims(1, 16, 32, 32, 32)) == 32768 * 8
+    assert tn.lib.tn_packed_bytes(tn.dims(2, 33, 1, 1, 1)) == 2 * 16
+    assert tn.lib.tn_packed_bytes(tn.dims(0, 16, 4, 4, 4)) == 0
+    assert tn.lib.tn_weight_bytes(64, 64) == 64 * 27 * 16
+    od = tn.conv_out_dims(tn.dims(1, 16, 96, 144, 144), 16, tn.geom(2, 1, 1))
+    assert (od.d, od.h, od.w, od.c) == (48, 72, 72, 16)
+    od = tn.conv_out_dims(tn.dims(1, 3, 9, 9, 9), 5, tn.geom(1, 2, 2))
+    assert (od.d, od.h, od.w) == (9, 9, 9)
+    with pytest.raises(tn.TNError) as e:
+        tn.conv_out_dims(tn.dims(1, 3, 1, 1, 1), 5, tn.geom(1, 0, 1))
+    assert e.value.status == tn.TN_ESHAPE
+
+
+def test_host_validation_before_any_launch(tn):
+    d = tn.dims(1, 16, 4, 4, 4)
+    g = tn.geom()
+    assert tn.lib.tn_pack_i8(None, d, None, None, None) == tn.TN_EINVAL
+    assert "NULL" in tn.lib.tn_last_error().decode()
+    assert tn.lib.tn_pack_i8(ctypes.c_void_p(0x1003), d, ctypes.c_void_p(0x1000), None, None) == tn.TN_EALIGN
+    assert tn.lib.tn_conv3d(None, d, None, 0, g, None, None) == tn.TN_EINVAL
+    bad_g = tn.geom(0, 1, 1)
+    assert tn.lib.tn_conv3d(ctypes.c_void_p(0x1000), d, ctypes.c_void_p(0x1000), 4, bad_g,
+                            ctypes.c_void_p(0x1000), None) == tn.TN_EINVAL
+    assert tn.lib.tn_pack_f32(ctypes.c_void_p(0x1000), tn.dims(1, 1, 4, 4, 4), 1.0, -1.0,
+                              ctypes.c_void_p(0x1000), None, None) == tn.TN_EINVAL
+    assert tn.lib.tn_conv3d_first(ctypes.c_void_p(0x1000), tn.dims(1, 2, 4, 4, 4), 0.0, 1.0,
+                                  ctypes.c_void_p(0x1000), 16, g, ctypes.c_void_p(0x1000),
+                                  ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), None, None) == tn.TN_ESHAPE
+    assert tn.lib.tn_predict(ctypes.c_void_p(0x1000), tn.dims(1, 64, 4, 4, 4), ctypes.c_void_p(0x1000),
+                             ctypes.c_void_p(0x1000), 2, ctypes.c_void_p(0x1000), None) == tn.TN_EUNSUPPORTED
+    # empty tensors are a successful no-op
+    assert tn.lib.tn_pack_i8(None, tn.dims(1, 16, 0, 4, 4), None, None, None) == tn.TN_OK
+    assert tn.lib.tn_set_conv_kernel(7) == tn.TN_EINVAL
+    assert tn.lib.tn_set_conv_kernel(tn.TN_KERNEL_AUTO) == tn.TN_OK
+
+
+def test_fcn_create_validation_and_workspace(tn):
+    P = ctypes.c_void_p(0x1000)
+    table = tn.fcn_table()
+    layers = (tn.tn_layer * len(table))()
+    for i, (kind, co, s, segs) in enumerate(table):
+        L = layers[i]
+        L.kind, L.c_out, L.stride, L.dil, L.nseg = kind, co, s, 1, len(segs)
+        for j, (src, up) in enumerate(segs):
+            L.src[j], L.upsample[j], L.wp[j] = src, up, 0x1000
+        L.lo = L.hi = 0x1000
+    h = ctypes.c_void_p()
+    assert tn.lib.tn_fcn_create(layers, len(table), -200.0, 200.0, P, P, 2, ctypes.byref(h)) == tn.TN_OK
+    ws = tn.lib.tn_fcn_workspace_bytes(h, tn.dims(1, 1, 96, 144, 144))
+    R0 = 96 * 144 * 144
+    # packed bytes/voxel: 8 for c <= 32, 16 for c = 64.  R0: #1 #2 #13 #14; R1: #3 #4 #11 #12;
+    # R2: #5 (32) #6 (64) #9 (64) #10 (32); R3: #7 #8 (64)
+    expect = 8 * R0 * 4 + 8 * (R0 // 8) * 4 + 48 * (R0 // 64) + 32 * (R0 // 512)
+    assert abs(ws - expect) < 256 * 16
+    tn.lib.tn_fcn_destroy(h)
+    # a forward reference is rejected
+    layers[3].src[0] = 5
+    assert tn.lib.tn_fcn_create(layers, len(table), -200.0, 200.0, P, P, 2, ctypes.byref(h)) == tn.TN_EINVAL
+
+
+def test_fcn_macs_per_voxel_matches_survey(tn):
+    # 45,360 ternary MACs per input voxel; C2 = 90.30 G MAC
+    assert tn.fcn_macs_per_voxel() == 45360
+    assert abs(45360 * 96 * 144 * 144 / 1e9 - 90.30) < 0.01

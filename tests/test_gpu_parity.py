@@ -1,0 +1,300 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): bit-exact for packed words and int32 accumulators;
+logits within 1e-5 relative in the sense of reading R13:
+    |g - o| <= 1e-5 * max(|o|, |b_j| + sum_c |w_jc|).
+Sizes span several CTA tiles with ragged tails; C0 runs whole; C1 runs at full size
+in the bench's launch configuration and is checked on sampled outputs.
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tn():
+    import paper_1801_09449_b200 as tn
+    return tn
+
+
+@pytest.fixture(params=["popc", "auto"])
+def kernel(request, tn):
+    sel = {"popc": tn.TN_KERNEL_POPC, "auto": tn.TN_KERNEL_AUTO}[request.param]
+    tn.tn_set_conv_kernel(sel)
+    yield request.param
+    tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def bad_value(flag):
+    torch.cuda.synchronize()
+    return int(flag.item())
+
+
+# --------------------------------------------------------------------------- A1 pack
+@pytest.mark.parametrize("shape", [(1, 16, 32, 32, 32), (2, 1, 3, 5, 7), (1, 33, 4, 5, 6), (1, 64, 6, 7, 9),
+                                   (2, 100, 3, 3, 4), (1, 130, 2, 3, 5), (1, 32, 1, 1, 1)])
+def test_pack_i8_i32_matches_oracle(tn, shape):
+    x = synth.ternary_codes(shape, 0.5, seed=sum(shape))
+    ref, bad = oracle.pack(x)
+    assert bad == -1
+    flag = tn.bad_flag()
+    got = tn.tn_pack_i8(dev(x), d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    np.testing.assert_array_equal(u32(got), ref)
+    got32 = tn.tn_pack_i32(dev(x.astype(np.int32)))
+    np.testing.assert_array_equal(u32(got32), ref)
+    # roundtrip through tn_unpack
+    back = tn.tn_unpack(got, shape[1], d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    np.testing.assert_array_equal(back.cpu().numpy(), x)
+
+
+def test_pack_domain_errors(tn):
+    x = synth.ternary_codes((1, 20, 4, 4, 8), 0.5, seed=1)
+    x[0, 7, 2, 1, 3] = 3
+    x[0, 19, 3, 3, 7] = -2
+    flag = tn.bad_flag()
+    tn.tn_pack_i8(dev(x), d_bad=flag)
+    _, obad = oracle.pack(x)
+    assert bad_value(flag) == obad == np.ravel_multi_index((0, 7, 2, 1, 3), x.shape)
+    flag = tn.bad_flag()
+    tn.tn_pack_i32(dev(x.astype(np.int32)), d_bad=flag)
+    assert bad_value(flag) == obad
+
+
+def test_pack_f32_eq6(tn):
+    x = synth.ct_volume((2, 3, 8, 9, 12), seed=2)
+    x[0, 1, 2, 3, 4] = np.float32(synth.CT_T_HI)  # boundary -> 0
+    x[1, 2, 7, 8, 11] = np.float32(synth.CT_T_LO)
+    t, bad = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    ref, _ = oracle.pack(t)
+    flag = tn.bad_flag()
+    got = tn.tn_pack_f32(dev(x), synth.CT_T_LO, synth.CT_T_HI, d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    np.testing.assert_array_equal(u32(got), ref)
+    x[1, 0, 5, 5, 5] = np.nan
+    x[1, 1, 0, 0, 0] = np.inf
+    _, obad = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    flag = tn.bad_flag()
+    tn.tn_pack_f32(dev(x), synth.CT_T_LO, synth.CT_T_HI, d_bad=flag)
+    assert bad_value(flag) == obad
+
+
+def test_pack_weights_and_unpack_noncanonical(tn):
+    for k, c in ((16, 16), (64, 64), (5, 33), (3, 1), (64, 128)):
+        w = synth.ternary_codes((k, c, 3, 3, 3), 0.6, seed=k * c)
+        ref, _ = oracle.pack_weights(w)
+        np.testing.assert_array_equal(u32(tn.tn_pack_weights(dev(w))), ref)
+    x = synth.ternary_codes((1, 3, 1, 2, 2), 0.5, seed=4)
+    xp, _ = oracle.pack(x)
+    xp[0, 0, 1, 0, 0, 0] |= np.uint32(1 << 1)
+    xp[0, 0, 1, 0, 1, 0] &= np.uint32(0xFFFFFFFD)
+    _, obad = oracle.unpack(xp, 3)
+    flag = tn.bad_flag()
+    tn.tn_unpack(dev(xp.view(np.int32)), 3, d_bad=flag)
+    assert bad_value(flag) == obad >= 0
+
+
+# --------------------------------------------------------------------------- A2/A3/A5 conv
+CONV_CASES = [
+    # (x shape NCDHW, k, stride, pad, dil)
+    ((1, 16, 32, 32, 32), 16, 1, 1, 1),          # C0 whole
+    ((1, 16, 9, 17, 35), 16, 1, 1, 1),           # ragged tails in every axis
+    ((2, 64, 7, 10, 21), 64, 1, 1, 1),
+    ((1, 32, 12, 18, 20), 32, 2, 1, 1),          # stride 2 (A5)
+    ((1, 64, 10, 12, 14), 64, 2, 1, 1),
+    ((1, 33, 6, 7, 8), 5, 1, 1, 1),              # 2 words, ragged channels, odd K
+    ((1, 16, 11, 12, 13), 16, 1, 2, 2),          # dilation 2
+    ((1, 1, 5, 6, 7), 3, 1, 1, 1),               # one channel
+    ((1, 128, 4, 5, 6), 16, 1, 1, 1),            # 4 words
+    ((1, 16, 5, 6, 7), 7, (1, 2, 1), (0, 1, 2), (1, 1, 2)),  # anisotropic geometry
+    ((1, 16, 1, 1, 1), 16, 1, 1, 1),             # a single voxel
+]
+
+
+def _case(shape, k, seed):
+    x = synth.ternary_codes(shape, 0.5, seed=seed)
+    w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.6, seed=seed + 1)
+    return x, w
+
+
+@pytest.mark.parametrize("case", CONV_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}")
+def test_conv3d_int32_matches_oracle(tn, kernel, case):
+    shape, k, s, p, dl = case
+    x, w = _case(shape, k, seed=zlib.crc32(str(case).encode()) % 1000)
+    ref = oracle.conv3d(x, w, s, p, dl)                       # [n,k,do,ho,wo]
+    xp = tn.tn_pack_i8(dev(x))
+    wp = tn.tn_pack_weights(dev(w))
+    y = tn.tn_conv3d(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl))
+    np.testing.assert_array_equal(y.cpu().numpy(), ref.transpose(0, 2, 3, 4, 1))
+
+
+@pytest.mark.parametrize("case", CONV_CASES[:7], ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}")
+def test_conv3d_requant_matches_oracle(tn, kernel, case):
+    shape, k, s, p, dl = case
+    x, w = _case(shape, k, seed=7 + shape[2])
+    base = synth.threshold_base(shape[1], 0.5)
+    lo, hi = synth.jittered_thresholds(k, base, seed=k)
+    acc = oracle.conv3d(x, w, s, p, dl)
+    ref, _ = oracle.pack(oracle.requant(acc, lo, hi))
+    xp = tn.tn_pack_i8(dev(x))
+    wp = tn.tn_pack_weights(dev(w))
+    yp = tn.tn_conv3d_requant(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+    # standalone requant of the int32 result gives the same words
+    y = tn.tn_conv3d(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl))
+    np.testing.assert_array_equal(u32(tn.tn_requant(y, dev(lo), dev(hi))), ref)
+
+
+def test_requant_sentinels_and_order(tn):
+    i32 = np.iinfo(np.int32)
+    y = np.arange(-40, 40, dtype=np.int32).reshape(1, 1, 1, 80, 1).repeat(40, axis=4)
+    lo = np.full(40, -3, np.int32)
+    hi = np.full(40, 3, np.int32)
+    lo[0], hi[0] = i32.min, i32.min          # always +1
+    lo[1], hi[1] = i32.max, i32.max          # always -1
+    lo[2], hi[2] = i32.min, i32.max          # always 0
+    lo[3], hi[3] = 5, 0                      # hi tested first
+    ref, _ = oracle.pack(oracle.requant(np.ascontiguousarray(y.transpose(0, 4, 1, 2, 3)), lo, hi))
+    np.testing.assert_array_equal(u32(tn.tn_requant(dev(y), dev(lo), dev(hi))), ref)
+
+
+# --------------------------------------------------------------------------- A6 upsample + concat
+@pytest.mark.parametrize("low,cl,cs,k", [((3, 4, 5), 16, 16, 16), ((2, 3, 9), 64, 64, 64),
+                                         ((4, 4, 4), 32, 32, 32), ((1, 1, 1), 16, 16, 8)])
+def test_conv3d_upsample_concat_matches_oracle(tn, kernel, low, cl, cs, k):
+    n = 1
+    a = synth.ternary_codes((n, cl) + low, 0.5, seed=cl)
+    b = synth.ternary_codes((n, cs) + tuple(2 * v for v in low), 0.5, seed=cs + 1)
+    w = synth.ternary_codes((k, cl + cs, 3, 3, 3), 0.6, seed=k + 2)
+    base = synth.threshold_base(cl + cs, 0.5)
+    lo, hi = synth.jittered_thresholds(k, base, seed=3)
+    acc = oracle.conv3d(oracle.concat(oracle.upsample2(a), b), w)
+    ref_t = oracle.requant(acc, lo, hi)
+    ref, _ = oracle.pack(ref_t)
+    ap, bp = tn.tn_pack_i8(dev(a)), tn.tn_pack_i8(dev(b))
+    wa = tn.tn_pack_weights(dev(np.ascontiguousarray(w[:, :cl])))
+    wb = tn.tn_pack_weights(dev(np.ascontiguousarray(w[:, cl:])))
+    segs = [(ap, tn.dims(n, cl, *low), 1, wa), (bp, tn.dims(n, cs, *b.shape[2:]), 0, wb)]
+    yp = tn.tn_conv3d_seg(segs, k, tn.geom(), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+    y = tn.tn_conv3d_seg(segs, k, tn.geom(), requant=False)
+    np.testing.assert_array_equal(y.cpu().numpy(), acc.transpose(0, 2, 3, 4, 1))
+
+
+# --------------------------------------------------------------------------- A7 first layer
+@pytest.mark.parametrize("shape,stride", [((1, 1, 16, 24, 40), 1), ((2, 1, 7, 9, 33), 1), ((1, 1, 12, 16, 16), 2)])
+def test_conv3d_first_matches_oracle(tn, shape, stride):
+    x = synth.ct_volume(shape, seed=shape[3])
+    w = synth.ternary_codes((16, 1, 3, 3, 3), 0.6, seed=5)
+    lo, hi = synth.jittered_thresholds(16, synth.threshold_base(1, 0.38), seed=6)
+    t, _ = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    ref, _ = oracle.pack(oracle.requant(oracle.conv3d(t, w, stride), lo, hi))
+    flag = tn.bad_flag()
+    yp = tn.tn_conv3d_first(dev(x), synth.CT_T_LO, synth.CT_T_HI, tn.tn_pack_weights(dev(w)), 16,
+                            tn.geom(stride), dev(lo), dev(hi), d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    np.testing.assert_array_equal(u32(yp), ref)
+    x[0, 0, 3, 4, 5] = np.nan
+    flag = tn.bad_flag()
+    tn.tn_conv3d_first(dev(x), synth.CT_T_LO, synth.CT_T_HI, tn.tn_pack_weights(dev(w)), 16,
+                       tn.geom(stride), dev(lo), dev(hi), d_bad=flag)
+    _, obad = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    assert bad_value(flag) == obad
+
+
+# --------------------------------------------------------------------------- A8 prediction
+def _logit_tol(w, b):
+    return 1e-5 * (np.abs(b)[None, :, None, None, None] + np.abs(w).sum(1)[None, :, None, None, None])
+
+
+def test_predict_matches_oracle(tn):
+    t = synth.ternary_codes((2, 16, 5, 9, 13), 0.5, seed=8)
+    p = synth.fcn_params()
+    ref = oracle.predict(t, p["pred_w"], p["pred_b"])
+    tp = tn.tn_pack_i8(dev(t))
+    got = tn.tn_predict(tp, 16, dev(p["pred_w"]), dev(p["pred_b"])).cpu().numpy()
+    tol = np.maximum(np.abs(ref), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(got - ref) <= tol)
+
+
+# --------------------------------------------------------------------------- A9 FCN
+def _fcn_compare(tn, x, p, per_layer=True):
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    xd = dev(x)
+    ws = net.workspace(x.shape)
+    flag = tn.bad_flag()
+    logits = net(xd, ws=ws, d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    ref_logits, acts, bad = oracle.fcn_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"],
+                                               p["pred_w"], p["pred_b"], want_acts=per_layer)
+    assert bad == -1
+    if per_layer:
+        for i in range(14):
+            view, od = net.layer_output(x.shape, ws, i)
+            ref, _ = oracle.pack(acts[i])
+            np.testing.assert_array_equal(u32(view), ref, err_msg=f"layer #{i + 1}")
+    got = logits.cpu().numpy()
+    tol = np.maximum(np.abs(ref_logits), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(got - ref_logits) <= tol)
+    return got
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 16, 16, 16), (1, 1, 32, 48, 48), (2, 1, 8, 24, 40)])
+def test_fcn_matches_oracle_small(tn, kernel, shape):
+    x = synth.ct_volume(shape, seed=shape[3])
+    _fcn_compare(tn, x, synth.fcn_params())
+
+
+def test_fcn_c2_full_size_matches_oracle(tn):
+    """BASELINE.json configs[2] at full size (96 x 144 x 144), every layer bit-exact."""
+    cfg = synth.CONFIGS["C2"]
+    x = synth.ct_volume(cfg["vol_shape"], seed=cfg["seeds"][0])
+    _fcn_compare(tn, x, synth.fcn_params(cfg["seed_params"]))
+
+
+# --------------------------------------------------------------------------- C1 at full size
+def test_c1_full_size_sampled(tn):
+    """configs[1] (1x64x64x128x128, K=64, fused requant) in the bench's launch
+    configuration; 4096 sampled outputs against the oracle's per-output sum, and the
+    canonical-form property on every output word."""
+    x, w, lo, hi = synth.conv_config("C1")
+    xp = tn.tn_pack_i8(dev(x))
+    wp = tn.tn_pack_weights(dev(w))
+    xd = tn.dims(*x.shape)
+    yp = u32(tn.tn_conv3d_requant(xp, xd, wp, 64, tn.geom(), dev(lo), dev(hi)))
+    y = tn.tn_conv3d(xp, xd, wp, 64, tn.geom()).cpu().numpy()
+    g = synth.rng(99)
+    m = 4096
+    at = np.stack([np.zeros(m, int), g.integers(0, 64, m), g.integers(0, 64, m), g.integers(0, 128, m),
+                   g.integers(0, 128, m)], 1).astype(np.int32)
+    # include the corners and faces (padding paths)
+    at[:8, 2:] = [[0, 0, 0], [63, 127, 127], [0, 127, 0], [63, 0, 127], [31, 0, 64], [31, 127, 64],
+                  [0, 64, 64], [63, 64, 64]]
+    ref_acc = oracle.conv3d_at(x, w, at)
+    n_, k_, z_, y_, x_ = at.T
+    np.testing.assert_array_equal(y[n_, z_, y_, x_, k_], ref_acc)
+    ref_t = np.where(ref_acc >= hi[k_], 1, np.where(ref_acc <= lo[k_], -1, 0))
+    s_bit = (yp[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
+    m_bit = (yp[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
+    got_t = np.where(m_bit == 1, np.where(s_bit == 1, 1, -1), 0)
+    np.testing.assert_array_equal(got_t, ref_t)
+    assert np.all(yp[..., 0, :] & ~yp[..., 1, :] == 0)
+    # the int32 and packed outputs agree everywhere (requant of the full int32 tensor)
+    y_t = torch.from_numpy(y).cuda()
+    np.testing.assert_array_equal(u32(tn.tn_requant(y_t, dev(lo), dev(hi))), yp)
