@@ -290,8 +290,8 @@ def main():
 
     # ---- roofline of the dominant kernel (the conv)
     conv_avg_s = float(np.mean(conv_ms)) / 1e3
-    kernel = tn.tn_get_conv_kernel()
-    uses_tc = bool(tn_peaks.get("tc_active_for_c1", False)) and kernel != tn.TN_KERNEL_POPC
+    kernel = tn.tn_conv_kernel_for([xd], 64, g)
+    uses_tc = kernel == tn.TN_KERNEL_TC
     clocks = clk.summary()
     if uses_tc:
         bf16 = peaks.get("bf16_tflops", 1590.0)
@@ -345,7 +345,7 @@ def main():
                                    "integer-threshold requant, P(0)=0.5 act / 0.6 weights (BASELINE configs[1])",
                        "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
                        "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
-                       "conv_kernel": {0: "auto", 1: "popc", 2: "tcgen05-i8"}[kernel],
+                       "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)", 2: "tcgen05 kind::i8 implicit GEMM"}.get(kernel, "?"),
                        "l2": "256 MiB buffer zeroed between timed steps, outside the events",
                        "parallelism": f"replicas x{world}", "parity": parity},
             "roofline": roof,

@@ -176,6 +176,10 @@ const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* w
 enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2 };
 tn_status tn_set_conv_kernel(int32_t which);
 int32_t   tn_get_conv_kernel(void);
+/* Which kernel (TN_KERNEL_POPC or TN_KERNEL_TC) a tn_conv3d_seg call with these
+ * arguments would run under the current selection; -1 if the call is invalid
+ * (or TN_KERNEL_TC is forced on a shape it does not cover).  Host only.       */
+int32_t   tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);
 
 #ifdef __cplusplus
 }

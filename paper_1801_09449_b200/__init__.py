@@ -84,6 +84,7 @@ SIGNATURES = {
     "tn_fcn_layer_output": (_P, [_P, _D, _P, _I32, ctypes.POINTER(_D)]),
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
     "tn_get_conv_kernel": (_I32, []),
+    "tn_conv_kernel_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
 }
 
 
@@ -263,6 +264,15 @@ def tn_set_conv_kernel(which: int):
 
 def tn_get_conv_kernel() -> int:
     return int(lib.tn_get_conv_kernel())
+
+
+def tn_conv_kernel_for(seg_dims, k, g: tn_geom, upsample=None) -> int:
+    """Kernel a conv over segments with these dims would use (shape logic only)."""
+    upsample = upsample or [0] * len(seg_dims)
+    arr = (tn_segment * len(seg_dims))()
+    for i, (d, up) in enumerate(zip(seg_dims, upsample)):
+        arr[i] = tn_segment(None, d, int(up), None)
+    return int(lib.tn_conv_kernel_for(arr, len(seg_dims), int(k), g))
 
 
 # ----------------------------------------------------------------------------- the FCN

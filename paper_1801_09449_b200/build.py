@@ -1,6 +1,7 @@
 """Build libtn.so (the CUDA path) in-tree with nvcc for sm_100a.
 
-`python -m paper_1801_09449_b200.build` or `build_library()`.  Object files go
+`python paper_1801_09449_b200/build.py [--force]` (run it by path: importing the
+package needs the library) or `__graft_entry__.build()`.  Object files go
 to paper_1801_09449_b200/build/ and are rebuilt when a source or header is
 newer; the shared library is linked next to this file so it travels with the
 repo snapshot to the GPU box.

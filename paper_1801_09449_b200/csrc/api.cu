@@ -202,6 +202,7 @@ tn_status build_conv(const tn_segment* segs, int nseg, int k, tn_geom g, const i
             return fail(TN_ESHAPE, "segment %d extents differ from segment 0 after upsampling", i);
         SegDesc& sd = cd.seg[i];
         sd.xp = s.xp; sd.wp = s.wp;
+        sd.c = s.d.c;
         sd.cw = (s.d.c + 31) / 32;
         sd.D = s.d.d; sd.H = s.d.h; sd.W = s.d.w; sd.zbeg = 0; sd.up = s.upsample;
         if (sd.cw != cd.seg[0].cw)
@@ -312,5 +313,24 @@ tn_status tn_set_conv_kernel(int32_t which) {
 }
 
 int32_t tn_get_conv_kernel(void) { return g_conv_kernel; }
+
+int32_t tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g) {
+    if (segs == nullptr) return -1;
+    // a dummy output pointer: only the shape logic of build_conv is used here
+    ConvDesc cd;
+    uint32_t* dummy = reinterpret_cast<uint32_t*>(static_cast<uintptr_t>(256));
+    static const int32_t zero = 0;
+    tn_segment tmp[kMaxSeg];
+    for (int i = 0; i < nseg && i < kMaxSeg; ++i) {
+        tmp[i] = segs[i];
+        if (tmp[i].xp == nullptr) tmp[i].xp = dummy;
+        if (tmp[i].wp == nullptr) tmp[i].wp = dummy;
+    }
+    if (build_conv(tmp, nseg, k, g, &zero, &zero, nullptr, dummy, &cd, nullptr) != TN_OK) return -1;
+    const bool tc = conv_tc_supported(cd);
+    if (g_conv_kernel == TN_KERNEL_TC) return tc ? TN_KERNEL_TC : -1;
+    if (g_conv_kernel == TN_KERNEL_POPC) return TN_KERNEL_POPC;
+    return tc ? TN_KERNEL_TC : TN_KERNEL_POPC;
+}
 
 }  // extern "C"

@@ -203,6 +203,7 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
             SegDesc& sd = cd.seg[sgi];
             sd.xp = reinterpret_cast<const uint32_t*>(base + sp.off);
             sd.wp = ly.wp[sgi];
+            sd.c = sp.out.c;
             sd.cw = (sp.out.c + 31) / 32;
             sd.D = sp.out.d; sd.H = sp.out.h; sd.W = sp.out.w;
             sd.zbeg = 0;

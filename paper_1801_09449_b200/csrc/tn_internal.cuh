@@ -18,6 +18,7 @@ constexpr int kMaxSeg = 2;
 struct SegDesc {
     const uint32_t* xp;   // packed [n][D][H][W][2][cw]
     const uint32_t* wp;   // packed weights [K][27][2][cw]
+    int c;                // logical channels of this segment
     int cw;               // words per bitplane per voxel
     int D, H, W;          // buffer extents (source resolution)
     int zbeg;             // global source-resolution z of buffer plane 0 (slabs)

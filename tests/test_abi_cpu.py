@@ -18,8 +18,8 @@ def _declared_functions():
 
 @pytest.fixture(scope="module")
 def tn():
-    from paper_1801_09449_b200 import build
-    build.build_library()
+    import __graft_entry__
+    __graft_entry__.build()
     import paper_1801_09449_b200 as tn
     return tn
 

@@ -24,12 +24,32 @@ def tn():
     return tn
 
 
-@pytest.fixture(params=["popc", "auto"])
+@pytest.fixture(params=["popc", "tc", "auto"])
 def kernel(request, tn):
+    """Run a conv test with the CUDA-core popc kernel, the tcgen05 kernel (skipped
+    for shapes it does not cover), or the automatic choice."""
+    sel = {"popc": tn.TN_KERNEL_POPC, "tc": tn.TN_KERNEL_TC, "auto": tn.TN_KERNEL_AUTO}[request.param]
+    tn.tn_set_conv_kernel(sel)
+    yield request.param
+    tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+
+
+@pytest.fixture(params=["popc", "auto"])
+def fcn_kernel(request, tn):
     sel = {"popc": tn.TN_KERNEL_POPC, "auto": tn.TN_KERNEL_AUTO}[request.param]
     tn.tn_set_conv_kernel(sel)
     yield request.param
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+
+
+def run_or_skip(kernel, fn, *a, **kw):
+    import paper_1801_09449_b200 as tn
+    try:
+        return fn(*a, **kw)
+    except tn.TNError as e:
+        if kernel == "tc" and e.status == tn.TN_EUNSUPPORTED:
+            pytest.skip("shape outside the tcgen05 kernel")
+        raise
 
 
 def dev(a):
@@ -140,7 +160,7 @@ def test_conv3d_int32_matches_oracle(tn, kernel, case):
     ref = oracle.conv3d(x, w, s, p, dl)                       # [n,k,do,ho,wo]
     xp = tn.tn_pack_i8(dev(x))
     wp = tn.tn_pack_weights(dev(w))
-    y = tn.tn_conv3d(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl))
+    y = run_or_skip(kernel, tn.tn_conv3d, xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl))
     np.testing.assert_array_equal(y.cpu().numpy(), ref.transpose(0, 2, 3, 4, 1))
 
 
@@ -154,7 +174,7 @@ def test_conv3d_requant_matches_oracle(tn, kernel, case):
     ref, _ = oracle.pack(oracle.requant(acc, lo, hi))
     xp = tn.tn_pack_i8(dev(x))
     wp = tn.tn_pack_weights(dev(w))
-    yp = tn.tn_conv3d_requant(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl), dev(lo), dev(hi))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl), dev(lo), dev(hi))
     np.testing.assert_array_equal(u32(yp), ref)
     # standalone requant of the int32 result gives the same words
     y = tn.tn_conv3d(xp, tn.dims(*shape), wp, k, tn.geom(s, p, dl))
@@ -191,7 +211,7 @@ def test_conv3d_upsample_concat_matches_oracle(tn, kernel, low, cl, cs, k):
     wa = tn.tn_pack_weights(dev(np.ascontiguousarray(w[:, :cl])))
     wb = tn.tn_pack_weights(dev(np.ascontiguousarray(w[:, cl:])))
     segs = [(ap, tn.dims(n, cl, *low), 1, wa), (bp, tn.dims(n, cs, *b.shape[2:]), 0, wb)]
-    yp = tn.tn_conv3d_seg(segs, k, tn.geom(), dev(lo), dev(hi))
+    yp = run_or_skip(kernel, tn.tn_conv3d_seg, segs, k, tn.geom(), dev(lo), dev(hi))
     np.testing.assert_array_equal(u32(yp), ref)
     y = tn.tn_conv3d_seg(segs, k, tn.geom(), requant=False)
     np.testing.assert_array_equal(y.cpu().numpy(), acc.transpose(0, 2, 3, 4, 1))
@@ -256,7 +276,7 @@ def _fcn_compare(tn, x, p, per_layer=True):
 
 
 @pytest.mark.parametrize("shape", [(1, 1, 16, 16, 16), (1, 1, 32, 48, 48), (2, 1, 8, 24, 40)])
-def test_fcn_matches_oracle_small(tn, kernel, shape):
+def test_fcn_matches_oracle_small(tn, fcn_kernel, shape):
     x = synth.ct_volume(shape, seed=shape[3])
     _fcn_compare(tn, x, synth.fcn_params())
 
