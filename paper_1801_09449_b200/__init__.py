@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtn.so")
+LIB_PATH = os.environ.get("TN_LIBTN_PATH") or os.path.join(_HERE, "libtn.so")  # override: experiments only
 
 INT64_MAX = (1 << 63) - 1
 

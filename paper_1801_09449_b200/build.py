@@ -48,7 +48,12 @@ def _compile(src, extra):
     return obj
 
 
-def build_library(force: bool = False, extra=None) -> str:
+def build_library(force: bool = False, extra=None, lib_path: str = None, obj_dir: str = None) -> str:
+    global OBJ, LIB
+    if obj_dir:
+        OBJ = obj_dir
+    if lib_path:
+        LIB = lib_path
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     if force:

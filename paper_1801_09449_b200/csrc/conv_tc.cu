@@ -18,30 +18,63 @@
 // with warp shuffles (rows are TMEM lanes), so each 128-row tile yields 126
 // outputs.  Per tile: 3 planes x (3*C/32) MMAs of 128 x 3K x 32.
 //
-// CTA = 9 warps, persistent (one CTA per SM, grid = #SMs), tiles split evenly:
-//   warps 0-3  epilogue: tcgen05.ld of the accumulator (one TMEM lane quadrant
-//              each), dx combine, integer-threshold requant, packed stores
-//   warps 4-7  producers: load packed words (coalesced 8/16 B per position),
-//              expand bits -> int8 into the canonical K-major no-swizzle UMMA
-//              layout, one plane (3 dy windows) per ring slot (4 slots)
-//   warp 8     TMEM allocation + single-thread tcgen05.mma issue + commits
+// CTA = 13 warps, persistent (one CTA per SM, grid = #SMs), tiles split evenly:
+//   warps 0-7  epilogue: tcgen05.ld of the accumulator (two warps per TMEM lane
+//              quadrant, each owning half of the output channels), dx combine
+//              with warp shuffles, integer-threshold requant, packed stores
+//   warps 8-11 producers: load packed words one plane ahead into registers
+//              (coalesced 8/16 B per position), expand bits -> int8 into the
+//              canonical K-major no-swizzle UMMA layout, one plane (the 3 dy
+//              windows) per ring slot (4-8 slots, as shared memory allows)
+//   warp 12    TMEM allocation + single-thread tcgen05.mma issue + commits
 // A tile walk goes along z for fixed (n, position tile), so each input plane is
 // expanded once and used by three consecutive tiles.  The filter bank (int8,
 // 3 x 3C x 3K bytes) is expanded once per CTA and stays resident in smem.
+// Tiles are 4 runs of 32 rows (one per lane quadrant) overlapping by 2, so each
+// output's x-neighbours live in its own warp: 120 outputs per 128-row tile.
 #include "tn_internal.cuh"
 
 #include <climits>
 
+#ifndef TN_EXP_NOPROD
+#define TN_EXP_NOPROD 0
+#endif
+#ifndef TN_EXP_NOFENCE
+#define TN_EXP_NOFENCE 0
+#endif
+#ifndef TN_EXP_NOEPI
+#define TN_EXP_NOEPI 0
+#endif
+#ifndef TN_EXP_TRACE
+#define TN_EXP_TRACE 0
+#endif
+#if TN_EXP_TRACE
+__device__ long long g_trace[2048];
+#define TRACE(i, cond) do { if ((cond) && blockIdx.x == 0 && (i) < 2048) g_trace[(i)] = clock64(); } while (0)
+#else
+#define TRACE(i, cond) do { } while (0)
+#endif
+
 namespace tn {
 namespace {
 
-constexpr int kEpiWarps = 4;
-constexpr int kProdWarps = 4;
-constexpr int kThreadsTC = (kEpiWarps + kProdWarps + 1) * 32;
+constexpr int kEpiWarps = 8;             // 2 per TMEM lane quadrant (K split in halves)
+constexpr int kLoadWarps = 4;            // cp.async packed rows -> staging (one row per thread)
+constexpr int kExpWarps = 4;             // staging -> int8 UMMA layout (one row per thread)
+constexpr int kLoadWarp0 = kEpiWarps;
+constexpr int kExpWarp0 = kEpiWarps + kLoadWarps;
+constexpr int kMmaWarp = kEpiWarps + kLoadWarps + kExpWarps;
+constexpr int kThreadsTC = (kMmaWarp + 1) * 32;
+constexpr int kMaxStage = 4;
 constexpr int kRows = 128;               // UMMA M
-constexpr int kOutPerTile = kRows - 2;   // rows 1..126 are outputs
-constexpr int kSlots = 4;                // plane ring
+constexpr int kOutPerWarp = 30;          // lanes 1..30 of each 32-row run are outputs
+constexpr int kOutPerTile = 4 * kOutPerWarp;
 constexpr int kChunkBytes = kRows * 16;  // one 16-channel K-chunk of one window
+
+// Row m of a tile <-> position q0 + row_pos(m): four runs of 32 consecutive
+// positions, one per TMEM lane quadrant, overlapping by two so that every
+// output row (lanes 1..30) has both x-neighbours inside its own warp.
+__host__ __device__ __forceinline__ int row_pos(int m) { return kOutPerWarp * (m >> 5) + (m & 31) - 1; }
 
 struct TcPlan {
     int P;          // positions per padded row = Wci + 1
@@ -51,8 +84,14 @@ struct TcPlan {
     int cch[2];     // 16-channel chunks per segment
     int cch_tot;    // chunks per window (all segments)
     int nchp;       // chunks per plane slot: 3 * cch_tot rounded up to even
+    int nslot;      // plane ring depth (4..8)
+    int nstage;     // packed staging depth (2..4)
+    int stage_bytes;
+    int nacc;       // TMEM accumulator buffers (2..4)
     int ring_bytes, w_bytes;
 };
+constexpr int kMaxSlots = 8;
+constexpr int kMaxAcc = 4;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,6 +143,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // UMMA shared-memory descriptor, K-major, no swizzle (canonical "interleave"
 // layout: 8-row x 16-byte core matrices; rows 16 B apart, 8-row groups SBO
 // apart, the two 16-byte K halves of a K=32 instruction LBO apart).
@@ -152,41 +201,116 @@ struct Walk {
     }
 };
 
-template <int K>
+// Producer-side walk over the planes a CTA expands, in order: for each run of
+// tiles (z in [zf, zl]) the planes zf-1 .. zl+1.  Per run it caches each row's
+// (y, x) offsets in the three dy windows (per segment).
+struct PlaneCursor {
+    Walk wk;
+    int n, tq, zf, zl, zp;
+    bool valid;
+    int yx[3][kMaxSeg];
+    bool ok[3];
+    __device__ PlaneCursor(const TcPlan& pl, const ConvDesc& cd, int m) : wk(pl.T, cd.Do, pl.NQ) {
+        valid = wk.next(n, tq, zf, zl);
+        if (valid) start_run(pl, cd, m);
+    }
+    __device__ void start_run(const TcPlan& pl, const ConvDesc& cd, int m) {
+        zp = zf - 1;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+            const int p = tq * kOutPerTile + row_pos(m) + (dy - 1) * pl.P;
+            const int y = p >= 0 ? p / pl.P : -1;
+            const int x = p - y * pl.P;
+            ok[dy] = p >= 0 && y < cd.Hci && x < cd.Wci;
+#pragma unroll
+            for (int sg = 0; sg < kMaxSeg; ++sg) {
+                const SegDesc& sd = cd.seg[sg];
+                const int ys = sd.up ? (y >> 1) : y, xs = sd.up ? (x >> 1) : x;
+                yx[dy][sg] = ys * sd.W + xs;
+            }
+        }
+    }
+    __device__ void advance(const TcPlan& pl, const ConvDesc& cd, int m) {
+        if (++zp > zl + 1) {
+            valid = wk.next(n, tq, zf, zl);
+            if (valid) start_run(pl, cd, m);
+        }
+    }
+};
+
+// One row's packed words of one plane: [segment][dy] x (sign0, sign1, mask0, mask1).
+template <int NSEG>
+struct PlaneWords { uint4 w[NSEG][3]; };
+
+template <int NSEG>
+__device__ __forceinline__ void load_plane(const ConvDesc& cd, const PlaneCursor& c, PlaneWords<NSEG>& pw) {
+    const int zg = cd.zo_beg + c.zp;    // global conv-input plane
+    const bool zin = zg >= 0 && zg < cd.Dci;
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg) {
+        const SegDesc& sd = cd.seg[sg];
+        const int zs = (sd.up ? (zg >> 1) : zg) - sd.zbeg;
+        const bool zok = zin && zs >= 0 && zs < sd.D;
+        const int64_t pbase = (static_cast<int64_t>(c.n) * sd.D + zs) * sd.H * sd.W;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (zok && c.ok[dy]) {
+                const uint32_t* src = sd.xp + (pbase + c.yx[dy][sg]) * 2 * sd.cw;
+                if (sd.cw == 1) {
+                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(src));
+                    v = make_uint4(q.x, 0u, q.y, 0u);
+                } else {
+                    v = __ldg(reinterpret_cast<const uint4*>(src));
+                }
+            }
+            pw.w[sg][dy] = v;
+        }
+    }
+}
+
+template <int K, int NSEG, int CT>
 __global__ void __launch_bounds__(kThreadsTC, 1)
 conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     constexpr int N = 3 * K;
-    constexpr int KC = K / 16;
+    constexpr int NCHP = (3 * CT + 1) & ~1;   // chunks per plane slot (== NCHP)
+    constexpr int HALF = NCHP / 2;            // K=32 MMAs per plane
+    constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_ring = smem;                                   // [slot][chunk][128][16]
     uint8_t* s_w = smem + pl.ring_bytes;                      // [dz][chunk][N][16]
-    int* s_x = reinterpret_cast<int*>(s_w + pl.w_bytes);      // [2][4][2][16] boundary rows
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_x + 2 * 4 * 2 * 16);
-    uint64_t* plane_full = bars;           // [4]
-    uint64_t* slot_free = bars + 4;        // [4]
-    uint64_t* acc_full = bars + 8;         // [2]
-    uint64_t* acc_empty = bars + 10;       // [2]
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 12);
+    uint8_t* s_stage = s_w + pl.w_bytes;                      // [stage][seg][dy][128][16] packed rows
+    int* s_lo = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes);  // [K]
+    int* s_hi = s_lo + K;                                     // [K]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_hi + K);
+    uint64_t* plane_full = bars;                           // [kMaxSlots]
+    uint64_t* slot_free = bars + kMaxSlots;                // [kMaxSlots]
+    uint64_t* acc_full = bars + 2 * kMaxSlots;             // [kMaxAcc]
+    uint64_t* acc_empty = bars + 2 * kMaxSlots + kMaxAcc;  // [kMaxAcc]
+    uint64_t* staged_full = bars + 2 * kMaxSlots + 2 * kMaxAcc;           // [kMaxStage]
+    uint64_t* staged_empty = staged_full + kMaxStage;                      // [kMaxStage]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(staged_empty + kMaxStage);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int slot_bytes = pl.nchp * kChunkBytes;
-    const int wdz_bytes = pl.nchp * N * 16;
+    constexpr int slot_bytes = NCHP * kChunkBytes;
+    constexpr int wdz_bytes = NCHP * N * 16;
+    const bool fused = cd.yp != nullptr;
 
     // ---- one-time setup: zero the ring (padding chunks stay zero), expand the
-    // packed filter bank into the B-operand image, init barriers, alloc TMEM.
+    // packed filter bank into the B-operand image, thresholds, barriers, TMEM.
     for (int i = threadIdx.x; i < pl.ring_bytes / 16; i += kThreadsTC)
         reinterpret_cast<uint4*>(s_ring)[i] = make_uint4(0u, 0u, 0u, 0u);
     {
-        const int units = 3 * pl.nchp * N;  // 16-byte units (dz, chunk, n)
+        const int units = 3 * NCHP * N;  // 16-byte units (dz, chunk, n)
         for (int u = threadIdx.x; u < units; u += kThreadsTC) {
             const int nrow = u % N;
-            const int ch = (u / N) % pl.nchp;
-            const int dz = u / (N * pl.nchp);
+            const int ch = (u / N) % NCHP;
+            const int dz = u / (N * NCHP);
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (ch < 3 * pl.cch_tot) {
-                const int dy = ch / pl.cch_tot;
-                int j = ch - dy * pl.cch_tot;
+            if (ch < 3 * CT) {
+                const int dy = ch / CT;
+                int j = ch - dy * CT;
                 const int sg = (j >= pl.cch[0]) ? 1 : 0;
                 if (sg) j -= pl.cch[0];
                 const int dx = nrow / K, k = nrow - dx * K;
@@ -199,13 +323,18 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
             *reinterpret_cast<uint4*>(s_w + dz * wdz_bytes + ch * (N * 16) + nrow * 16) = v;
         }
     }
+    if (fused) {
+        for (int k = threadIdx.x; k < K; k += kThreadsTC) { s_lo[k] = __ldg(cd.lo + k); s_hi[k] = __ldg(cd.hi + k); }
+    }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) { mbar_init(plane_full + i, kProdWarps * 32); mbar_init(slot_free + i, 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, kEpiWarps * 32); }
+        for (int i = 0; i < kMaxSlots; ++i) { mbar_init(plane_full + i, kExpWarps * 32); mbar_init(slot_free + i, 1); }
+        for (int i = 0; i < kMaxStage; ++i) { mbar_init(staged_full + i, kLoadWarps * 32); mbar_init(staged_empty + i, kExpWarps * 32); }
+        for (int i = 0; i < kMaxAcc; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, kEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    constexpr uint32_t kTmemCols = (2 * N <= 128) ? 128 : (2 * N <= 256 ? 256 : 512);
-    if (warp == 8) {
+    constexpr int kAccMax = (512 / N) < kMaxAcc ? (512 / N) : kMaxAcc;   // == pl.nacc
+    constexpr uint32_t kTmemCols = (kAccMax * N <= 128) ? 128 : (kAccMax * N <= 256 ? 256 : 512);
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -216,158 +345,211 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     tc_fence_after();
     const uint32_t tmem_base = *s_tmem;
 
-    if (warp >= kEpiWarps && warp < kEpiWarps + kProdWarps) {
-        // ================= producers: expand one plane (3 dy windows) per slot
-        const int m = threadIdx.x - kEpiWarps * 32;    // row 0..127
+    uint32_t total_planes = 0;
+    if (warp >= kLoadWarp0 && warp < kMmaWarp) {
         Walk wk(pl.T, cd.Do, pl.NQ);
         int n, tq, zf, zl;
-        uint32_t g = 0;
-        while (wk.next(n, tq, zf, zl)) {
-            const int q0 = tq * kOutPerTile - 1;
-            for (int zp = zf - 1; zp <= zl + 1; ++zp, ++g) {
-                const int s = g & 3;
-                if (g >= 4) mbar_wait(slot_free + s, ((g >> 2) - 1) & 1);
-                uint8_t* slot = s_ring + s * slot_bytes;
-                const int zg = cd.zo_beg + zp;    // global conv-input plane
-                const bool zin = zg >= 0 && zg < cd.Dci;
+        while (wk.next(n, tq, zf, zl)) total_planes += (zl - zf) + 3;
+    }
+    if (warp >= kLoadWarp0 && warp < kExpWarp0) {
+        // ================= loaders: cp.async each row's packed words of one plane
+        // (3 dy windows x segments) into a staging slot; zero-fill outside the
+        // volume.  Completion is signalled on staged_full by the async unit, so
+        // these threads never stall on the loads and run up to nstage planes ahead.
+        const int m = threadIdx.x - kLoadWarp0 * 32;
+        PlaneCursor cur(pl, cd, m);
+        for (uint32_t g = 0; g < total_planes; ++g) {
+            const uint32_t st = g % pl.nstage;
+            if (g >= static_cast<uint32_t>(pl.nstage)) mbar_wait(staged_empty + st, ((g / pl.nstage) - 1) & 1);
+            const int zg = cd.zo_beg + cur.zp;
+            const bool zin = zg >= 0 && zg < cd.Dci;
+#pragma unroll
+            for (int sg = 0; sg < NSEG; ++sg) {
+                const SegDesc& sd = cd.seg[sg];
+                const int zs = (sd.up ? (zg >> 1) : zg) - sd.zbeg;
+                const bool zok = zin && zs >= 0 && zs < sd.D;
+                const int64_t pbase = (static_cast<int64_t>(cur.n) * sd.D + zs) * sd.H * sd.W;
 #pragma unroll
                 for (int dy = 0; dy < 3; ++dy) {
-                    const int p = q0 + (dy - 1) * pl.P + m;
-                    const int y = p >= 0 ? p / pl.P : -1;
-                    const int x = p - y * pl.P;
-                    const bool in = zin && p >= 0 && y < cd.Hci && x < cd.Wci;
-                    int choff = dy * pl.cch_tot;
-                    for (int sg = 0; sg < cd.nseg; ++sg) {
-                        const SegDesc& sd = cd.seg[sg];
-                        uint32_t sw[2] = {0u, 0u}, mw[2] = {0u, 0u};
-                        if (in) {
-                            int zs = zg, ys = y, xs = x;
-                            if (sd.up) { zs >>= 1; ys >>= 1; xs >>= 1; }
-                            zs -= sd.zbeg;
-                            if (zs >= 0 && zs < sd.D) {
-                                const uint32_t* src =
-                                    sd.xp + (((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ys) * sd.W + xs) * 2 * sd.cw;
-                                if (sd.cw == 1) {
-                                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(src));
-                                    sw[0] = q.x; mw[0] = q.y;
-                                } else {
-                                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(src));
-                                    sw[0] = q.x; sw[1] = q.y; mw[0] = q.z; mw[1] = q.w;
-                                }
-                            }
-                        }
-                        for (int j = 0; j < pl.cch[sg]; ++j) {
-                            const int word = j >> 1, sh = (j & 1) * 16;
-                            const uint4 v = expand16(word ? sw[1] : sw[0], word ? mw[1] : mw[0], sh);
-                            *reinterpret_cast<uint4*>(slot + (choff + j) * kChunkBytes + m * 16) = v;
-                        }
-                        choff += pl.cch[sg];
-                    }
+                    const bool ok = zok && cur.ok[dy];
+                    const uint32_t* src = ok ? sd.xp + (pbase + cur.yx[dy][sg]) * 2 * sd.cw : sd.xp;
+                    const uint32_t dst = smem_u32(s_stage + st * pl.stage_bytes + ((sg * 3 + dy) * kRows + m) * 16);
+                    if (sd.cw == 1)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                                     "r"(ok ? 8 : 0) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                                     "r"(ok ? 16 : 0) : "memory");
                 }
-                fence_proxy_async();
-                mbar_arrive(plane_full + s);
             }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(staged_full + st))
+                         : "memory");
+            cur.advance(pl, cd, m);
         }
-    } else if (warp == 8) {
-        // ================= MMA issuer (one thread)
-        if (lane == 0) {
-            const uint32_t idesc = idesc_i8(N);
-            const uint32_t ring_a = smem_u32(s_ring), w_a = smem_u32(s_w);
-            Walk wk(pl.T, cd.Do, pl.NQ);
-            int n, tq, zf, zl;
-            uint32_t gbase = 0, tc = 0;
-            while (wk.next(n, tq, zf, zl)) {
-                for (int z = zf; z <= zl; ++z, ++tc) {
-                    const uint32_t a = gbase + (z - zf);
-                    for (int dz = 0; dz < 3; ++dz) mbar_wait(plane_full + ((a + dz) & 3), ((a + dz) >> 2) & 1);
-                    const uint32_t buf = tc & 1;
-                    if (tc >= 2) mbar_wait(acc_empty + buf, ((tc >> 1) - 1) & 1);
-                    tc_fence_after();
+    } else if (warp >= kExpWarp0 && warp < kMmaWarp) {
+        // ================= expanders: staging (packed) -> ring slot (int8, UMMA
+        // K-major no-swizzle layout), then the generic->async proxy fence.  These
+        // threads have no global loads in flight, so the fence is cheap.
+        const int m = threadIdx.x - kExpWarp0 * 32;
+        const uint32_t S = pl.nslot;
+        for (uint32_t g = 0; g < total_planes; ++g) {
+            const uint32_t st = g % pl.nstage;
+            mbar_wait(staged_full + st, (g / pl.nstage) & 1);
+            uint4 v[NSEG][3];
+#pragma unroll
+            for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+                for (int dy = 0; dy < 3; ++dy)
+                    v[sg][dy] = *reinterpret_cast<const uint4*>(s_stage + st * pl.stage_bytes +
+                                                                ((sg * 3 + dy) * kRows + m) * 16);
+            mbar_arrive(staged_empty + st);
+            const uint32_t sl = g % S;
+            TRACE(600 + 2 * g, g < 64 && m == 0);
+            if (g >= S) mbar_wait(slot_free + sl, ((g / S) - 1) & 1);
+            TRACE(601 + 2 * g, g < 64 && m == 0);
+            uint8_t* slot = s_ring + sl * slot_bytes + m * 16;
+#if TN_EXP_NOPROD
+            if (v[0][0].x == 0x12345u)
+#endif
+#pragma unroll
+            for (int sg = 0; sg < NSEG; ++sg) {
+                const int choff = sg ? pl.cch[0] : 0;
+                const int cch = pl.cch[sg];
+                const bool two = cd.seg[sg].cw == 2;
+#pragma unroll
+                for (int dy = 0; dy < 3; ++dy) {
+                    const uint4 q = v[sg][dy];
+                    const uint32_t s0 = q.x, m0 = two ? q.z : q.y, s1 = q.y, m1 = q.w;
+                    uint8_t* dst = slot + (dy * CT + choff) * kChunkBytes;
+                    *reinterpret_cast<uint4*>(dst) = expand16(s0, m0, 0);
+                    if (cch > 1) *reinterpret_cast<uint4*>(dst + kChunkBytes) = expand16(s0, m0, 16);
+                    if (cch > 2) *reinterpret_cast<uint4*>(dst + 2 * kChunkBytes) = expand16(s1, m1, 0);
+                    if (cch > 3) *reinterpret_cast<uint4*>(dst + 3 * kChunkBytes) = expand16(s1, m1, 16);
+                }
+            }
+            fence_proxy_async();
+            mbar_arrive(plane_full + sl);
+            TRACE(800 + g, g < 64 && m == 0);
+        }
+    } else if (warp == kMmaWarp) {
+        // ================= MMA issuer: the whole warp walks the schedule (so
+        // descriptors stay warp-uniform, in uniform registers) and one elected
+        // lane issues each tcgen05.mma / tcgen05.commit.
+        const uint32_t idesc = idesc_i8(N);
+        const uint64_t adesc0 = umma_desc(smem_u32(s_ring), kChunkBytes, 128);
+        const uint64_t bdesc0 = umma_desc(smem_u32(s_w), N * 16, 128);
+        const bool leader = elect_one();
+        Walk wk(pl.T, cd.Do, pl.NQ);
+        int n, tq, zf, zl;
+        const uint32_t S = pl.nslot, A = pl.nacc;
+        const uint64_t aslot = static_cast<uint64_t>(slot_bytes >> 4);   // descriptor step per ring slot
+        // Incremental ring / accumulator bookkeeping (no divisions in the loop):
+        // plane a (first plane of the current tile) lives in slot sa with phase pa.
+        uint32_t sa = 0, pa = 0, buf = 0, round = 0, tc = 0;
+        auto next_slot = [S](uint32_t sl, uint32_t ph, uint32_t& sl2, uint32_t& ph2) {
+            sl2 = sl + 1;
+            ph2 = ph;
+            if (sl2 == S) { sl2 = 0; ph2 ^= 1u; }
+        };
+        while (wk.next(n, tq, zf, zl)) {
+            for (int z = zf; z <= zl; ++z, ++tc) {
+                uint32_t s1, p1, s2, p2;
+                next_slot(sa, pa, s1, p1);
+                next_slot(s1, p1, s2, p2);
+                TRACE(5 * tc + 0, tc < 64 && leader);
+                if (round > 0) mbar_wait(acc_empty + buf, (round - 1) & 1);
+                TRACE(5 * tc + 1, tc < 64 && leader);
+                // planes a, a+1 were already seen complete by the previous tile of
+                // this run; only the newest one needs a wait (all three at run start)
+                if (z == zf) {
+                    mbar_wait(plane_full + sa, pa);
+                    mbar_wait(plane_full + s1, p1);
+                }
+                mbar_wait(plane_full + s2, p2);
+                TRACE(5 * tc + 2, tc < 64 && leader);
+                tc_fence_after();
+                if (leader) {
                     const uint32_t d = tmem_base + buf * N;
-                    uint32_t acc = 0;
+#pragma unroll
                     for (int dz = 0; dz < 3; ++dz) {
-                        const uint32_t sa = ring_a + ((a + dz) & 3) * slot_bytes;
-                        const uint32_t sb = w_a + dz * wdz_bytes;
-                        for (int j = 0; j < pl.nchp / 2; ++j) {
-                            const uint64_t ad = umma_desc(sa + 2 * j * kChunkBytes, kChunkBytes, 128);
-                            const uint64_t bd = umma_desc(sb + 2 * j * N * 16, N * 16, 128);
-                            tc_mma_i8(d, ad, bd, idesc, acc);
-                            acc = 1;
-                        }
+                        const uint32_t sl = dz == 0 ? sa : (dz == 1 ? s1 : s2);
+                        const uint64_t ad = adesc0 + sl * aslot;
+                        const uint64_t bd = bdesc0 + static_cast<uint64_t>((dz * wdz_bytes) >> 4);
+#pragma unroll
+                        for (int j = 0; j < HALF; ++j)
+                            tc_mma_i8(d, ad + static_cast<uint64_t>((2 * j * kChunkBytes) >> 4),
+                                      bd + static_cast<uint64_t>((2 * j * N * 16) >> 4), idesc, (dz | j) != 0);
                     }
                     tc_commit(acc_full + buf);
-                    tc_commit(slot_free + (a & 3));
+                    tc_commit(slot_free + sa);
                     if (z == zl) {
-                        tc_commit(slot_free + ((a + 1) & 3));
-                        tc_commit(slot_free + ((a + 2) & 3));
+                        tc_commit(slot_free + s1);
+                        tc_commit(slot_free + s2);
                     }
                 }
-                gbase += (zl - zf) + 3;
+                __syncwarp();
+                TRACE(320 + tc, tc < 64 && leader);
+                sa = s1;
+                pa = p1;
+                if (++buf == A) { buf = 0; ++round; }
             }
+            // the run's last two planes (a+1, a+2 of its last tile) are done too
+            uint32_t t1, q1;
+            next_slot(sa, pa, t1, q1);
+            next_slot(t1, q1, sa, pa);
         }
-        __syncwarp();
     } else {
-        // ================= epilogue: warps 0-3, row m = 32*warp + lane
-        const int q = warp;
-        const int m = 32 * q + lane;
-        const bool fused = cd.yp != nullptr;
+        // ================= epilogue: warps 0-7; lane quadrant q, K half h
+        const int q = warp & 3;
+        const int h = warp >> 2;
+        // chunks of 16 output channels handled by this warp (at most 2 = one word)
+        const int kc0 = (K > 32) ? 2 * h : 0;
+        const bool active = (K > 32) || h == 0;
+        const int word = (K > 32) ? h : 0;
         Walk wk(pl.T, cd.Do, pl.NQ);
         int n, tq, zf, zl;
         uint32_t tc = 0;
-        int par = 0;
         while (wk.next(n, tq, zf, zl)) {
-            const int q0 = tq * kOutPerTile - 1;
-            const int p = q0 + m;
+            const int p = tq * kOutPerTile + row_pos(32 * q + lane);
             const int y = p >= 0 ? p / pl.P : 0;
             const int x = p - y * pl.P;
-            const bool vrow = m >= 1 && m <= kOutPerTile && p < pl.NP && x < cd.Wo && y < cd.Ho;
+            const bool vrow = active && lane >= 1 && lane <= kOutPerWarp && p < pl.NP && x < cd.Wo && y < cd.Ho;
             for (int z = zf; z <= zl; ++z, ++tc) {
-                const uint32_t buf = tc & 1;
-                mbar_wait(acc_full + buf, (tc >> 1) & 1);
+                const uint32_t buf = tc % static_cast<uint32_t>(pl.nacc);
+                mbar_wait(acc_full + buf, (tc / static_cast<uint32_t>(pl.nacc)) & 1);
+                TRACE(400 + tc, tc < 64 && threadIdx.x == 1);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + buf * N;
-                uint32_t osw[(K + 31) / 32], omw[(K + 31) / 32];
-#pragma unroll
-                for (int i = 0; i < (K + 31) / 32; ++i) { osw[i] = 0u; omw[i] = 0u; }
                 const int64_t vox = ((static_cast<int64_t>(n) * cd.Do + z) * cd.Ho + y) * cd.Wo + x;
+                uint32_t sbits = 0u, mbits = 0u;
 #pragma unroll
-                for (int kc = 0; kc < KC; ++kc) {
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int kc = kc0 + cc;
+                    if (!active || 16 * kc >= K) break;
+#if TN_EXP_NOEPI
+                    if (tc != 0xFFFFFFFFu) break;
+#endif
                     int d0[16], d1[16], d2[16];
                     tmem_ld16(taddr + 0 * K + 16 * kc, d0);
                     tmem_ld16(taddr + 1 * K + 16 * kc, d1);
                     tmem_ld16(taddr + 2 * K + 16 * kc, d2);
                     tmem_wait_ld();
-                    int* xb = s_x + par * (4 * 2 * 16);
-                    if (lane == 31) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) xb[(q * 2 + 0) * 16 + i] = d0[i];
-                    }
-                    if (lane == 0) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) xb[(q * 2 + 1) * 16 + i] = d2[i];
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
                     int accv[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        int up = __shfl_up_sync(0xFFFFFFFFu, d0[i], 1);
-                        int dn = __shfl_down_sync(0xFFFFFFFFu, d2[i], 1);
-                        if (lane == 0) up = q > 0 ? xb[((q - 1) * 2 + 0) * 16 + i] : 0;
-                        if (lane == 31) dn = q < 3 ? xb[((q + 1) * 2 + 1) * 16 + i] : 0;
-                        accv[i] = up + d1[i] + dn;
-                    }
-                    par ^= 1;
+                    for (int i = 0; i < 16; ++i)
+                        accv[i] = __shfl_up_sync(0xFFFFFFFFu, d0[i], 1) + d1[i] +
+                                  __shfl_down_sync(0xFFFFFFFFu, d2[i], 1);
                     if (fused) {
                         // A4 (reading R5): +1 if acc >= hi; else -1 if acc <= lo; else 0
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int k = 16 * kc + i;
-                            const bool pos = accv[i] >= __ldg(cd.hi + k);
-                            const bool neg = !pos && accv[i] <= __ldg(cd.lo + k);
-                            osw[k >> 5] |= (pos ? 1u : 0u) << (k & 31);
-                            omw[k >> 5] |= ((pos || neg) ? 1u : 0u) << (k & 31);
+                            const uint32_t pos = accv[i] >= s_hi[k];
+                            const uint32_t nz = pos | static_cast<uint32_t>(accv[i] <= s_lo[k]);
+                            sbits |= pos << (16 * cc + i);
+                            mbits |= nz << (16 * cc + i);
                         }
-                    } else if (vrow && z < cd.Do) {
+                    } else if (vrow) {
                         int4* dst = reinterpret_cast<int4*>(cd.y + vox * K + 16 * kc);
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
@@ -376,12 +558,14 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                 }
                 tc_fence_before();
                 mbar_arrive(acc_empty + buf);
+                TRACE(500 + tc, tc < 64 && threadIdx.x == 1);
                 if (fused && vrow) {
-                    uint32_t* dst = cd.yp + vox * 2 * ((K + 31) / 32);
-                    if constexpr (K <= 32) {
-                        *reinterpret_cast<uint2*>(dst) = make_uint2(osw[0], omw[0]);
+                    uint32_t* dst = cd.yp + vox * 2 * CWO;
+                    if constexpr (CWO == 1) {
+                        *reinterpret_cast<uint2*>(dst) = make_uint2(sbits, mbits);
                     } else {
-                        *reinterpret_cast<uint4*>(dst) = make_uint4(osw[0], osw[1], omw[0], omw[1]);
+                        dst[word] = sbits;
+                        dst[CWO + word] = mbits;
                     }
                 }
             }
@@ -390,7 +574,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
     }
@@ -404,7 +588,7 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     if (cd.nseg < 1 || cd.nseg > 2) return false;
     for (int a = 0; a < 3; ++a)
         if (cd.s[a] != 1 || cd.p[a] != 1 || cd.dl[a] != 1) return false;
-    if (cd.K != 16 && cd.K != 32 && cd.K != 48 && cd.K != 64) return false;
+    if (cd.K != 16 && cd.K != 32 && cd.K != 64) return false;
     pl.cch_tot = 0;
     pl.cch[1] = 0;
     for (int i = 0; i < cd.nseg; ++i) {
@@ -422,26 +606,86 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     pl.NP = static_cast<int>(np);
     pl.NQ = (pl.NP + kOutPerTile - 1) / kOutPerTile;
     pl.T = static_cast<int64_t>(cd.N) * pl.NQ * cd.Do;
-    pl.ring_bytes = kSlots * pl.nchp * kChunkBytes;
     pl.w_bytes = 3 * pl.nchp * 3 * cd.K * 16;
+    pl.nacc = (512 / (3 * cd.K)) < kMaxAcc ? (512 / (3 * cd.K)) : kMaxAcc;
+    const int slot_bytes = pl.nchp * kChunkBytes;
+    const int fixed = pl.w_bytes + 2 * cd.K * 4 + (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 64;
+    pl.stage_bytes = cd.nseg * 3 * kRows * 16;
+    pl.nslot = kMaxSlots;
+    pl.nstage = kMaxStage;
+    while (fixed + pl.nslot * slot_bytes + pl.nstage * pl.stage_bytes > 225 * 1024) {
+        if (pl.nslot > 4) --pl.nslot;
+        else if (pl.nstage > 2) --pl.nstage;
+        else break;
+    }
+    pl.ring_bytes = pl.nslot * slot_bytes;
     if (cd.Do != cd.Dci || cd.Ho != cd.Hci || cd.Wo != cd.Wci) return false;
     return true;
 }
 
-static size_t smem_bytes(const TcPlan& pl) {
-    return static_cast<size_t>(pl.ring_bytes) + pl.w_bytes + 2 * 4 * 2 * 16 * sizeof(int) + 12 * 8 + 16;
+// Launched as (trivial) 1-CTA clusters: st.async addresses shared::cluster.
+static cudaError_t launch_one(void (*kern)(ConvDesc, TcPlan), const ConvDesc& cd, const TcPlan& pl, int64_t grid,
+                              size_t smem, cudaStream_t st) {
+    // cudaFuncSetAttribute is a slow host call: raise the kernel's smem limit once
+    // to the maximum instead of per launch.
+    static void* configured[32] = {nullptr};
+    bool done = false;
+    for (void* f : configured) done = done || f == reinterpret_cast<void*>(kern);
+    if (!done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        for (void*& f : configured)
+            if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreadsTC);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 0;   // plain launch (no cluster needed)
+    return cudaLaunchKernelEx(&cfg, kern, cd, pl);
+}
+
+template <int K>
+static cudaError_t dispatch_ct(const ConvDesc& cd, const TcPlan& pl, int64_t grid, size_t smem, cudaStream_t st) {
+    if (cd.nseg == 1) {
+        switch (pl.cch_tot) {
+            case 1: return launch_one(conv_tc_kernel<K, 1, 1>, cd, pl, grid, smem, st);
+            case 2: return launch_one(conv_tc_kernel<K, 1, 2>, cd, pl, grid, smem, st);
+            case 3: return launch_one(conv_tc_kernel<K, 1, 3>, cd, pl, grid, smem, st);
+            case 4: return launch_one(conv_tc_kernel<K, 1, 4>, cd, pl, grid, smem, st);
+        }
+    } else {
+        switch (pl.cch_tot) {
+            case 2: return launch_one(conv_tc_kernel<K, 2, 2>, cd, pl, grid, smem, st);
+            case 3: return launch_one(conv_tc_kernel<K, 2, 3>, cd, pl, grid, smem, st);
+            case 4: return launch_one(conv_tc_kernel<K, 2, 4>, cd, pl, grid, smem, st);
+        }
+    }
+    return cudaErrorNotSupported;
+}
+
+static size_t smem_bytes(const TcPlan& pl, int K) {
+    return static_cast<size_t>(pl.ring_bytes) + pl.w_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
+           2 * K * sizeof(int) + (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 16;
 }
 
 bool conv_tc_supported(const ConvDesc& cd) {
     TcPlan pl{};
     if (!plan_full(cd, pl)) return false;
-    return smem_bytes(pl) <= 227 * 1024 && pl.T > 0;
+    return smem_bytes(pl, cd.K) <= 227 * 1024 && pl.T > 0;
 }
 
 cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t st) {
     TcPlan pl{};
     if (!plan_full(cd, pl)) return cudaErrorNotSupported;
-    const size_t smem = smem_bytes(pl);
+    const size_t smem = smem_bytes(pl, cd.K);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     if (g_num_sms == 0) {
         int dev = 0;
@@ -451,22 +695,20 @@ cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t st) {
     const int64_t grid = pl.T < g_num_sms ? pl.T : g_num_sms;
     if (grid <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-#define TN_TC_CASE(KV)                                                                                  \
-    case KV:                                                                                            \
-        e = cudaFuncSetAttribute(conv_tc_kernel<KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                 static_cast<int>(smem));                                               \
-        if (e != cudaSuccess) return e;                                                                 \
-        conv_tc_kernel<KV><<<static_cast<unsigned>(grid), kThreadsTC, smem, st>>>(cd, pl);               \
-        break;
     switch (cd.K) {
-        TN_TC_CASE(16)
-        TN_TC_CASE(32)
-        TN_TC_CASE(48)
-        TN_TC_CASE(64)
+        case 16: e = dispatch_ct<16>(cd, pl, grid, smem, st); break;
+        case 32: e = dispatch_ct<32>(cd, pl, grid, smem, st); break;
+        case 64: e = dispatch_ct<64>(cd, pl, grid, smem, st); break;
         default: return cudaErrorNotSupported;
     }
-#undef TN_TC_CASE
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 }  // namespace tn
+
+#if TN_EXP_TRACE
+extern "C" int tn_exp_trace(long long* host, int n) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n));
+}
+#endif
