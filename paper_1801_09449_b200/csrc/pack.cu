@@ -148,15 +148,15 @@ pack_generic_kernel(const T* __restrict__ x, int C, int cw, int64_t DHW, int64_t
 }
 
 // ----------------------------------------------------------------------------
-// int8 fast path: 16 voxels per thread (one 16-byte load per channel), SWAR
-// classification of 4 voxels per 32-bit word.  For a word q of 4 int8 codes:
+// int8 fast path: 4 voxels per thread (one 32-bit load per channel), SWAR
+// classification of the 4 voxels in one 32-bit word.  For a word q of 4 int8 codes:
 //   lsb  = q & 0x01010101              (nonzero bit of each byte: 0x01, 0xFF -> 1)
 //   t7   = (q >> 7) & 0x01010101       (bit 7 of each byte)
 //   pos  = lsb & ~t7                   (+1 <=> byte == 0x01)
 // and the byte is a valid code iff bits 1..7 all equal bit 7 and (bit 7 => lsb).
 // Bits of 8 consecutive channels accumulate per byte lane (acc += bit << j),
 // so byte i of acc holds voxel i's 8 channel bits; a 4x4 byte transpose (PRMT)
-// then forms each voxel's 32-channel word.
+// of the four 8-channel groups then forms each voxel's 32-channel word.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                              uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
@@ -172,7 +172,9 @@ template <int CW>
 __global__ void __launch_bounds__(kThreads)
 pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t total,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
-    constexpr int VPT = 16;
+    // 4 voxels per thread: one 32-bit load per channel (a warp reads 128
+    // contiguous bytes per channel), 16 channel loads in flight per thread.
+    constexpr int VPT = 4;
     const int64_t g0 = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) * VPT;
     if (g0 >= total) return;
     const int64_t n = g0 / DHW;
@@ -182,21 +184,21 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
     uint32_t bad = 0;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
-        uint32_t accS[4][4], accM[4][4];   // [quad][group of 8 channels]
+        uint32_t accS[4], accM[4];   // [group of 8 channels]
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            uint4 q[8];
+        for (int gh = 0; gh < 2; ++gh) {
+            uint32_t q[16];
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int c = 32 * j + 8 * g + jj;
-                q[jj] = c < C ? __ldg(reinterpret_cast<const uint4*>(xb + c * DHW)) : make_uint4(0u, 0u, 0u, 0u);
+            for (int jj = 0; jj < 16; ++jj) {
+                const int c = 32 * j + 16 * gh + jj;
+                q[jj] = c < C ? __ldg(reinterpret_cast<const uint32_t*>(xb + c * DHW)) : 0u;
             }
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) {
+            for (int g2 = 0; g2 < 2; ++g2) {
                 uint32_t as = 0u, am = 0u;
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                    const uint32_t w = qd == 0 ? q[jj].x : qd == 1 ? q[jj].y : qd == 2 ? q[jj].z : q[jj].w;
+                    const uint32_t w = q[8 * g2 + jj];
                     const uint32_t lsb = w & 0x01010101u;
                     const uint32_t t7 = (w >> 7) & 0x01010101u;
                     const uint32_t pos = lsb & ~t7;
@@ -204,17 +206,12 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
                     am += lsb << jj;
                     as += pos << jj;
                 }
-                accS[qd][g] = as;
-                accM[qd][g] = am;
+                accS[2 * gh + g2] = as;
+                accM[2 * gh + g2] = am;
             }
         }
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-            transpose4x4(accS[qd][0], accS[qd][1], accS[qd][2], accS[qd][3],
-                         os[4 * qd][j], os[4 * qd + 1][j], os[4 * qd + 2][j], os[4 * qd + 3][j]);
-            transpose4x4(accM[qd][0], accM[qd][1], accM[qd][2], accM[qd][3],
-                         om[4 * qd][j], om[4 * qd + 1][j], om[4 * qd + 2][j], om[4 * qd + 3][j]);
-        }
+        transpose4x4(accS[0], accS[1], accS[2], accS[3], os[0][j], os[1][j], os[2][j], os[3][j]);
+        transpose4x4(accM[0], accM[1], accM[2], accM[3], om[0][j], om[1][j], om[2][j], om[3][j]);
     }
     if (bad != 0u) {
         // rare slow path: find this thread's first offending NCDHW index exactly
@@ -386,9 +383,9 @@ cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d
     const int64_t DHW = static_cast<int64_t>(xd.d) * xd.h * xd.w;
     const int64_t total = DHW * xd.n;
     const int cw = (xd.c + 31) / 32;
-    if (total > 0 && DHW % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
+    if (total > 0 && DHW % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
         (cw == 1 || cw == 2 || cw == 4)) {
-        const int64_t nt = total / 16;
+        const int64_t nt = total / 4;
         const unsigned blocks = static_cast<unsigned>((nt + kThreads - 1) / kThreads);
         if (cw == 1) pack_i8_swar_kernel<1><<<blocks, kThreads, 0, s>>>(x, xd.c, DHW, total, xp, d_bad);
         else if (cw == 2) pack_i8_swar_kernel<2><<<blocks, kThreads, 0, s>>>(x, xd.c, DHW, total, xp, d_bad);
