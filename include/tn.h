@@ -171,6 +171,44 @@ void      tn_fcn_destroy(tn_fcn* net);
 const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* ws, int32_t i,
                                     tn_dims* out_dims /*host*/);
 
+/* ---- Multi-GPU: z-slab decomposition of one volume (BASELINE configs[4]) ----
+ * Rank r of nranks owns input planes [z0, z1) (multiples of the FCN's total
+ * downsampling, 8 for the Table-1 analogue; ranks in z order).  Every layer's
+ * packed output is kept with one halo plane per side, exchanged after the
+ * layer with ranks r-1 / r+1 by NCCL send/recv on `stream` (NVLink through
+ * NVSwitch); planes outside the volume are never read (zero padding).  Results
+ * are bit-identical to tn_fcn_forward on the whole volume.  n must be 1.     */
+typedef struct tn_comm tn_comm;
+tn_status tn_comm_unique_id(void* id_out /*host, 128 bytes (ncclUniqueId)*/);
+tn_status tn_comm_init(const void* nccl_unique_id /*host, 128 B*/, int32_t rank, int32_t nranks,
+                       tn_comm** out);
+void      tn_comm_destroy(tn_comm* comm);
+/* Per-layer slab geometry (host planner; also used by the CPU tests). */
+typedef struct {
+    int32_t level_scale;    /* global depth / layer depth (1, 2, 4, 8)            */
+    int32_t c, h, w, gd;    /* channels, in-plane extents, global depth of layer   */
+    int32_t z0, z1;         /* owned planes at this layer's resolution             */
+    int32_t halo;           /* 1 if the layer's halo planes are exchanged          */
+    int64_t plane_bytes;    /* packed bytes per plane                              */
+    int64_t offset;         /* byte offset of the buffer [z0-1, z1+1) in ws        */
+} tn_slab_layer;
+tn_status tn_fcn_slab_plan(const tn_fcn* net, tn_dims global, int32_t z0, int32_t z1,
+                           tn_slab_layer* out /*host, n_layers or NULL*/, int32_t max_layers,
+                           size_t* ws_bytes /*host, may be NULL*/);
+size_t    tn_fcn_slab_workspace_bytes(const tn_fcn* net, tn_dims global, int32_t z0, int32_t z1);
+/* x_slab float [1][1][z1-z0][h][w] (own planes); logits_slab float
+ * [1][nclass][z1-z0][h][w].                                                    */
+tn_status tn_fcn_forward_slab(const tn_fcn* net, tn_comm* comm, const float* x_slab, tn_dims global,
+                              int32_t z0, int32_t z1, float* logits_slab, void* ws, size_t ws_bytes,
+                              int64_t* d_bad, tn_stream stream);
+/* Single-device emulation: all nslabs slabs of one volume on this GPU, layer by
+ * layer, halos exchanged by device copies (same kernels, offsets and schedule
+ * as tn_fcn_forward_slab).  x / logits as in tn_fcn_forward.                  */
+size_t    tn_fcn_slabs_local_workspace_bytes(const tn_fcn* net, tn_dims global, int32_t nslabs);
+tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims global, int32_t nslabs,
+                                     float* logits, void* ws, size_t ws_bytes, int64_t* d_bad,
+                                     tn_stream stream);
+
 /* Kernel selection for the ternary conv (both exact; parity tests run both).
  * TN_KERNEL_AUTO picks per shape.  Host, process-wide.                        */
 enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2 };

@@ -48,6 +48,12 @@ class tn_segment(ctypes.Structure):
                 ("wp", ctypes.c_void_p)]
 
 
+class tn_slab_layer(ctypes.Structure):
+    _fields_ = [("level_scale", ctypes.c_int32), ("c", ctypes.c_int32), ("h", ctypes.c_int32),
+                ("w", ctypes.c_int32), ("gd", ctypes.c_int32), ("z0", ctypes.c_int32), ("z1", ctypes.c_int32),
+                ("halo", ctypes.c_int32), ("plane_bytes", ctypes.c_int64), ("offset", ctypes.c_int64)]
+
+
 class tn_layer(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("c_out", ctypes.c_int32), ("stride", ctypes.c_int32),
                 ("dil", ctypes.c_int32), ("nseg", ctypes.c_int32), ("src", ctypes.c_int32 * 2),
@@ -85,6 +91,15 @@ SIGNATURES = {
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
     "tn_get_conv_kernel": (_I32, []),
     "tn_conv_kernel_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
+    "tn_comm_unique_id": (ctypes.c_int, [_P]),
+    "tn_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_P)]),
+    "tn_comm_destroy": (None, [_P]),
+    "tn_fcn_slab_plan": (ctypes.c_int, [_P, _D, _I32, _I32, ctypes.POINTER(tn_slab_layer), _I32,
+                                        ctypes.POINTER(_SZ)]),
+    "tn_fcn_slab_workspace_bytes": (_SZ, [_P, _D, _I32, _I32]),
+    "tn_fcn_forward_slab": (ctypes.c_int, [_P, _P, _P, _D, _I32, _I32, _P, _P, _SZ, _P, _P]),
+    "tn_fcn_slabs_local_workspace_bytes": (_SZ, [_P, _D, _I32]),
+    "tn_fcn_forward_slabs_local": (ctypes.c_int, [_P, _P, _D, _I32, _P, _P, _SZ, _P, _P]),
 }
 
 
@@ -385,6 +400,41 @@ class TernaryFCN:
 
     __call__ = forward
 
+    def slab_plan(self, global_shape, z0, z1):
+        """Per-layer slab geometry from the library's planner (host only)."""
+        n = len(self.table)
+        arr = (tn_slab_layer * n)()
+        nb = ctypes.c_size_t()
+        _check(lib.tn_fcn_slab_plan(self.handle, dims(*global_shape), int(z0), int(z1), arr, n, ctypes.byref(nb)),
+               "tn_fcn_slab_plan")
+        return list(arr), int(nb.value)
+
+    def forward_slabs_local(self, x, nslabs, logits=None, ws=None, d_bad=None, stream=None):
+        """All z-slabs of one volume on this device, halos by device copies."""
+        xd = dims_of(x)
+        if ws is None:
+            nb = int(lib.tn_fcn_slabs_local_workspace_bytes(self.handle, xd, int(nslabs)))
+            if nb == 0:
+                raise TNError(TN_ESHAPE, "tn_fcn_slabs_local_workspace_bytes", lib.tn_last_error().decode())
+            ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        if logits is None:
+            logits = torch.empty((xd.n, self.nclass, xd.d, xd.h, xd.w), dtype=torch.float32, device=x.device)
+        _check(lib.tn_fcn_forward_slabs_local(self.handle, _ptr(x), xd, int(nslabs), _ptr(logits), _ptr(ws),
+                                              ws.numel(), _ptr(d_bad), _stream(stream)), "tn_fcn_forward_slabs_local")
+        return logits
+
+    def forward_slab(self, comm, x_slab, global_shape, z0, z1, logits=None, ws=None, d_bad=None, stream=None):
+        """This rank's slab [z0, z1) of a volume decomposed over the ranks of comm (NCCL halos)."""
+        gd = dims(*global_shape)
+        if ws is None:
+            nb = int(lib.tn_fcn_slab_workspace_bytes(self.handle, gd, int(z0), int(z1)))
+            ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=x_slab.device)
+        if logits is None:
+            logits = torch.empty((1, self.nclass, z1 - z0, gd.h, gd.w), dtype=torch.float32, device=x_slab.device)
+        _check(lib.tn_fcn_forward_slab(self.handle, comm.handle, _ptr(x_slab), gd, int(z0), int(z1), _ptr(logits),
+                                       _ptr(ws), ws.numel(), _ptr(d_bad), _stream(stream)), "tn_fcn_forward_slab")
+        return logits
+
     def layer_output(self, x_shape, ws, i):
         """(packed tensor view, dims) of layer i's output inside ws."""
         od = tn_dims()
@@ -395,3 +445,31 @@ class TernaryFCN:
         nwords = od.n * od.d * od.h * od.w * 2 * cw(od.c)
         view = ws[off:off + 4 * nwords].view(torch.int32).view(od.n, od.d, od.h, od.w, 2, cw(od.c))
         return view, od
+
+
+class Comm:
+    """tn_comm_init over a 128-byte NCCL unique id broadcast through torch.distributed."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            _check(lib.tn_comm_unique_id(buf), "tn_comm_unique_id")
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if world > 1:
+            backend = dist.get_backend(group)
+            t = uid.cuda() if backend == "nccl" else uid
+            dist.broadcast(t, src=0, group=group)
+            uid = t.cpu()
+        raw = (ctypes.c_uint8 * 128)(*uid.tolist())
+        h = ctypes.c_void_p()
+        _check(lib.tn_comm_init(raw, int(rank), int(world), ctypes.byref(h)), "tn_comm_init")
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.tn_comm_destroy(h)
+            self.handle = None

@@ -17,14 +17,7 @@ tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where);
 
 using namespace tn;
 
-struct tn_fcn {
-    std::vector<tn_layer> layers;
-    std::vector<int> cin[kMaxSeg];
-    float t_lo, t_hi;
-    const float* pred_w;
-    const float* pred_b;
-    int nclass;
-};
+
 
 namespace {
 

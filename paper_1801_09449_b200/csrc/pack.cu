@@ -352,7 +352,7 @@ constexpr int kMaxClass = 8;
 __global__ void __launch_bounds__(kThreads)
 predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t total,
                const float* __restrict__ w, const float* __restrict__ b, int nclass,
-               float* __restrict__ logits) {
+               float* __restrict__ logits, int64_t cstride) {
     __shared__ float sw[kMaxClass * 32];
     __shared__ float sb[kMaxClass];
     for (int i = threadIdx.x; i < nclass * C; i += kThreads) sw[i] = w[i];
@@ -371,7 +371,7 @@ predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t tota
             const bool p = (sm.x >> c) & 1u;
             acc += nz ? (p ? wv : -wv) : 0.0f;
         }
-        logits[(n * nclass + j) * DHW + v] = acc;
+        logits[(n * nclass + j) * cstride + v] = acc;
     }
 }
 
@@ -431,12 +431,12 @@ cudaError_t launch_requant(const int32_t* y, tn_dims yd, const int32_t* lo, cons
 }
 
 cudaError_t launch_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
-                           int nclass, float* logits, cudaStream_t s) {
+                           int nclass, float* logits, cudaStream_t s, int64_t cstride) {
     const int64_t DHW = static_cast<int64_t>(td.d) * td.h * td.w;
     const int64_t total = DHW * td.n;
     if (total == 0) return cudaSuccess;
     predict_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
-        tp, td.c, DHW, total, w, b, nclass, logits);
+        tp, td.c, DHW, total, w, b, nclass, logits, cstride < 0 ? DHW : cstride);
     return cudaGetLastError();
 }
 

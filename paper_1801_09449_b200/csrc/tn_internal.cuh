@@ -71,8 +71,9 @@ cudaError_t launch_pack_weights(const int8_t* w, int k, int c, uint32_t* wp, int
 cudaError_t launch_unpack(const uint32_t* xp, tn_dims xd, int8_t* x, int64_t* d_bad, cudaStream_t s);
 cudaError_t launch_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int32_t* hi,
                            uint32_t* yp, cudaStream_t s);
+// logits[(n*nclass + j)*cstride + v]; cstride < 0 means d*h*w of td.
 cudaError_t launch_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
-                           int nclass, float* logits, cudaStream_t s);
+                           int nclass, float* logits, cudaStream_t s, int64_t cstride = -1);
 cudaError_t launch_bad_init(int64_t* d_bad, cudaStream_t s);
 
 cudaError_t launch_conv_popc(const ConvDesc& cd, cudaStream_t s);
@@ -82,6 +83,21 @@ cudaError_t launch_conv_first(const FirstDesc& fd, cudaStream_t s);
 // outside what the kernel handles (caller then uses the popc kernel).
 bool        conv_tc_supported(const ConvDesc& cd);
 cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
+
+}  // namespace tn
+
+// The FCN object behind the opaque tn_fcn handle (fcn.cu, slab.cu).
+#include <vector>
+struct tn_fcn {
+    std::vector<tn_layer> layers;
+    std::vector<int> cin[tn::kMaxSeg];
+    float t_lo, t_hi;
+    const float* pred_w;
+    const float* pred_b;
+    int nclass;
+};
+
+namespace tn {
 
 // Host-side error text.
 void set_error(const char* fmt, ...);

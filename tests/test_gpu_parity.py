@@ -318,3 +318,38 @@ def test_c1_full_size_sampled(tn):
     # the int32 and packed outputs agree everywhere (requant of the full int32 tensor)
     y_t = torch.from_numpy(y).cuda()
     np.testing.assert_array_equal(u32(tn.tn_requant(y_t, dev(lo), dev(hi))), yp)
+
+
+# --------------------------------------------------------------------------- configs[4]: z-slabs
+@pytest.mark.parametrize("shape,nslabs", [((1, 1, 32, 48, 48), 2), ((1, 1, 32, 48, 48), 4),
+                                          ((1, 1, 64, 24, 40), 8)])
+def test_fcn_slabs_local_bit_identical(tn, shape, nslabs):
+    """All z-slabs on one device with halos exchanged by device copies (the schedule
+    tn_fcn_forward_slab runs over NCCL) == the whole-volume forward, bit for bit."""
+    x = synth.ct_volume(shape, seed=11)
+    p = synth.fcn_params()
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    xd = dev(x)
+    whole = net(xd).cpu().numpy()
+    flag = tn.bad_flag()
+    slabs = net.forward_slabs_local(xd, nslabs, d_bad=flag).cpu().numpy()
+    assert bad_value(flag) == tn.INT64_MAX
+    np.testing.assert_array_equal(slabs, whole)
+    ref, _, _ = oracle.fcn_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"])
+    tol = np.maximum(np.abs(ref), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(slabs - ref) <= tol)
+
+
+def test_fcn_slab_nccl_single_rank(tn):
+    """tn_fcn_forward_slab through a 1-rank NCCL communicator (the degenerate slab)."""
+    shape = (1, 1, 16, 32, 32)
+    x = synth.ct_volume(shape, seed=12)
+    p = synth.fcn_params()
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    comm = tn.Comm(0, 1)
+    xd = dev(x)
+    got = net.forward_slab(comm, xd, shape, 0, shape[2]).cpu().numpy()
+    np.testing.assert_array_equal(got, net(xd).cpu().numpy())
+    # a non-multiple-of-8 slab is rejected before any work is queued
+    with pytest.raises(tn.TNError):
+        net.forward_slab(comm, xd, shape, 0, 12)
