@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--fcn-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fcn", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     return ap.parse_args()
 
 
@@ -320,6 +321,11 @@ def main():
     if not args.no_fcn:
         fcn = bench_fcn(args, tn, torch, dist, world, rank, dev, stream)
 
+    # ---- configs[4]: one 256x512x512 volume, z-slabs over the ranks (NCCL halos)
+    c4 = None
+    if not args.no_c4:
+        c4 = bench_c4(args, tn, torch, dist, world, rank, dev, stream)
+
     # ---- cpu baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -356,6 +362,7 @@ def main():
             "clocks": clocks,
             "pack_ms": float(np.mean(pack_ms)),
             "fcn": fcn,
+            "fcn_slab": c4,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -396,6 +403,51 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
             "config": "C3: 8 CT-like volumes 1x1x128x256x256, one volume per rank at a time (BASELINE configs[3])",
             "ms_per_batch": ms / args.fcn_steps, "effective_gmacs": total_vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
             "steps": args.fcn_steps, "gpu_launches_per_volume": 15, "scaling": "strong (fixed batch of 8)"}
+
+
+def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
+    cfg = synth.CONFIGS["C4"]
+    shape = cfg["vol_shape"]
+    D, H, W = shape[2:]
+    p = synth.fcn_params(cfg["seed_params"])
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"], device=dev)
+    z0, z1 = rank * D // world, (rank + 1) * D // world
+    vol = synth.ct_volume(shape, seed=cfg["seeds"][0])
+    x = torch.from_numpy(np.ascontiguousarray(vol[:, :, z0:z1])).to(dev)
+    del vol
+    if world > 1:
+        comm = tn.Comm(rank, world)
+        nb = int(tn.lib.tn_fcn_slab_workspace_bytes(net.handle, tn.dims(*shape), z0, z1))
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        logits = torch.empty((1, 2, z1 - z0, H, W), dtype=torch.float32, device=dev)
+        run = lambda: net.forward_slab(comm, x, shape, z0, z1, logits=logits, ws=ws)
+        mode = f"z-slabs of {D // world} planes per rank, NCCL halo exchange per layer"
+    else:
+        ws = net.workspace(shape, dev)
+        logits = torch.empty((1, 2, D, H, W), dtype=torch.float32, device=dev)
+        run = lambda: net(x, logits=logits, ws=ws)
+        mode = "whole volume on one GPU"
+    run()
+    torch.cuda.synchronize()
+    steps = max(2, args.fcn_steps)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    vox = D * H * W
+    return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s",
+            "config": f"C4: one CT-like volume 1x1x{D}x{H}x{W} (BASELINE configs[4]); {mode}",
+            "ms_per_volume": ms, "effective_gmacs": vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
+            "steps": steps, "scaling": "strong (fixed volume)"}
 
 
 if __name__ == "__main__":

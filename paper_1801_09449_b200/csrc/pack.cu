@@ -169,7 +169,7 @@ __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t 
 }
 
 template <int CW>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t total,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
     // 4 voxels per thread: one 32-bit load per channel (a warp reads 128
@@ -184,31 +184,29 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
     uint32_t bad = 0;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
+        // all 32 channel loads of this word first (32 x 128 B per warp in flight)
+        uint32_t q[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+            const int c = 32 * j + jj;
+            q[jj] = c < C ? __ldg(reinterpret_cast<const uint32_t*>(xb + c * DHW)) : 0u;
+        }
         uint32_t accS[4], accM[4];   // [group of 8 channels]
 #pragma unroll
-        for (int gh = 0; gh < 2; ++gh) {
-            uint32_t q[16];
+        for (int g = 0; g < 4; ++g) {
+            uint32_t as = 0u, am = 0u;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-                const int c = 32 * j + 16 * gh + jj;
-                q[jj] = c < C ? __ldg(reinterpret_cast<const uint32_t*>(xb + c * DHW)) : 0u;
+            for (int jj = 0; jj < 8; ++jj) {
+                const uint32_t w = q[8 * g + jj];
+                const uint32_t lsb = w & 0x01010101u;
+                const uint32_t t7 = (w >> 7) & 0x01010101u;
+                const uint32_t pos = lsb & ~t7;
+                bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
+                am += lsb << jj;
+                as += pos << jj;
             }
-#pragma unroll
-            for (int g2 = 0; g2 < 2; ++g2) {
-                uint32_t as = 0u, am = 0u;
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const uint32_t w = q[8 * g2 + jj];
-                    const uint32_t lsb = w & 0x01010101u;
-                    const uint32_t t7 = (w >> 7) & 0x01010101u;
-                    const uint32_t pos = lsb & ~t7;
-                    bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
-                    am += lsb << jj;
-                    as += pos << jj;
-                }
-                accS[2 * gh + g2] = as;
-                accM[2 * gh + g2] = am;
-            }
+            accS[g] = as;
+            accM[g] = am;
         }
         transpose4x4(accS[0], accS[1], accS[2], accS[3], os[0][j], os[1][j], os[2][j], os[3][j]);
         transpose4x4(accM[0], accM[1], accM[2], accM[3], om[0][j], om[1][j], om[2][j], om[3][j]);
