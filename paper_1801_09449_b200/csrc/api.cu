@@ -174,6 +174,16 @@ namespace tn {
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
     if (cd.N == 0 || cd.Do == 0 || cd.Ho == 0 || cd.Wo == 0) return TN_OK;
     const int mode = g_conv_kernel;
+    if (cd.logits != nullptr) {
+        // fused prediction only in the tensor-core epilogue; otherwise conv + predict kernel
+        if (mode != TN_KERNEL_POPC && conv_tc_supported(cd)) return cuda_status(launch_conv_tc(cd, st), where);
+        ConvDesc c2 = cd;
+        c2.logits = nullptr;
+        tn_status s2 = run_conv(c2, st, where);
+        if (s2 != TN_OK) return s2;
+        const tn_dims td{cd.N, cd.K, cd.Do, cd.Ho, cd.Wo};
+        return cuda_status(launch_predict(cd.yp, td, cd.pw, cd.pb, cd.nclass, cd.logits, st, cd.lstride), where);
+    }
     if (mode != TN_KERNEL_POPC && conv_tc_supported(cd)) {
         return cuda_status(launch_conv_tc(cd, st), where);
     }

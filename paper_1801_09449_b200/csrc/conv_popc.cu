@@ -296,15 +296,14 @@ conv_first_kernel(const FirstDesc fd, const Tiling tl) {
         }
         s_code[i] = code;
     }
-    for (int k = threadIdx.x; k < fd.K; k += kThreads) {
-        uint32_t ws = 0, wm = 0;
-        for (int tap = 0; tap < 27; ++tap) {
-            const uint2 q = __ldg(reinterpret_cast<const uint2*>(fd.wp + (k * 27 + tap) * 2));
-            ws |= (q.x & 1u) << tap;
-            wm |= (q.y & 1u) << tap;
-        }
-        s_wt[2 * k] = ws;
-        s_wt[2 * k + 1] = wm;
+    // tap-packed weights: one thread per (k, tap) loads its word pair in parallel
+    for (int i = threadIdx.x; i < 2 * fd.K; i += kThreads) s_wt[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 27 * fd.K; i += kThreads) {
+        const int k = i / 27, tap = i - 27 * k;
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(fd.wp + i * 2));
+        if (q.x & 1u) atomicOr(s_wt + 2 * k, 1u << tap);
+        if (q.y & 1u) atomicOr(s_wt + 2 * k + 1, 1u << tap);
     }
     if (bad != LLONG_MAX) atomicMin(reinterpret_cast<long long*>(&s_bad), static_cast<long long>(bad));
     __syncthreads();

@@ -34,6 +34,7 @@
 // output's x-neighbours live in its own warp: 120 outputs per 128-row tile.
 #include "tn_internal.cuh"
 
+#include <algorithm>
 #include <climits>
 
 #ifndef TN_EXP_NOPROD
@@ -48,8 +49,23 @@
 #ifndef TN_EXP_TRACE
 #define TN_EXP_TRACE 0
 #endif
-#if TN_EXP_TRACE
+#ifndef TN_EXP_NOLOAD
+#define TN_EXP_NOLOAD 0
+#endif
+#ifndef TN_EXP_PROF
+#define TN_EXP_PROF 0
+#endif
+#if TN_EXP_TRACE || TN_EXP_PROF
 __device__ long long g_trace[2048];
+#endif
+#if TN_EXP_PROF
+#define PSTAMP(v) long long v = clock64()
+#define PACC(acc, t0) acc += clock64() - (t0)
+#else
+#define PSTAMP(v) do { } while (0)
+#define PACC(acc, t0) do { } while (0)
+#endif
+#if TN_EXP_TRACE
 #define TRACE(i, cond) do { if ((cond) && blockIdx.x == 0 && (i) < 2048) g_trace[(i)] = clock64(); } while (0)
 #else
 #define TRACE(i, cond) do { } while (0)
@@ -60,12 +76,14 @@ namespace {
 
 constexpr int kEpiWarps = 8;             // 2 per TMEM lane quadrant (K split in halves)
 constexpr int kLoadWarps = 4;            // cp.async packed rows -> staging (one row per thread)
-constexpr int kExpWarps = 4;             // staging -> int8 UMMA layout (one row per thread)
+constexpr int kExpWarps = 8;             // staging -> int8 UMMA layout: two groups of 4 (one row per
+                                         // thread) expanding alternate planes
 constexpr int kLoadWarp0 = kEpiWarps;
 constexpr int kExpWarp0 = kEpiWarps + kLoadWarps;
 constexpr int kMmaWarp = kEpiWarps + kLoadWarps + kExpWarps;
 constexpr int kThreadsTC = (kMmaWarp + 1) * 32;
-constexpr int kMaxStage = 4;
+constexpr int kMaxStage = 16;
+constexpr int kMaxClass = 8;
 constexpr int kRows = 128;               // UMMA M
 constexpr int kOutPerWarp = 30;          // lanes 1..30 of each 32-row run are outputs
 constexpr int kOutPerTile = 4 * kOutPerWarp;
@@ -87,10 +105,9 @@ struct TcPlan {
     int nslot;      // plane ring depth (4..8)
     int nstage;     // packed staging depth (2..4)
     int stage_bytes;
-    int nacc;       // TMEM accumulator buffers (2..4)
     int ring_bytes, w_bytes;
 };
-constexpr int kMaxSlots = 8;
+constexpr int kMaxSlots = 16;
 constexpr int kMaxAcc = 4;
 
 // ---------------------------------------------------------------- PTX helpers
@@ -103,13 +120,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Wait for the phase with the given parity to complete.  The suspend-time hint
+// lets the hardware park the warp until the phase completes instead of
+// re-polling: with 17+ warps per SM, spinning waiters were ~25 % of all issued
+// instructions (ncu), stealing issue slots from the warps doing the work.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "TN_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra TN_WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra TN_WAIT_%=;\n\t}" ::"r"(a), "r"(parity), "r"(1000000u) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -275,6 +296,10 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     constexpr int N = 3 * K;
     constexpr int NCHP = (3 * CT + 1) & ~1;   // chunks per plane slot (== NCHP)
     constexpr int HALF = NCHP / 2;            // K=32 MMAs per plane
+    // macro tile: ZT consecutive output planes share one MMA round / barrier set;
+    // two macro buffers of ZT accumulators of N columns fit in TMEM (<= 384 of 512)
+    constexpr int ZT = K == 16 ? 4 : (K == 32 ? 2 : 1);
+    constexpr int PB = 1;                     // planes per producer batch
     constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_ring = smem;                                   // [slot][chunk][128][16]
@@ -282,7 +307,8 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     uint8_t* s_stage = s_w + pl.w_bytes;                      // [stage][seg][dy][128][16] packed rows
     int* s_lo = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes);  // [K]
     int* s_hi = s_lo + K;                                     // [K]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_hi + K);
+    float* s_pred = reinterpret_cast<float*>(s_hi + K);       // [kMaxClass][K] weights, then [kMaxClass] bias
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_pred + kMaxClass * (K + 1) + ((kMaxClass * (K + 1)) & 1));
     uint64_t* plane_full = bars;                           // [kMaxSlots]
     uint64_t* slot_free = bars + kMaxSlots;                // [kMaxSlots]
     uint64_t* acc_full = bars + 2 * kMaxSlots;             // [kMaxAcc]
@@ -325,15 +351,18 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     }
     if (fused) {
         for (int k = threadIdx.x; k < K; k += kThreadsTC) { s_lo[k] = __ldg(cd.lo + k); s_hi[k] = __ldg(cd.hi + k); }
+        if (cd.logits != nullptr) {
+            for (int i = threadIdx.x; i < cd.nclass * K; i += kThreadsTC) s_pred[i] = __ldg(cd.pw + i);
+            for (int i = threadIdx.x; i < cd.nclass; i += kThreadsTC) s_pred[kMaxClass * K + i] = __ldg(cd.pb + i);
+        }
     }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kMaxSlots; ++i) { mbar_init(plane_full + i, kExpWarps * 32); mbar_init(slot_free + i, 1); }
-        for (int i = 0; i < kMaxStage; ++i) { mbar_init(staged_full + i, kLoadWarps * 32); mbar_init(staged_empty + i, kExpWarps * 32); }
+        for (int i = 0; i < kMaxSlots; ++i) { mbar_init(plane_full + i, kRows); mbar_init(slot_free + i, 1); }
+        for (int i = 0; i < kMaxStage; ++i) { mbar_init(staged_full + i, kLoadWarps * 32); mbar_init(staged_empty + i, kRows); }
         for (int i = 0; i < kMaxAcc; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, kEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    constexpr int kAccMax = (512 / N) < kMaxAcc ? (512 / N) : kMaxAcc;   // == pl.nacc
-    constexpr uint32_t kTmemCols = (kAccMax * N <= 128) ? 128 : (kAccMax * N <= 256 ? 256 : 512);
+    constexpr uint32_t kTmemCols = (2 * ZT * N <= 128) ? 128 : (2 * ZT * N <= 256 ? 256 : 512);
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                      "r"(kTmemCols));
@@ -358,79 +387,135 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
         // these threads never stall on the loads and run up to nstage planes ahead.
         const int m = threadIdx.x - kLoadWarp0 * 32;
         PlaneCursor cur(pl, cd, m);
+        const uint32_t NS = pl.nstage;
+#if TN_EXP_PROF
+        long long l_wait = 0;
+        const long long l_begin = clock64();
+#endif
+        // incremental ring bookkeeping (no integer divisions in the loop)
+        uint32_t st = 0, st_round = 0;
         for (uint32_t g = 0; g < total_planes; ++g) {
-            const uint32_t st = g % pl.nstage;
-            if (g >= static_cast<uint32_t>(pl.nstage)) mbar_wait(staged_empty + st, ((g / pl.nstage) - 1) & 1);
-            const int zg = cd.zo_beg + cur.zp;
-            const bool zin = zg >= 0 && zg < cd.Dci;
+            {
+                PSTAMP(l0);
+                if (st_round > 0) mbar_wait(staged_empty + st, (st_round - 1) & 1);
+                PACC(l_wait, l0);
+                const int zg = cd.zo_beg + cur.zp;
+                const bool zin = zg >= 0 && zg < cd.Dci;
 #pragma unroll
-            for (int sg = 0; sg < NSEG; ++sg) {
-                const SegDesc& sd = cd.seg[sg];
-                const int zs = (sd.up ? (zg >> 1) : zg) - sd.zbeg;
-                const bool zok = zin && zs >= 0 && zs < sd.D;
-                const int64_t pbase = (static_cast<int64_t>(cur.n) * sd.D + zs) * sd.H * sd.W;
+                for (int sg = 0; sg < NSEG; ++sg) {
+                    const SegDesc& sd = cd.seg[sg];
+                    const int zs = (sd.up ? (zg >> 1) : zg) - sd.zbeg;
+                    const bool zok = zin && zs >= 0 && zs < sd.D;
+                    const int64_t pbase = (static_cast<int64_t>(cur.n) * sd.D + zs) * sd.H * sd.W;
 #pragma unroll
-                for (int dy = 0; dy < 3; ++dy) {
-                    const bool ok = zok && cur.ok[dy];
-                    const uint32_t* src = ok ? sd.xp + (pbase + cur.yx[dy][sg]) * 2 * sd.cw : sd.xp;
-                    const uint32_t dst = smem_u32(s_stage + st * pl.stage_bytes + ((sg * 3 + dy) * kRows + m) * 16);
-                    if (sd.cw == 1)
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
-                                     "r"(ok ? 8 : 0) : "memory");
-                    else
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                                     "r"(ok ? 16 : 0) : "memory");
+                    for (int dy = 0; dy < 3; ++dy) {
+                        const bool ok = zok && cur.ok[dy];
+                        const uint32_t* src = ok ? sd.xp + (pbase + cur.yx[dy][sg]) * 2 * sd.cw : sd.xp;
+                        const uint32_t dst =
+                            smem_u32(s_stage + st * pl.stage_bytes + ((sg * 3 + dy) * kRows + m) * 16);
+#if TN_EXP_NOLOAD
+                        if (ok && reinterpret_cast<uintptr_t>(src) == 1) asm volatile("trap;");
+                        continue;
+#endif
+                        if (sd.cw == 1)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                                         "r"(ok ? 8 : 0) : "memory");
+                        else
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                                         "r"(ok ? 16 : 0) : "memory");
+                    }
                 }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(staged_full + st))
+                             : "memory");
+                TRACE(1200 + g, g < 64 && m == 0);
+                cur.advance(pl, cd, m);
+                if (++st == NS) { st = 0; ++st_round; }
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(staged_full + st))
-                         : "memory");
-            cur.advance(pl, cd, m);
         }
+#if TN_EXP_PROF
+        if (m == 0) {
+            long long* o = g_trace + 16 * blockIdx.x;
+            o[12] = clock64() - l_begin; o[13] = l_wait;
+        }
+#endif
     } else if (warp >= kExpWarp0 && warp < kMmaWarp) {
         // ================= expanders: staging (packed) -> ring slot (int8, UMMA
         // K-major no-swizzle layout), then the generic->async proxy fence.  These
         // threads have no global loads in flight, so the fence is cheap.
-        const int m = threadIdx.x - kExpWarp0 * 32;
-        const uint32_t S = pl.nslot;
-        for (uint32_t g = 0; g < total_planes; ++g) {
-            const uint32_t st = g % pl.nstage;
-            mbar_wait(staged_full + st, (g / pl.nstage) & 1);
-            uint4 v[NSEG][3];
+        const int m = (threadIdx.x - kExpWarp0 * 32) & (kRows - 1);
+        const uint32_t eg = (warp - kExpWarp0) >> 2;     // this group expands planes g % 2 == eg
+        const uint32_t S = pl.nslot, NS = pl.nstage;
+#if TN_EXP_PROF
+        long long e_staged = 0, e_slot = 0, e_work = 0, e_fence = 0;
+        const long long e_begin = clock64();
+#endif
+        // Planes in batches of PB: one wait per barrier kind and one proxy fence per
+        // batch (barriers of both rings complete in plane order, so waiting for
+        // the batch's last plane covers the earlier ones).
+        // incremental ring bookkeeping (no integer divisions in the loop): plane g
+        // uses stage st (round st_r) and ring slot sl (round sl_r); this group
+        // steps g by 2
+        uint32_t st = eg, st_r = 0, sl = eg, sl_r = 0;
+        for (uint32_t g0 = eg; g0 < total_planes; g0 += 2) {
+            const uint32_t nb = 1;
+            TRACE(1000 + 2 * g0, g0 < 64 && m == 0);
+            PSTAMP(p0);
+            mbar_wait(staged_full + st, st_r & 1);
+            PACC(e_staged, p0);
+            TRACE(1001 + 2 * g0, g0 < 64 && m == 0);
+            PSTAMP(p1);
+            if (sl_r > 0) mbar_wait(slot_free + sl, (sl_r - 1) & 1);
+            PACC(e_slot, p1);
+            TRACE(601 + 2 * g0, g0 < 64 && m == 0);
+            PSTAMP(p2);
+            for (uint32_t g = g0; g < g0 + nb; ++g) {
+                uint4 v[NSEG][3];
 #pragma unroll
-            for (int sg = 0; sg < NSEG; ++sg)
+                for (int sg = 0; sg < NSEG; ++sg)
 #pragma unroll
-                for (int dy = 0; dy < 3; ++dy)
-                    v[sg][dy] = *reinterpret_cast<const uint4*>(s_stage + st * pl.stage_bytes +
-                                                                ((sg * 3 + dy) * kRows + m) * 16);
-            mbar_arrive(staged_empty + st);
-            const uint32_t sl = g % S;
-            TRACE(600 + 2 * g, g < 64 && m == 0);
-            if (g >= S) mbar_wait(slot_free + sl, ((g / S) - 1) & 1);
-            TRACE(601 + 2 * g, g < 64 && m == 0);
-            uint8_t* slot = s_ring + sl * slot_bytes + m * 16;
+                    for (int dy = 0; dy < 3; ++dy)
+                        v[sg][dy] = *reinterpret_cast<const uint4*>(s_stage + st * pl.stage_bytes +
+                                                                    ((sg * 3 + dy) * kRows + m) * 16);
+                mbar_arrive(staged_empty + st);
+                uint8_t* slot = s_ring + sl * slot_bytes + m * 16;
 #if TN_EXP_NOPROD
-            if (v[0][0].x == 0x12345u)
+                if (v[0][0].x == 0x12345u)
 #endif
 #pragma unroll
-            for (int sg = 0; sg < NSEG; ++sg) {
-                const int choff = sg ? pl.cch[0] : 0;
-                const int cch = pl.cch[sg];
-                const bool two = cd.seg[sg].cw == 2;
+                for (int sg = 0; sg < NSEG; ++sg) {
+                    const int choff = sg ? pl.cch[0] : 0;
+                    const int cch = pl.cch[sg];
+                    const bool two = cd.seg[sg].cw == 2;
 #pragma unroll
-                for (int dy = 0; dy < 3; ++dy) {
-                    const uint4 q = v[sg][dy];
-                    const uint32_t s0 = q.x, m0 = two ? q.z : q.y, s1 = q.y, m1 = q.w;
-                    uint8_t* dst = slot + (dy * CT + choff) * kChunkBytes;
-                    *reinterpret_cast<uint4*>(dst) = expand16(s0, m0, 0);
-                    if (cch > 1) *reinterpret_cast<uint4*>(dst + kChunkBytes) = expand16(s0, m0, 16);
-                    if (cch > 2) *reinterpret_cast<uint4*>(dst + 2 * kChunkBytes) = expand16(s1, m1, 0);
-                    if (cch > 3) *reinterpret_cast<uint4*>(dst + 3 * kChunkBytes) = expand16(s1, m1, 16);
+                    for (int dy = 0; dy < 3; ++dy) {
+                        const uint4 q = v[sg][dy];
+                        const uint32_t s0 = q.x, m0 = two ? q.z : q.y, s1 = q.y, m1 = q.w;
+                        uint8_t* dst = slot + (dy * CT + choff) * kChunkBytes;
+                        *reinterpret_cast<uint4*>(dst) = expand16(s0, m0, 0);
+                        if (cch > 1) *reinterpret_cast<uint4*>(dst + kChunkBytes) = expand16(s0, m0, 16);
+                        if (cch > 2) *reinterpret_cast<uint4*>(dst + 2 * kChunkBytes) = expand16(s1, m1, 0);
+                        if (cch > 3) *reinterpret_cast<uint4*>(dst + 3 * kChunkBytes) = expand16(s1, m1, 16);
+                    }
                 }
             }
+            PACC(e_work, p2);
+            PSTAMP(p3);
             fence_proxy_async();
+            PACC(e_fence, p3);
             mbar_arrive(plane_full + sl);
-            TRACE(800 + g, g < 64 && m == 0);
+            TRACE(800 + g0, g0 < 64 && m == 0);
+            st += 2;
+            if (st >= NS) { st -= NS; ++st_r; }
+            sl += 2;
+            if (sl >= S) { sl -= S; ++sl_r; }
         }
+#if TN_EXP_PROF
+        if (m == 0) {
+            long long* o = g_trace + 16 * blockIdx.x;
+            o[0] = clock64() - e_begin; o[1] = e_staged; o[2] = e_slot; o[3] = e_work; o[4] = e_fence;
+            o[5] = total_planes;
+        }
+#endif
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer: the whole warp walks the schedule (so
         // descriptors stay warp-uniform, in uniform registers) and one elected
@@ -441,135 +526,212 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
         const bool leader = elect_one();
         Walk wk(pl.T, cd.Do, pl.NQ);
         int n, tq, zf, zl;
-        const uint32_t S = pl.nslot, A = pl.nacc;
+        const uint32_t S = pl.nslot;
         const uint64_t aslot = static_cast<uint64_t>(slot_bytes >> 4);   // descriptor step per ring slot
         // Incremental ring / accumulator bookkeeping (no divisions in the loop):
-        // plane a (first plane of the current tile) lives in slot sa with phase pa.
-        uint32_t sa = 0, pa = 0, buf = 0, round = 0, tc = 0;
+        // plane a (first plane of the current macro tile) lives in slot sa, phase pa.
+        uint32_t sa = 0, pa = 0, buf = 0, round = 0, mt = 0;
+#if TN_EXP_PROF
+        long long m_accw = 0, m_planew = 0;
+        const long long m_begin = clock64();
+#endif
         auto next_slot = [S](uint32_t sl, uint32_t ph, uint32_t& sl2, uint32_t& ph2) {
             sl2 = sl + 1;
             ph2 = ph;
             if (sl2 == S) { sl2 = 0; ph2 ^= 1u; }
         };
         while (wk.next(n, tq, zf, zl)) {
-            for (int z = zf; z <= zl; ++z, ++tc) {
-                uint32_t s1, p1, s2, p2;
-                next_slot(sa, pa, s1, p1);
-                next_slot(s1, p1, s2, p2);
-                TRACE(5 * tc + 0, tc < 64 && leader);
+            for (int z = zf; z <= zl; z += ZT, ++mt) {
+                const int zt = min(ZT, zl - z + 1);          // output planes in this macro tile
+                uint32_t sl[ZT + 2], ph[ZT + 2];             // planes a .. a + zt + 1
+                sl[0] = sa;
+                ph[0] = pa;
+#pragma unroll
+                for (int i = 1; i < ZT + 2; ++i) next_slot(sl[i - 1], ph[i - 1], sl[i], ph[i]);
+                TRACE(5 * mt + 0, mt < 64 && leader);
+                PSTAMP(q0);
                 if (round > 0) mbar_wait(acc_empty + buf, (round - 1) & 1);
-                TRACE(5 * tc + 1, tc < 64 && leader);
-                // planes a, a+1 were already seen complete by the previous tile of
-                // this run; only the newest one needs a wait (all three at run start)
-                if (z == zf) {
-                    mbar_wait(plane_full + sa, pa);
-                    mbar_wait(plane_full + s1, p1);
-                }
-                mbar_wait(plane_full + s2, p2);
-                TRACE(5 * tc + 2, tc < 64 && leader);
+                PACC(m_accw, q0);
+                TRACE(5 * mt + 1, mt < 64 && leader);
+                // planes complete in order (the same expander threads arrive for them
+                // in order), so waiting for the newest one covers all of them
+                uint32_t s_new = sl[ZT + 1], p_new = ph[ZT + 1];
+#pragma unroll
+                for (int i = 2; i < ZT + 2; ++i)
+                    if (i == zt + 1) { s_new = sl[i]; p_new = ph[i]; }
+                PSTAMP(q1);
+                mbar_wait(plane_full + s_new, p_new);
+                PACC(m_planew, q1);
+                TRACE(5 * mt + 2, mt < 64 && leader);
                 tc_fence_after();
                 if (leader) {
-                    const uint32_t d = tmem_base + buf * N;
 #pragma unroll
-                    for (int dz = 0; dz < 3; ++dz) {
-                        const uint32_t sl = dz == 0 ? sa : (dz == 1 ? s1 : s2);
-                        const uint64_t ad = adesc0 + sl * aslot;
-                        const uint64_t bd = bdesc0 + static_cast<uint64_t>((dz * wdz_bytes) >> 4);
+                    for (int zz = 0; zz < ZT; ++zz) {
+                        if (zz < zt) {
+                            const uint32_t d = tmem_base + (buf * ZT + zz) * N;
 #pragma unroll
-                        for (int j = 0; j < HALF; ++j)
-                            tc_mma_i8(d, ad + static_cast<uint64_t>((2 * j * kChunkBytes) >> 4),
-                                      bd + static_cast<uint64_t>((2 * j * N * 16) >> 4), idesc, (dz | j) != 0);
+                            for (int dz = 0; dz < 3; ++dz) {
+                                const uint64_t ad = adesc0 + sl[zz + dz] * aslot;
+                                const uint64_t bd = bdesc0 + static_cast<uint64_t>((dz * wdz_bytes) >> 4);
+#pragma unroll
+                                for (int j = 0; j < HALF; ++j)
+                                    tc_mma_i8(d, ad + static_cast<uint64_t>((2 * j * kChunkBytes) >> 4),
+                                              bd + static_cast<uint64_t>((2 * j * N * 16) >> 4), idesc,
+                                              (dz | j) != 0);
+                            }
+                        }
                     }
                     tc_commit(acc_full + buf);
-                    tc_commit(slot_free + sa);
-                    if (z == zl) {
-                        tc_commit(slot_free + s1);
-                        tc_commit(slot_free + s2);
+#pragma unroll
+                    for (int i = 0; i < ZT + 2; ++i) {
+                        // planes a .. a+zt-1 are not needed again; at the end of the run
+                        // neither are a+zt and a+zt+1
+                        const bool last = (z + zt - 1 == zl);
+                        if (i < zt || (last && i < zt + 2)) tc_commit(slot_free + sl[i]);
                     }
                 }
                 __syncwarp();
-                TRACE(320 + tc, tc < 64 && leader);
-                sa = s1;
-                pa = p1;
-                if (++buf == A) { buf = 0; ++round; }
+                TRACE(320 + mt, mt < 64 && leader);
+                // advance to plane a + zt
+#pragma unroll
+                for (int i = 1; i < ZT + 1; ++i)
+                    if (i == zt) { sa = sl[i]; pa = ph[i]; }
+                buf ^= 1u;
+                if (buf == 0) ++round;
             }
-            // the run's last two planes (a+1, a+2 of its last tile) are done too
-            uint32_t t1, q1;
-            next_slot(sa, pa, t1, q1);
-            next_slot(t1, q1, sa, pa);
+            // the run's last two planes (a+zt, a+zt+1 of its last macro tile) are done too
+            uint32_t t1, qq1;
+            next_slot(sa, pa, t1, qq1);
+            next_slot(t1, qq1, sa, pa);
         }
+#if TN_EXP_PROF
+        if (leader) {
+            long long* o = g_trace + 16 * blockIdx.x;
+            o[6] = clock64() - m_begin; o[7] = m_accw; o[8] = m_planew; o[9] = mt;
+        }
+#endif
     } else {
-        // ================= epilogue: warps 0-7; lane quadrant q, K half h
+        // ================= epilogue: warps 0-7 = two groups of four (one warp per
+        // TMEM lane quadrant q).  K <= 32: group h takes the macro tile's planes
+        // zz with zz % 2 == h (all channels); K = 64 (one plane per macro tile):
+        // group h takes channels [32h, 32h + 32).
         const int q = warp & 3;
         const int h = warp >> 2;
-        // chunks of 16 output channels handled by this warp (at most 2 = one word)
         const int kc0 = (K > 32) ? 2 * h : 0;
-        const bool active = (K > 32) || h == 0;
         const int word = (K > 32) ? h : 0;
         Walk wk(pl.T, cd.Do, pl.NQ);
         int n, tq, zf, zl;
-        uint32_t tc = 0;
+        uint32_t buf = 0, round = 0, mt = 0;
+#if TN_EXP_PROF
+        long long ep_wait = 0;
+        const long long ep_begin = clock64();
+#endif
         while (wk.next(n, tq, zf, zl)) {
             const int p = tq * kOutPerTile + row_pos(32 * q + lane);
             const int y = p >= 0 ? p / pl.P : 0;
             const int x = p - y * pl.P;
-            const bool vrow = active && lane >= 1 && lane <= kOutPerWarp && p < pl.NP && x < cd.Wo && y < cd.Ho;
-            for (int z = zf; z <= zl; ++z, ++tc) {
-                const uint32_t buf = tc % static_cast<uint32_t>(pl.nacc);
-                mbar_wait(acc_full + buf, (tc / static_cast<uint32_t>(pl.nacc)) & 1);
-                TRACE(400 + tc, tc < 64 && threadIdx.x == 1);
+            const bool vpos = lane >= 1 && lane <= kOutPerWarp && p < pl.NP && x < cd.Wo && y < cd.Ho;
+            for (int z = zf; z <= zl; z += ZT, ++mt) {
+                const int zt = min(ZT, zl - z + 1);
+                PSTAMP(r0);
+                mbar_wait(acc_full + buf, round & 1);
+                PACC(ep_wait, r0);
+                TRACE(400 + mt, mt < 64 && threadIdx.x == 1);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + buf * N;
-                const int64_t vox = ((static_cast<int64_t>(n) * cd.Do + z) * cd.Ho + y) * cd.Wo + x;
-                uint32_t sbits = 0u, mbits = 0u;
 #pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int kc = kc0 + cc;
-                    if (!active || 16 * kc >= K) break;
+                for (int zz = 0; zz < ZT; ++zz) {
+                    const bool mine = zz < zt && (K > 32 || (zz & 1) == h);
+                    if (!mine) continue;
+                    const uint32_t taddr =
+                        tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (buf * ZT + zz) * N;
+                    const int zo = z + zz;
+                    const int64_t vox = ((static_cast<int64_t>(n) * cd.Do + zo) * cd.Ho + y) * cd.Wo + x;
+                    uint32_t nhi = 0u, nlo = 0u;   // collected high channel first (see below)
+#pragma unroll
+                    for (int cc = 1; cc >= 0; --cc) {
+                        const int kc = kc0 + cc;
+                        if (16 * kc >= K) continue;
 #if TN_EXP_NOEPI
-                    if (tc != 0xFFFFFFFFu) break;
+                        if (mt != 0xFFFFFFFFu) break;
 #endif
-                    int d0[16], d1[16], d2[16];
-                    tmem_ld16(taddr + 0 * K + 16 * kc, d0);
-                    tmem_ld16(taddr + 1 * K + 16 * kc, d1);
-                    tmem_ld16(taddr + 2 * K + 16 * kc, d2);
-                    tmem_wait_ld();
-                    int accv[16];
+                        // out[m] = D[m-1][dx=0] + D[m][dx=1] + D[m+1][dx=2] (rows = lanes)
+                        int accv[16], dd[16];
+                        tmem_ld16(taddr + 1 * K + 16 * kc, accv);
+                        tmem_ld16(taddr + 0 * K + 16 * kc, dd);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        accv[i] = __shfl_up_sync(0xFFFFFFFFu, d0[i], 1) + d1[i] +
-                                  __shfl_down_sync(0xFFFFFFFFu, d2[i], 1);
-                    if (fused) {
-                        // A4 (reading R5): +1 if acc >= hi; else -1 if acc <= lo; else 0
+                        for (int i = 0; i < 16; ++i) accv[i] += __shfl_up_sync(0xFFFFFFFFu, dd[i], 1);
+                        tmem_ld16(taddr + 2 * K + 16 * kc, dd);
+                        tmem_wait_ld();
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int k = 16 * kc + i;
-                            const uint32_t pos = accv[i] >= s_hi[k];
-                            const uint32_t nz = pos | static_cast<uint32_t>(accv[i] <= s_lo[k]);
-                            sbits |= pos << (16 * cc + i);
-                            mbits |= nz << (16 * cc + i);
+                        for (int i = 0; i < 16; ++i) accv[i] += __shfl_down_sync(0xFFFFFFFFu, dd[i], 1);
+                        if (fused) {
+                            // A4 (reading R5): +1 if acc >= hi; else -1 if acc <= lo; else 0.
+                            // Sign bits of (acc - hi) and (lo - acc) are shifted in with funnel
+                            // shifts, channels high to low: bit i of nhi = (acc_i < hi_i),
+                            // bit i of nlo = (acc_i > lo_i); then sign = ~nhi, mask = ~(nhi & nlo).
+#pragma unroll
+                            for (int i4 = 3; i4 >= 0; --i4) {
+                                const int4 h4 = *reinterpret_cast<const int4*>(s_hi + 16 * kc + 4 * i4);
+                                const int4 l4 = *reinterpret_cast<const int4*>(s_lo + 16 * kc + 4 * i4);
+                                const int hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                                for (int i = 3; i >= 0; --i) {
+                                    const int a = accv[4 * i4 + i];
+                                    nhi = __funnelshift_l(static_cast<uint32_t>(a - hh[i]), nhi, 1);
+                                    nlo = __funnelshift_l(static_cast<uint32_t>(ll[i] - a), nlo, 1);
+                                }
+                            }
+                        } else if (vpos) {
+                            int4* dst = reinterpret_cast<int4*>(cd.y + vox * K + 16 * kc);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_int4(accv[4 * i], accv[4 * i + 1], accv[4 * i + 2], accv[4 * i + 3]);
                         }
-                    } else if (vrow) {
-                        int4* dst = reinterpret_cast<int4*>(cd.y + vox * K + 16 * kc);
+                    }
+                    // channels were shifted in from the highest present one down to the
+                    // word's channel 0; the word holds min(K - 32*word, 32) channels
+                    const uint32_t sbits = fused ? ~nhi & (K - 32 * word >= 32 ? 0xFFFFFFFFu : ((1u << (K - 32 * word)) - 1u)) : 0u;
+                    const uint32_t mbits = fused ? ~(nhi & nlo) & (K - 32 * word >= 32 ? 0xFFFFFFFFu : ((1u << (K - 32 * word)) - 1u)) : 0u;
+                    if (fused && vpos && cd.logits != nullptr) {
+                        // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending -- the
+                        // same operations as predict_kernel; K <= 32 so this warp holds all k
+                        const int64_t v = (static_cast<int64_t>(zo) * cd.Ho + y) * cd.Wo + x;
+                        for (int j = 0; j < cd.nclass; ++j) {
+                            float acc = s_pred[kMaxClass * K + j];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[i] = make_int4(accv[4 * i], accv[4 * i + 1], accv[4 * i + 2], accv[4 * i + 3]);
+                            for (int k = 0; k < (K < 32 ? K : 32); ++k) {
+                                const float wv = s_pred[j * K + k];
+                                const bool nz = (mbits >> k) & 1u;
+                                const bool ps = (sbits >> k) & 1u;
+                                acc += nz ? (ps ? wv : -wv) : 0.0f;
+                            }
+                            cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = acc;
+                        }
+                    }
+                    if (fused && vpos) {
+                        uint32_t* dst = cd.yp + vox * 2 * CWO;
+                        if constexpr (CWO == 1) {
+                            *reinterpret_cast<uint2*>(dst) = make_uint2(sbits, mbits);
+                        } else {
+                            dst[word] = sbits;
+                            dst[CWO + word] = mbits;
+                        }
                     }
                 }
                 tc_fence_before();
                 mbar_arrive(acc_empty + buf);
-                TRACE(500 + tc, tc < 64 && threadIdx.x == 1);
-                if (fused && vrow) {
-                    uint32_t* dst = cd.yp + vox * 2 * CWO;
-                    if constexpr (CWO == 1) {
-                        *reinterpret_cast<uint2*>(dst) = make_uint2(sbits, mbits);
-                    } else {
-                        dst[word] = sbits;
-                        dst[CWO + word] = mbits;
-                    }
-                }
+                TRACE(500 + mt, mt < 64 && threadIdx.x == 1);
+                buf ^= 1u;
+                if (buf == 0) ++round;
             }
         }
+#if TN_EXP_PROF
+        if (threadIdx.x == 0) {
+            long long* o = g_trace + 16 * blockIdx.x;
+            o[10] = clock64() - ep_begin; o[11] = ep_wait;
+        }
+#endif
     }
 
     tc_fence_before();
@@ -607,16 +769,20 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     pl.NQ = (pl.NP + kOutPerTile - 1) / kOutPerTile;
     pl.T = static_cast<int64_t>(cd.N) * pl.NQ * cd.Do;
     pl.w_bytes = 3 * pl.nchp * 3 * cd.K * 16;
-    pl.nacc = (512 / (3 * cd.K)) < kMaxAcc ? (512 / (3 * cd.K)) : kMaxAcc;
     const int slot_bytes = pl.nchp * kChunkBytes;
-    const int fixed = pl.w_bytes + 2 * cd.K * 4 + (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 64;
+    const int fixed = pl.w_bytes + 2 * cd.K * 4 + (kMaxClass * (cd.K + 1) + 1) * 4 +
+                      (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 64;
     pl.stage_bytes = cd.nseg * 3 * kRows * 16;
-    pl.nslot = kMaxSlots;
+    // ring depth: at least the macro tile's ZT + 2 planes + 1 being filled; packed
+    // staging depth: deep enough to cover HBM/L2 latency (the loaders run ahead)
+    const int zt = cd.K == 16 ? 4 : (cd.K == 32 ? 2 : 1);
+    pl.nslot = std::min(kMaxSlots, 2 * zt + 4);
     pl.nstage = kMaxStage;
     while (fixed + pl.nslot * slot_bytes + pl.nstage * pl.stage_bytes > 225 * 1024) {
-        if (pl.nslot > 4) --pl.nslot;
+        if (pl.nstage > 8) --pl.nstage;
+        else if (pl.nslot > zt + 3) --pl.nslot;
         else if (pl.nstage > 2) --pl.nstage;
-        else break;
+        else return false;
     }
     pl.ring_bytes = pl.nslot * slot_bytes;
     if (cd.Do != cd.Dci || cd.Ho != cd.Hci || cd.Wo != cd.Wci) return false;
@@ -673,10 +839,12 @@ static cudaError_t dispatch_ct(const ConvDesc& cd, const TcPlan& pl, int64_t gri
 
 static size_t smem_bytes(const TcPlan& pl, int K) {
     return static_cast<size_t>(pl.ring_bytes) + pl.w_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
-           2 * K * sizeof(int) + (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 16;
+           2 * K * sizeof(int) + (kMaxClass * (K + 1) + 1) * sizeof(float) +
+           (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 16;
 }
 
 bool conv_tc_supported(const ConvDesc& cd) {
+    if (cd.logits != nullptr && (cd.K > 32 || cd.nclass < 1 || cd.nclass > kMaxClass || cd.yp == nullptr)) return false;
     TcPlan pl{};
     if (!plan_full(cd, pl)) return false;
     return smem_bytes(pl, cd.K) <= 227 * 1024 && pl.T > 0;
@@ -707,7 +875,7 @@ cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t st) {
 
 }  // namespace tn
 
-#if TN_EXP_TRACE
+#if TN_EXP_TRACE || TN_EXP_PROF
 extern "C" int tn_exp_trace(long long* host, int n) {
     return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n));
 }

@@ -100,7 +100,9 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
 
 // Queue layer i's kernel for one slab (n = 1); the caller then fills the
 // layer's halo planes (if sp.L[i].halo) before any consumer runs.
-tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i, int64_t* d_bad, cudaStream_t s) {
+// logits/lstride: when i is the last layer, the A8 prediction is fused into it.
+tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i, int64_t* d_bad, cudaStream_t s,
+                         float* logits, int64_t lstride) {
     {
         const tn_layer& ly = net->layers[i];
         const tn_slab_layer& o = sp.L[i];
@@ -142,19 +144,14 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             cd.Do = o.z1 - o.z0; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = o.z0;
             cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
             cd.cwo = (ly.c_out + 31) / 32;
+            if (i + 1 == static_cast<int>(net->layers.size())) {
+                cd.logits = logits; cd.lstride = lstride;
+                cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
+            }
             tn_status st = run_conv(cd, s, "slab conv");
             if (st != TN_OK) return st;
         }
     }
-    return TN_OK;
-}
-
-tn_status predict_slab(const tn_fcn* net, const SlabPlan& sp, const char* ws, float* logits, cudaStream_t s) {
-    const tn_slab_layer& o = sp.L.back();
-    const tn_dims td{1, o.c, o.z1 - o.z0, o.h, o.w};
-    cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(ws + o.offset + o.plane_bytes), td,
-                                   net->pred_w, net->pred_b, net->nclass, logits, s);
-    if (e != cudaSuccess) { set_error("slab prediction: %s", cudaGetErrorString(e)); return TN_ECUDA; }
     return TN_OK;
 }
 
@@ -256,8 +253,9 @@ tn_status tn_fcn_forward_slab(const tn_fcn* net, tn_comm* comm, const float* x_s
     if (e != cudaSuccess) { set_error("input copy: %s", cudaGetErrorString(e)); return TN_ECUDA; }
     st = exchange_halo(comm, base + sp.x_off, static_cast<int64_t>(sp.x_plane), z1 - z0 + 2, s);
     if (st != TN_OK) return st;
+    const int64_t lstride = static_cast<int64_t>(z1 - z0) * global.h * global.w;
     for (int i = 0; i < static_cast<int>(net->layers.size()); ++i) {
-        st = run_slab_layer(net, sp, base, i, d_bad, s);
+        st = run_slab_layer(net, sp, base, i, d_bad, s, logits_slab, lstride);
         if (st != TN_OK) return st;
         const tn_slab_layer& o = sp.L[i];
         if (o.halo) {
@@ -265,7 +263,7 @@ tn_status tn_fcn_forward_slab(const tn_fcn* net, tn_comm* comm, const float* x_s
             if (st != TN_OK) return st;
         }
     }
-    return predict_slab(net, sp, base, logits_slab, s);
+    return TN_OK;
 }
 
 size_t tn_fcn_slabs_local_workspace_bytes(const tn_fcn* net, tn_dims global, int32_t nslabs) {
@@ -334,7 +332,9 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
     const int nl = static_cast<int>(net->layers.size());
     for (int i = 0; i < nl; ++i) {
         for (int r = 0; r < nslabs; ++r) {
-            st = run_slab_layer(net, P[r], B[r], i, d_bad, s);
+            const int64_t cstride = static_cast<int64_t>(global.d) * global.h * global.w;
+            float* lg = logits + static_cast<int64_t>(P[r].L.back().z0) * global.h * global.w;
+            st = run_slab_layer(net, P[r], B[r], i, d_bad, s, lg, cstride);
             if (st != TN_OK) return st;
         }
         if (P[0].L[i].halo) {
@@ -343,16 +343,6 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
                               [&](int r) { return P[r].L[i].z1 - P[r].L[i].z0 + 2; });
             if (st != TN_OK) return st;
         }
-    }
-    // prediction of each slab straight into the global [1][nclass][D][H][W] logits
-    for (int r = 0; r < nslabs; ++r) {
-        const tn_slab_layer& o = P[r].L.back();
-        const tn_dims td{1, o.c, o.z1 - o.z0, o.h, o.w};
-        const int64_t cstride = static_cast<int64_t>(global.d) * global.h * global.w;
-        cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(B[r] + o.offset + o.plane_bytes), td,
-                                       net->pred_w, net->pred_b, net->nclass,
-                                       logits + static_cast<int64_t>(o.z0) * o.h * o.w, s, cstride);
-        if (e != cudaSuccess) { set_error("slab prediction: %s", cudaGetErrorString(e)); return TN_ECUDA; }
     }
     return TN_OK;
 }

@@ -43,6 +43,14 @@ struct ConvDesc {
     const int32_t* lo;
     const int32_t* hi;
     int cwo;
+    // Optional A8 fused into the requant epilogue (tensor-core kernel, K <= 32):
+    // logits[(n*nclass + j)*lstride + (z*Ho + y)*Wo + x] = pb[j] + sum_k pw[j][k]*t_k
+    // (fp32, k ascending); the packed output yp is written as well.
+    float* logits;
+    int64_t lstride;
+    const float* pw;
+    const float* pb;
+    int nclass;
 };
 
 struct FirstDesc {

@@ -14,10 +14,10 @@ for _ in range(3):
 buf = (ctypes.c_longlong * 2048)()
 tn.lib.tn_exp_trace(buf, 2048)
 t = np.array(buf[:]); t0 = t[0]
-T = lambda i: int(t[i] - t0)
-print("tile: start acc_empty_ok plane0 plane1 plane2 committed | epi_full epi_done")
-for tc in range(40):
-    print(tc, [T(5*tc+j) for j in range(5)], T(320+tc), '|', T(400+tc), T(500+tc))
-print("producer plane: pre_wait post_wait arrived")
+T = lambda i: int(t[i] - t0) if t[i] else None
+print("macro: start acc_empty_ok planes_ok | committed | epi_full epi_done")
+for m in range(24):
+    print(m, [T(5*m+j) for j in range(3)], T(320+m), '|', T(400+m), T(500+m))
+print("plane: loader_issued | batch: exp_pre_staged exp_post_staged exp_post_slot exp_arrived")
 for g in range(40):
-    print(g, T(600+2*g), T(601+2*g), T(800+g))
+    print(g, T(1200+g), '|', T(1000+2*g), T(1001+2*g), T(601+2*g), T(800+g))
