@@ -171,9 +171,35 @@ tn_status tn_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int3
 namespace tn {
 
 // Shared by tn_conv3d / tn_conv3d_requant / tn_conv3d_seg and the FCN driver.
+// Two-segment conv whose concatenated channels exceed the tensor-core kernel's
+// resident filter bank (e.g. the FCN's 64+64 -> 64 decoder block): pass 1 =
+// segment 0 into int32 partial sums (scratch), pass 2 = segment 1 plus the
+// partials through the epilogue.  Returns false if the split does not apply.
+static bool split_tc_possible(const ConvDesc& cd) {
+    if (cd.nseg != 2 || cd.y_in != nullptr || conv_tc_supported(cd)) return false;
+    ConvDesc a = cd, b = cd;
+    a.nseg = 1; a.yp = nullptr; a.y = reinterpret_cast<int32_t*>(16); a.logits = nullptr;
+    b.nseg = 1; b.seg[0] = cd.seg[1]; b.y_in = reinterpret_cast<const int32_t*>(16);
+    return conv_tc_supported(a) && conv_tc_supported(b);
+}
+
+tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch) {
+    if (scratch != nullptr && g_conv_kernel != TN_KERNEL_POPC && split_tc_possible(cd)) {
+        ConvDesc a = cd, b = cd;
+        a.nseg = 1; a.yp = nullptr; a.y = scratch; a.logits = nullptr; a.lo = a.hi = nullptr;
+        tn_status s1 = cuda_status(launch_conv_tc(a, st), where);
+        if (s1 != TN_OK) return s1;
+        b.nseg = 1; b.seg[0] = cd.seg[1]; b.y_in = scratch;
+        return run_conv(b, st, where);
+    }
+    return run_conv(cd, st, where);
+}
+
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
     if (cd.N == 0 || cd.Do == 0 || cd.Ho == 0 || cd.Wo == 0) return TN_OK;
     const int mode = g_conv_kernel;
+    if (cd.y_in != nullptr && !(mode != TN_KERNEL_POPC && conv_tc_supported(cd)))
+        return fail(TN_EUNSUPPORTED, "%s: partial-sum input needs the tensor-core kernel", where);
     if (cd.logits != nullptr) {
         // fused prediction only in the tensor-core epilogue; otherwise conv + predict kernel
         if (mode != TN_KERNEL_POPC && conv_tc_supported(cd)) return cuda_status(launch_conv_tc(cd, st), where);

@@ -98,6 +98,8 @@ struct TcPlan {
     int P;          // positions per padded row = Wci + 1
     int NP;         // positions per plane = Hci * P
     int NQ;         // position tiles per plane
+    int s;          // stride (1 or 2, all axes)
+    int ntx;        // stride 2: position tiles per (even) conv-input row
     int64_t T;      // tiles = N * NQ * Do
     int cch[2];     // 16-channel chunks per segment
     int cch_tot;    // chunks per window (all segments)
@@ -106,6 +108,7 @@ struct TcPlan {
     int nstage;     // packed staging depth (2..4)
     int stage_bytes;
     int ring_bytes, w_bytes;
+    int ptab_floats;    // fused-prediction quad tables (0 if not fused)
 };
 constexpr int kMaxSlots = 16;
 constexpr int kMaxAcc = 4;
@@ -222,6 +225,15 @@ struct Walk {
     }
 };
 
+// First position (row-padded conv-input plane) of position tile tq.  Stride 1:
+// tiles are contiguous runs of the plane; stride 2: tiles cover the even rows
+// only (the output rows), ntx tiles per row.
+__device__ __forceinline__ int tile_q0(const TcPlan& pl, int tq) {
+    if (pl.s == 1) return tq * kOutPerTile;
+    const int yr = tq / pl.ntx;
+    return 2 * yr * pl.P + (tq - yr * pl.ntx) * kOutPerTile;
+}
+
 // Producer-side walk over the planes a CTA expands, in order: for each run of
 // tiles (z in [zf, zl]) the planes zf-1 .. zl+1.  Per run it caches each row's
 // (y, x) offsets in the three dy windows (per segment).
@@ -236,10 +248,10 @@ struct PlaneCursor {
         if (valid) start_run(pl, cd, m);
     }
     __device__ void start_run(const TcPlan& pl, const ConvDesc& cd, int m) {
-        zp = zf - 1;
+        zp = pl.s * zf - 1;          // conv-input planes s*zf-1 .. s*zl+1 of this run
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy) {
-            const int p = tq * kOutPerTile + row_pos(m) + (dy - 1) * pl.P;
+            const int p = tile_q0(pl, tq) + row_pos(m) + (dy - 1) * pl.P;
             const int y = p >= 0 ? p / pl.P : -1;
             const int x = p - y * pl.P;
             ok[dy] = p >= 0 && y < cd.Hci && x < cd.Wci;
@@ -252,45 +264,14 @@ struct PlaneCursor {
         }
     }
     __device__ void advance(const TcPlan& pl, const ConvDesc& cd, int m) {
-        if (++zp > zl + 1) {
+        if (++zp > pl.s * zl + 1) {
             valid = wk.next(n, tq, zf, zl);
             if (valid) start_run(pl, cd, m);
         }
     }
 };
 
-// One row's packed words of one plane: [segment][dy] x (sign0, sign1, mask0, mask1).
-template <int NSEG>
-struct PlaneWords { uint4 w[NSEG][3]; };
-
-template <int NSEG>
-__device__ __forceinline__ void load_plane(const ConvDesc& cd, const PlaneCursor& c, PlaneWords<NSEG>& pw) {
-    const int zg = cd.zo_beg + c.zp;    // global conv-input plane
-    const bool zin = zg >= 0 && zg < cd.Dci;
-#pragma unroll
-    for (int sg = 0; sg < NSEG; ++sg) {
-        const SegDesc& sd = cd.seg[sg];
-        const int zs = (sd.up ? (zg >> 1) : zg) - sd.zbeg;
-        const bool zok = zin && zs >= 0 && zs < sd.D;
-        const int64_t pbase = (static_cast<int64_t>(c.n) * sd.D + zs) * sd.H * sd.W;
-#pragma unroll
-        for (int dy = 0; dy < 3; ++dy) {
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (zok && c.ok[dy]) {
-                const uint32_t* src = sd.xp + (pbase + c.yx[dy][sg]) * 2 * sd.cw;
-                if (sd.cw == 1) {
-                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(src));
-                    v = make_uint4(q.x, 0u, q.y, 0u);
-                } else {
-                    v = __ldg(reinterpret_cast<const uint4*>(src));
-                }
-            }
-            pw.w[sg][dy] = v;
-        }
-    }
-}
-
-template <int K, int NSEG, int CT>
+template <int K, int NSEG, int CT, int STR>
 __global__ void __launch_bounds__(kThreadsTC, 1)
 conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     constexpr int N = 3 * K;
@@ -300,6 +281,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     // two macro buffers of ZT accumulators of N columns fit in TMEM (<= 384 of 512)
     constexpr int ZT = K == 16 ? 4 : (K == 32 ? 2 : 1);
     constexpr int PB = 1;                     // planes per producer batch
+    constexpr int PMAX = STR * (ZT - 1) + 3;  // conv-input planes read by a full macro tile
     constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_ring = smem;                                   // [slot][chunk][128][16]
@@ -307,8 +289,9 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     uint8_t* s_stage = s_w + pl.w_bytes;                      // [stage][seg][dy][128][16] packed rows
     int* s_lo = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes);  // [K]
     int* s_hi = s_lo + K;                                     // [K]
-    float* s_pred = reinterpret_cast<float*>(s_hi + K);       // [kMaxClass][K] weights, then [kMaxClass] bias
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_pred + kMaxClass * (K + 1) + ((kMaxClass * (K + 1)) & 1));
+    float* s_pred = reinterpret_cast<float*>(s_hi + K);       // [kMaxClass] bias, then quad tables
+    float* s_ptab = s_pred + kMaxClass;                       // [nclass][K/4][256] (fused A8 only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_ptab + pl.ptab_floats);
     uint64_t* plane_full = bars;                           // [kMaxSlots]
     uint64_t* slot_free = bars + kMaxSlots;                // [kMaxSlots]
     uint64_t* acc_full = bars + 2 * kMaxSlots;             // [kMaxAcc]
@@ -352,8 +335,18 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     if (fused) {
         for (int k = threadIdx.x; k < K; k += kThreadsTC) { s_lo[k] = __ldg(cd.lo + k); s_hi[k] = __ldg(cd.hi + k); }
         if (cd.logits != nullptr) {
-            for (int i = threadIdx.x; i < cd.nclass * K; i += kThreadsTC) s_pred[i] = __ldg(cd.pw + i);
-            for (int i = threadIdx.x; i < cd.nclass; i += kThreadsTC) s_pred[kMaxClass * K + i] = __ldg(cd.pb + i);
+            for (int i = threadIdx.x; i < cd.nclass; i += kThreadsTC) s_pred[i] = __ldg(cd.pb + i);
+            // quad tables: entry (mask nibble | sign nibble << 4) = (((t0 w0) + t1 w1) + t2 w2) + t3 w3
+            for (int e = threadIdx.x; e < cd.nclass * (K / 4) * 256; e += kThreadsTC) {
+                const int idx = e & 255, qd = (e >> 8) % (K / 4), j = e / (256 * (K / 4));
+                float part = 0.0f;
+                for (int i = 0; i < 4; ++i) {
+                    const float wv = __ldg(cd.pw + j * K + 4 * qd + i);
+                    const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
+                    part += nz ? (ps ? wv : -wv) : 0.0f;
+                }
+                s_ptab[e] = part;
+            }
         }
     }
     if (threadIdx.x == 0) {
@@ -378,7 +371,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     if (warp >= kLoadWarp0 && warp < kMmaWarp) {
         Walk wk(pl.T, cd.Do, pl.NQ);
         int n, tq, zf, zl;
-        while (wk.next(n, tq, zf, zl)) total_planes += (zl - zf) + 3;
+        while (wk.next(n, tq, zf, zl)) total_planes += pl.s * (zl - zf) + 3;
     }
     if (warp >= kLoadWarp0 && warp < kExpWarp0) {
         // ================= loaders: cp.async each row's packed words of one plane
@@ -399,7 +392,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                 PSTAMP(l0);
                 if (st_round > 0) mbar_wait(staged_empty + st, (st_round - 1) & 1);
                 PACC(l_wait, l0);
-                const int zg = cd.zo_beg + cur.zp;
+                const int zg = pl.s * cd.zo_beg + cur.zp;   // global conv-input plane
                 const bool zin = zg >= 0 && zg < cd.Dci;
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) {
@@ -543,23 +536,25 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
         while (wk.next(n, tq, zf, zl)) {
             for (int z = zf; z <= zl; z += ZT, ++mt) {
                 const int zt = min(ZT, zl - z + 1);          // output planes in this macro tile
-                uint32_t sl[ZT + 2], ph[ZT + 2];             // planes a .. a + zt + 1
+                const int np = STR * (zt - 1) + 3;           // conv-input planes it reads: a .. a+np-1
+                uint32_t sl[PMAX], ph[PMAX];
                 sl[0] = sa;
                 ph[0] = pa;
 #pragma unroll
-                for (int i = 1; i < ZT + 2; ++i) next_slot(sl[i - 1], ph[i - 1], sl[i], ph[i]);
+                for (int i = 1; i < PMAX; ++i) next_slot(sl[i - 1], ph[i - 1], sl[i], ph[i]);
                 TRACE(5 * mt + 0, mt < 64 && leader);
                 PSTAMP(q0);
                 if (round > 0) mbar_wait(acc_empty + buf, (round - 1) & 1);
                 PACC(m_accw, q0);
                 TRACE(5 * mt + 1, mt < 64 && leader);
-                // planes complete in order (the same expander threads arrive for them
-                // in order), so waiting for the newest one covers all of them
-                uint32_t s_new = sl[ZT + 1], p_new = ph[ZT + 1];
+                // each expander group completes its planes in order, so waiting for
+                // the newest plane of each group (a+np-1 and a+np-2) covers all of them
+                uint32_t s_new = sl[PMAX - 1], p_new = ph[PMAX - 1], s_prv = sl[PMAX - 2], p_prv = ph[PMAX - 2];
 #pragma unroll
-                for (int i = 2; i < ZT + 2; ++i)
-                    if (i == zt + 1) { s_new = sl[i]; p_new = ph[i]; }
+                for (int i = 2; i < PMAX; ++i)
+                    if (i == np - 1) { s_new = sl[i]; p_new = ph[i]; s_prv = sl[i - 1]; p_prv = ph[i - 1]; }
                 PSTAMP(q1);
+                mbar_wait(plane_full + s_prv, p_prv);
                 mbar_wait(plane_full + s_new, p_new);
                 PACC(m_planew, q1);
                 TRACE(5 * mt + 2, mt < 64 && leader);
@@ -571,7 +566,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                             const uint32_t d = tmem_base + (buf * ZT + zz) * N;
 #pragma unroll
                             for (int dz = 0; dz < 3; ++dz) {
-                                const uint64_t ad = adesc0 + sl[zz + dz] * aslot;
+                                const uint64_t ad = adesc0 + sl[STR * zz + dz] * aslot;
                                 const uint64_t bd = bdesc0 + static_cast<uint64_t>((dz * wdz_bytes) >> 4);
 #pragma unroll
                                 for (int j = 0; j < HALF; ++j)
@@ -582,27 +577,31 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                         }
                     }
                     tc_commit(acc_full + buf);
+                    const bool last = (z + zt - 1 == zl);
 #pragma unroll
-                    for (int i = 0; i < ZT + 2; ++i) {
-                        // planes a .. a+zt-1 are not needed again; at the end of the run
-                        // neither are a+zt and a+zt+1
-                        const bool last = (z + zt - 1 == zl);
-                        if (i < zt || (last && i < zt + 2)) tc_commit(slot_free + sl[i]);
+                    for (int i = 0; i < PMAX; ++i) {
+                        // planes a .. a+STR*zt-1 are not needed by the next macro tile; at
+                        // the end of the run none of this tile's planes is
+                        if (i < STR * zt || (last && i < np)) tc_commit(slot_free + sl[i]);
                     }
                 }
                 __syncwarp();
                 TRACE(320 + mt, mt < 64 && leader);
-                // advance to plane a + zt
+                // advance to plane a + STR*zt
 #pragma unroll
-                for (int i = 1; i < ZT + 1; ++i)
-                    if (i == zt) { sa = sl[i]; pa = ph[i]; }
+                for (int i = 1; i < PMAX; ++i)
+                    if (i == STR * zt) { sa = sl[i]; pa = ph[i]; }
                 buf ^= 1u;
                 if (buf == 0) ++round;
             }
-            // the run's last two planes (a+zt, a+zt+1 of its last macro tile) are done too
-            uint32_t t1, qq1;
-            next_slot(sa, pa, t1, qq1);
-            next_slot(t1, qq1, sa, pa);
+            // the run's remaining planes (a+STR*zt .. a+np-1 of its last macro tile)
+#pragma unroll
+            for (int i = 0; i < 3 - STR; ++i) {
+                uint32_t t1, qq1;
+                next_slot(sa, pa, t1, qq1);
+                sa = t1;
+                pa = qq1;
+            }
         }
 #if TN_EXP_PROF
         if (leader) {
@@ -627,10 +626,13 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
         const long long ep_begin = clock64();
 #endif
         while (wk.next(n, tq, zf, zl)) {
-            const int p = tq * kOutPerTile + row_pos(32 * q + lane);
-            const int y = p >= 0 ? p / pl.P : 0;
-            const int x = p - y * pl.P;
-            const bool vpos = lane >= 1 && lane <= kOutPerWarp && p < pl.NP && x < cd.Wo && y < cd.Ho;
+            const int p = tile_q0(pl, tq) + row_pos(32 * q + lane);
+            const int yi = p >= 0 ? p / pl.P : 0;      // conv-input coordinates of this row
+            const int xi = p - yi * pl.P;
+            const bool ctr = STR == 1 || ((yi | xi) & 1) == 0;    // stride 2: even-even centres only
+            const int y = yi / STR, x = xi / STR;                    // output coordinates
+            const bool vpos = lane >= 1 && lane <= kOutPerWarp && p < pl.NP && ctr && xi < cd.Wci &&
+                              yi < cd.Hci && x < cd.Wo && y < cd.Ho;
             for (int z = zf; z <= zl; z += ZT, ++mt) {
                 const int zt = min(ZT, zl - z + 1);
                 PSTAMP(r0);
@@ -665,6 +667,15 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                         tmem_wait_ld();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) accv[i] += __shfl_down_sync(0xFFFFFFFFu, dd[i], 1);
+                        if (cd.y_in != nullptr && vpos) {   // partial sums of an earlier channel split
+                            const int4* src = reinterpret_cast<const int4*>(cd.y_in + vox * K + 16 * kc);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int4 t = __ldg(src + i);
+                                accv[4 * i] += t.x; accv[4 * i + 1] += t.y;
+                                accv[4 * i + 2] += t.z; accv[4 * i + 3] += t.w;
+                            }
+                        }
                         if (fused) {
                             // A4 (reading R5): +1 if acc >= hi; else -1 if acc <= lo; else 0.
                             // Sign bits of (acc - hi) and (lo - acc) are shifted in with funnel
@@ -698,13 +709,12 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                         // same operations as predict_kernel; K <= 32 so this warp holds all k
                         const int64_t v = (static_cast<int64_t>(zo) * cd.Ho + y) * cd.Wo + x;
                         for (int j = 0; j < cd.nclass; ++j) {
-                            float acc = s_pred[kMaxClass * K + j];
+                            float acc = s_pred[j];
+                            const float* tab = s_ptab + j * (K / 4) * 256;
 #pragma unroll
-                            for (int k = 0; k < (K < 32 ? K : 32); ++k) {
-                                const float wv = s_pred[j * K + k];
-                                const bool nz = (mbits >> k) & 1u;
-                                const bool ps = (sbits >> k) & 1u;
-                                acc += nz ? (ps ? wv : -wv) : 0.0f;
+                            for (int qd = 0; qd < (K < 32 ? K : 32) / 4; ++qd) {
+                                const uint32_t idx = ((mbits >> (4 * qd)) & 0xFu) | (((sbits >> (4 * qd)) & 0xFu) << 4);
+                                acc += tab[qd * 256 + idx];
                             }
                             cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = acc;
                         }
@@ -749,8 +759,10 @@ int g_num_sms = 0;
 static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     if (cd.nseg < 1 || cd.nseg > 2) return false;
     for (int a = 0; a < 3; ++a)
-        if (cd.s[a] != 1 || cd.p[a] != 1 || cd.dl[a] != 1) return false;
+        if (cd.s[a] != cd.s[0] || cd.p[a] != 1 || cd.dl[a] != 1) return false;
+    if (cd.s[0] != 1 && !(cd.s[0] == 2 && cd.nseg == 1)) return false;
     if (cd.K != 16 && cd.K != 32 && cd.K != 64) return false;
+    pl.s = cd.s[0];
     pl.cch_tot = 0;
     pl.cch[1] = 0;
     for (int i = 0; i < cd.nseg; ++i) {
@@ -766,26 +778,31 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     const int64_t np = static_cast<int64_t>(cd.Hci) * pl.P;
     if (np > INT_MAX / 2) return false;
     pl.NP = static_cast<int>(np);
-    pl.NQ = (pl.NP + kOutPerTile - 1) / kOutPerTile;
+    pl.ntx = (cd.Wci + kOutPerTile - 1) / kOutPerTile;
+    pl.NQ = pl.s == 1 ? (pl.NP + kOutPerTile - 1) / kOutPerTile : ((cd.Hci + 1) / 2) * pl.ntx;
     pl.T = static_cast<int64_t>(cd.N) * pl.NQ * cd.Do;
     pl.w_bytes = 3 * pl.nchp * 3 * cd.K * 16;
     const int slot_bytes = pl.nchp * kChunkBytes;
-    const int fixed = pl.w_bytes + 2 * cd.K * 4 + (kMaxClass * (cd.K + 1) + 1) * 4 +
+    pl.ptab_floats = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
+    const int fixed = pl.w_bytes + 2 * cd.K * 4 + (kMaxClass + pl.ptab_floats) * 4 +
                       (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 64;
     pl.stage_bytes = cd.nseg * 3 * kRows * 16;
     // ring depth: at least the macro tile's ZT + 2 planes + 1 being filled; packed
     // staging depth: deep enough to cover HBM/L2 latency (the loaders run ahead)
     const int zt = cd.K == 16 ? 4 : (cd.K == 32 ? 2 : 1);
-    pl.nslot = std::min(kMaxSlots, 2 * zt + 4);
+    const int pmax = pl.s * (zt - 1) + 3;
+    pl.nslot = std::min(kMaxSlots, pmax + pl.s * zt + 2);
     pl.nstage = kMaxStage;
     while (fixed + pl.nslot * slot_bytes + pl.nstage * pl.stage_bytes > 225 * 1024) {
         if (pl.nstage > 8) --pl.nstage;
-        else if (pl.nslot > zt + 3) --pl.nslot;
+        else if (pl.nslot > pmax + 1) --pl.nslot;
         else if (pl.nstage > 2) --pl.nstage;
         else return false;
     }
     pl.ring_bytes = pl.nslot * slot_bytes;
-    if (cd.Do != cd.Dci || cd.Ho != cd.Hci || cd.Wo != cd.Wci) return false;
+    if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
+        cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
+        return false;
     return true;
 }
 
@@ -794,7 +811,7 @@ static cudaError_t launch_one(void (*kern)(ConvDesc, TcPlan), const ConvDesc& cd
                               size_t smem, cudaStream_t st) {
     // cudaFuncSetAttribute is a slow host call: raise the kernel's smem limit once
     // to the maximum instead of per launch.
-    static void* configured[32] = {nullptr};
+    static void* configured[48] = {nullptr};
     bool done = false;
     for (void* f : configured) done = done || f == reinterpret_cast<void*>(kern);
     if (!done) {
@@ -820,18 +837,25 @@ static cudaError_t launch_one(void (*kern)(ConvDesc, TcPlan), const ConvDesc& cd
 
 template <int K>
 static cudaError_t dispatch_ct(const ConvDesc& cd, const TcPlan& pl, int64_t grid, size_t smem, cudaStream_t st) {
-    if (cd.nseg == 1) {
+    if (cd.nseg == 1 && pl.s == 1) {
         switch (pl.cch_tot) {
-            case 1: return launch_one(conv_tc_kernel<K, 1, 1>, cd, pl, grid, smem, st);
-            case 2: return launch_one(conv_tc_kernel<K, 1, 2>, cd, pl, grid, smem, st);
-            case 3: return launch_one(conv_tc_kernel<K, 1, 3>, cd, pl, grid, smem, st);
-            case 4: return launch_one(conv_tc_kernel<K, 1, 4>, cd, pl, grid, smem, st);
+            case 1: return launch_one(conv_tc_kernel<K, 1, 1, 1>, cd, pl, grid, smem, st);
+            case 2: return launch_one(conv_tc_kernel<K, 1, 2, 1>, cd, pl, grid, smem, st);
+            case 3: return launch_one(conv_tc_kernel<K, 1, 3, 1>, cd, pl, grid, smem, st);
+            case 4: return launch_one(conv_tc_kernel<K, 1, 4, 1>, cd, pl, grid, smem, st);
+        }
+    } else if (cd.nseg == 1) {
+        switch (pl.cch_tot) {
+            case 1: return launch_one(conv_tc_kernel<K, 1, 1, 2>, cd, pl, grid, smem, st);
+            case 2: return launch_one(conv_tc_kernel<K, 1, 2, 2>, cd, pl, grid, smem, st);
+            case 3: return launch_one(conv_tc_kernel<K, 1, 3, 2>, cd, pl, grid, smem, st);
+            case 4: return launch_one(conv_tc_kernel<K, 1, 4, 2>, cd, pl, grid, smem, st);
         }
     } else {
         switch (pl.cch_tot) {
-            case 2: return launch_one(conv_tc_kernel<K, 2, 2>, cd, pl, grid, smem, st);
-            case 3: return launch_one(conv_tc_kernel<K, 2, 3>, cd, pl, grid, smem, st);
-            case 4: return launch_one(conv_tc_kernel<K, 2, 4>, cd, pl, grid, smem, st);
+            case 2: return launch_one(conv_tc_kernel<K, 2, 2, 1>, cd, pl, grid, smem, st);
+            case 3: return launch_one(conv_tc_kernel<K, 2, 3, 1>, cd, pl, grid, smem, st);
+            case 4: return launch_one(conv_tc_kernel<K, 2, 4, 1>, cd, pl, grid, smem, st);
         }
     }
     return cudaErrorNotSupported;
@@ -839,12 +863,14 @@ static cudaError_t dispatch_ct(const ConvDesc& cd, const TcPlan& pl, int64_t gri
 
 static size_t smem_bytes(const TcPlan& pl, int K) {
     return static_cast<size_t>(pl.ring_bytes) + pl.w_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
-           2 * K * sizeof(int) + (kMaxClass * (K + 1) + 1) * sizeof(float) +
+           2 * K * sizeof(int) + (kMaxClass + pl.ptab_floats) * sizeof(float) +
            (2 * kMaxSlots + 2 * kMaxAcc + 2 * kMaxStage) * 8 + 16;
 }
 
 bool conv_tc_supported(const ConvDesc& cd) {
-    if (cd.logits != nullptr && (cd.K > 32 || cd.nclass < 1 || cd.nclass > kMaxClass || cd.yp == nullptr)) return false;
+    if (cd.logits != nullptr &&
+        (cd.K > 32 || cd.nclass < 1 || cd.nclass > kMaxClass || cd.yp == nullptr || cd.nclass * cd.K > 64))
+        return false;   // quad tables: nclass * K/4 * 1 KB <= 16 KB
     TcPlan pl{};
     if (!plan_full(cd, pl)) return false;
     return smem_bytes(pl, cd.K) <= 227 * 1024 && pl.T > 0;

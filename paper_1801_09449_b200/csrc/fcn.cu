@@ -8,12 +8,10 @@
 // by the caller (reading R9; the Python binding's fcn_table()).
 #include "tn_internal.cuh"
 
+#include <algorithm>
 #include <new>
 #include <vector>
 
-namespace tn {
-tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where);
-}
 
 using namespace tn;
 
@@ -31,10 +29,11 @@ constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t* total) {
+tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t* total,
+               size_t* scratch_off) {
     const int L = static_cast<int>(net->layers.size());
     P.assign(L, LayerPlan{});
-    size_t off = 0;
+    size_t off = 0, scratch = 0;
     for (int i = 0; i < L; ++i) {
         const tn_layer& ly = net->layers[i];
         int d, h, w;
@@ -64,8 +63,11 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
         P[i].off = off;
         P[i].bytes = tn_packed_bytes(o);
         off = align_up(off + P[i].bytes);
+        if (ly.nseg == 2 && net->cin[0][i] + net->cin[1][i] > 64)   // split over two tensor-core passes
+            scratch = std::max(scratch, static_cast<size_t>(o.n) * o.d * o.h * o.w * o.c * 4);
     }
-    *total = off;
+    *scratch_off = off;
+    *total = align_up(off + scratch);
     return TN_OK;
 }
 
@@ -134,7 +136,8 @@ size_t tn_fcn_workspace_bytes(const tn_fcn* net, tn_dims xd) {
     if (net == nullptr) return 0;
     std::vector<LayerPlan> P;
     size_t total = 0;
-    if (plan(net, xd, P, &total) != TN_OK) return 0;
+    size_t soff = 0;
+    if (plan(net, xd, P, &total, &soff) != TN_OK) return 0;
     return total;
 }
 
@@ -143,7 +146,8 @@ const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* w
     if (net == nullptr || ws == nullptr || i < 0 || i >= static_cast<int>(net->layers.size())) return nullptr;
     std::vector<LayerPlan> P;
     size_t total = 0;
-    if (plan(net, xd, P, &total) != TN_OK) return nullptr;
+    size_t soff = 0;
+    if (plan(net, xd, P, &total, &soff) != TN_OK) return nullptr;
     if (out_dims) *out_dims = P[i].out;
     return reinterpret_cast<const uint32_t*>(static_cast<const char*>(ws) + P[i].off);
 }
@@ -155,7 +159,8 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
     if (xd.n < 1 || xd.d < 1 || xd.h < 1 || xd.w < 1) { set_error("FCN input must be non-empty"); return TN_ESHAPE; }
     std::vector<LayerPlan> P;
     size_t total = 0;
-    tn_status st = plan(net, xd, P, &total);
+    size_t soff = 0;
+    tn_status st = plan(net, xd, P, &total, &soff);
     if (st != TN_OK) return st;
     if (ws == nullptr || ws_bytes < total) {
         set_error("workspace too small: need %zu bytes, got %zu", total, ws_bytes);
@@ -213,7 +218,7 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
             cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
             cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
         }
-        st = run_conv(cd, s, "tn_fcn_forward");
+        st = run_conv_scratch(cd, s, "tn_fcn_forward", reinterpret_cast<int32_t*>(base + soff));
         if (st != TN_OK) return st;
     }
     if (net->layers[L - 1].kind == TN_LAYER_FIRST) {

@@ -344,7 +344,7 @@ requant_kernel(const int32_t* __restrict__ y, int64_t V, int K, int cwo,
 
 // ----------------------------------------------------------------------------
 // Prediction (A8): logits[n][j][v] = b[j] + sum_c w[j][c] * t_c in fp32, c
-// ascending (reading R12).  One thread per voxel; C <= 32.
+// ascending within quads of 4 channels, quads ascending (reading R12).  One thread per voxel; C <= 32.
 // ----------------------------------------------------------------------------
 constexpr int kMaxClass = 8;
 __global__ void __launch_bounds__(kThreads)
@@ -362,12 +362,18 @@ predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t tota
     const int64_t n = g / DHW;
     const int64_t v = g - n * DHW;
     for (int j = 0; j < nclass; ++j) {
+        // b + sum over channel quads of ((((t0 w0) + t1 w1) + t2 w2) + t3 w3): the
+        // summation order the tensor-core epilogue's quad tables reproduce exactly
         float acc = sb[j];
-        for (int c = 0; c < C; ++c) {
-            const float wv = sw[j * C + c];
-            const bool nz = (sm.y >> c) & 1u;
-            const bool p = (sm.x >> c) & 1u;
-            acc += nz ? (p ? wv : -wv) : 0.0f;
+        for (int c0 = 0; c0 < C; c0 += 4) {
+            float part = 0.0f;
+            for (int c = c0; c < c0 + 4 && c < C; ++c) {
+                const float wv = sw[j * C + c];
+                const bool nz = (sm.y >> c) & 1u;
+                const bool p = (sm.x >> c) & 1u;
+                part += nz ? (p ? wv : -wv) : 0.0f;
+            }
+            acc += part;
         }
         logits[(n * nclass + j) * cstride + v] = acc;
     }

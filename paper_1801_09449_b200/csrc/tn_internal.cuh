@@ -40,6 +40,8 @@ struct ConvDesc {
     // outputs: exactly one of y / yp
     int32_t* y;                   // int32 channel-last [N][Do][Ho][Wo][K]
     uint32_t* yp;                 // packed [N][Do][Ho][Wo][2][cwo]
+    const int32_t* y_in;          // optional int32 partial sums [N][Do][Ho][Wo][K] added before the
+                                  // epilogue (tensor-core kernel; split-channel convs)
     const int32_t* lo;
     const int32_t* hi;
     int cwo;
@@ -106,6 +108,11 @@ struct tn_fcn {
 };
 
 namespace tn {
+
+// Conv dispatch (api.cu): kernel selection; the _scratch variant may split a
+// two-segment conv into two tensor-core passes through int32 partial sums.
+tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where);
+tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch);
 
 // Host-side error text.
 void set_error(const char* fmt, ...);

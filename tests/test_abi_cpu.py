@@ -89,6 +89,7 @@ def test_fcn_create_validation_and_workspace(tn):
     # packed bytes/voxel: 8 for c <= 32, 16 for c = 64.  R0: #1 #2 #13 #14; R1: #3 #4 #11 #12;
     # R2: #5 (32) #6 (64) #9 (64) #10 (32); R3: #7 #8 (64)
     expect = 8 * R0 * 4 + 8 * (R0 // 8) * 4 + 48 * (R0 // 64) + 32 * (R0 // 512)
+    expect += (R0 // 64) * 64 * 4   # int32 partial sums of the split 64+64 -> 64 block (#9)
     assert abs(ws - expect) < 256 * 16
     tn.lib.tn_fcn_destroy(h)
     # a forward reference is rejected

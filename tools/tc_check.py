@@ -8,6 +8,21 @@ import paper_1801_09449_b200 as tn
 def dev(a): return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 cases = [((1, 16, 4, 5, 6), 16), ((1, 16, 32, 32, 32), 16), ((1, 64, 5, 7, 9), 64), ((1, 32, 6, 20, 130), 32),
          ((2, 32, 3, 4, 5), 64), ((1, 64, 8, 128, 128), 64)]
+cases2 = [((1, 16, 8, 20, 36), 16), ((1, 32, 12, 18, 20), 32), ((1, 64, 10, 12, 14), 64), ((1, 16, 32, 64, 256), 16),
+          ((1, 64, 9, 7, 5), 64)]
+for shape, k in cases2:
+    x = synth.ternary_codes(shape, 0.5, seed=5); w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.6, seed=6)
+    xp = tn.tn_pack_i8(dev(x)); wp = tn.tn_pack_weights(dev(w)); xd = tn.dims(*shape)
+    tn.tn_set_conv_kernel(tn.TN_KERNEL_POPC)
+    yr = tn.tn_conv3d(xp, xd, wp, k, tn.geom(2)).cpu().numpy()
+    tn.tn_set_conv_kernel(tn.TN_KERNEL_TC)
+    y = tn.tn_conv3d(xp, xd, wp, k, tn.geom(2)).cpu().numpy()
+    ok = np.array_equal(y, yr)
+    msg = f"stride2 {shape} k={k}: tc==popc {ok}"
+    if not ok:
+        bad = np.argwhere(y != yr)
+        msg += f" mismatches={len(bad)} first={bad[:3].tolist()}"
+    print(msg, flush=True)
 for shape, k in cases:
     x = synth.ternary_codes(shape, 0.5, seed=1); w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.6, seed=2)
     xp = tn.tn_pack_i8(dev(x)); wp = tn.tn_pack_weights(dev(w)); xd = tn.dims(*shape)
