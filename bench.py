@@ -299,7 +299,7 @@ def main():
         peak = 2.0 * bf16          # int8 dense = 2 x bf16 dense (nominal 4.5 vs 2.25 PFLOP/s)
         achieved = 2.0 * C1_MACS / conv_avg_s / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": tn_peaks.get("c1_tc_conv_dram_bytes"),
                 "peak_source": "2 x MEASURED_PEAKS.bf16_tflops (int8/bf16 nominal ratio)"}
     else:
         popc_per_clk = tn_peaks.get("popc_per_clk_per_sm", 16.0)

@@ -209,14 +209,24 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
                                      float* logits, void* ws, size_t ws_bytes, int64_t* d_bad,
                                      tn_stream stream);
 
-/* Kernel selection for the ternary conv (both exact; parity tests run both).
- * TN_KERNEL_AUTO picks per shape.  Host, process-wide.                        */
-enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2 };
+/* Kernel selection for the ternary conv (all exact; parity tests run each).
+ *   TN_KERNEL_POPC  CUDA-core XOR/AND/POPC form of Eq. 9 (any geometry)
+ *   TN_KERNEL_TC    tcgen05 kind::i8, dx taps merged along N (stride 1, C <= 64)
+ *   TN_KERNEL_TZ    tcgen05 kind::i8, taps as descriptor offsets and the three
+ *                   kernel planes merged along N (stride 1/2, C <= 64, small
+ *                   27*C*K filter bank; W even)
+ * TN_KERNEL_AUTO picks TZ, else TC, else POPC per shape.  Host, process-wide. */
+enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2, TN_KERNEL_TZ = 3 };
 tn_status tn_set_conv_kernel(int32_t which);
 int32_t   tn_get_conv_kernel(void);
-/* Which kernel (TN_KERNEL_POPC or TN_KERNEL_TC) a tn_conv3d_seg call with these
+/* Upper bound on the CTAs of the persistent tensor-core conv grids (0 = one per
+ * SM, the default).  Results do not depend on it (integer math); tests use a
+ * small cap to give each CTA long runs of output planes.  Host, process-wide;
+ * TN_EINVAL if max_ctas < 0.                                                  */
+tn_status tn_set_grid_cap(int32_t max_ctas);
+/* Which kernel (TN_KERNEL_POPC, _TC or _TZ) a tn_conv3d_seg call with these
  * arguments would run under the current selection; -1 if the call is invalid
- * (or TN_KERNEL_TC is forced on a shape it does not cover).  Host only.       */
+ * (or a forced tensor-core kernel does not cover the shape).  Host only.      */
 int32_t   tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);
 
 #ifdef __cplusplus

@@ -23,7 +23,7 @@ INT64_MAX = (1 << 63) - 1
 
 TN_OK, TN_EINVAL, TN_ESHAPE, TN_EALIGN, TN_EUNSUPPORTED, TN_EDOMAIN, TN_ECUDA, TN_ENCCL = range(8)
 TN_LAYER_FIRST, TN_LAYER_CONV = 1, 2
-TN_KERNEL_AUTO, TN_KERNEL_POPC, TN_KERNEL_TC = 0, 1, 2
+TN_KERNEL_AUTO, TN_KERNEL_POPC, TN_KERNEL_TC, TN_KERNEL_TZ = 0, 1, 2, 3
 _STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ESHAPE", 3: "TN_EALIGN", 4: "TN_EUNSUPPORTED",
            5: "TN_EDOMAIN", 6: "TN_ECUDA", 7: "TN_ENCCL"}
 
@@ -90,6 +90,7 @@ SIGNATURES = {
     "tn_fcn_layer_output": (_P, [_P, _D, _P, _I32, ctypes.POINTER(_D)]),
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
     "tn_get_conv_kernel": (_I32, []),
+    "tn_set_grid_cap": (ctypes.c_int, [_I32]),
     "tn_conv_kernel_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
     "tn_comm_unique_id": (ctypes.c_int, [_P]),
     "tn_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_P)]),
@@ -279,6 +280,10 @@ def tn_set_conv_kernel(which: int):
 
 def tn_get_conv_kernel() -> int:
     return int(lib.tn_get_conv_kernel())
+
+
+def tn_set_grid_cap(max_ctas: int):
+    _check(lib.tn_set_grid_cap(int(max_ctas)), "tn_set_grid_cap")
 
 
 def tn_conv_kernel_for(seg_dims, k, g: tn_geom, upsample=None) -> int:

@@ -1,7 +1,7 @@
 // api.cu -- the C ABI of libtn.so (include/tn.h): host-side validation, error
 // text, descriptor construction and kernel selection.  No compute happens here;
 // every step of the path runs in the kernels of pack.cu / conv_popc.cu /
-// conv_tc.cu.
+// conv_tc.cu / conv_tz.cu.
 #include "tn_internal.cuh"
 
 #include <cstdarg>
@@ -12,6 +12,9 @@ namespace tn {
 
 static thread_local char g_err[512] = "";
 static int g_conv_kernel = TN_KERNEL_AUTO;
+static int g_grid_cap = 0;
+
+int persistent_grid_cap() { return g_grid_cap; }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -184,7 +187,8 @@ static bool split_tc_possible(const ConvDesc& cd) {
 }
 
 tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch) {
-    if (scratch != nullptr && g_conv_kernel != TN_KERNEL_POPC && split_tc_possible(cd)) {
+    if (scratch != nullptr && (g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TC) &&
+        !(g_conv_kernel == TN_KERNEL_AUTO && conv_tz_supported(cd)) && split_tc_possible(cd)) {
         ConvDesc a = cd, b = cd;
         a.nseg = 1; a.yp = nullptr; a.y = scratch; a.logits = nullptr; a.lo = a.hi = nullptr;
         tn_status s1 = cuda_status(launch_conv_tc(a, st), where);
@@ -195,14 +199,38 @@ tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int
     return run_conv(cd, st, where);
 }
 
+// Kernel choice for one conv launch under the process-wide selector:
+// TN_KERNEL_TZ (tap-offset z-merged tensor-core kernel, small C*K), then
+// TN_KERNEL_TC (dx-merged tensor-core kernel), then the CUDA-core popc kernel;
+// a forced selector only takes its own kernel.  -1 if nothing covers the shape.
+static int pick_kernel(const ConvDesc& cd, int mode) {
+    // AUTO: TZ for stride 2 (measured faster there), TC, then TZ
+    if ((mode == TN_KERNEL_TZ || (mode == TN_KERNEL_AUTO && cd.s[0] == 2)) && conv_tz_supported(cd)) return TN_KERNEL_TZ;
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TC) && conv_tc_supported(cd)) return TN_KERNEL_TC;
+    if (mode == TN_KERNEL_AUTO && conv_tz_supported(cd)) return TN_KERNEL_TZ;
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC) && cd.y_in == nullptr && cd.logits == nullptr)
+        return TN_KERNEL_POPC;
+    return -1;
+}
+
+static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st) {
+    switch (kernel) {
+        case TN_KERNEL_TZ: return launch_conv_tz(cd, st);
+        case TN_KERNEL_TC: return launch_conv_tc(cd, st);
+        case TN_KERNEL_POPC: return launch_conv_popc(cd, st);
+    }
+    return cudaErrorNotSupported;
+}
+
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
     if (cd.N == 0 || cd.Do == 0 || cd.Ho == 0 || cd.Wo == 0) return TN_OK;
     const int mode = g_conv_kernel;
-    if (cd.y_in != nullptr && !(mode != TN_KERNEL_POPC && conv_tc_supported(cd)))
-        return fail(TN_EUNSUPPORTED, "%s: partial-sum input needs the tensor-core kernel", where);
+    if (cd.y_in != nullptr && pick_kernel(cd, mode) != TN_KERNEL_TC)
+        return fail(TN_EUNSUPPORTED, "%s: partial-sum input needs the tcgen05 (TC) kernel", where);
     if (cd.logits != nullptr) {
-        // fused prediction only in the tensor-core epilogue; otherwise conv + predict kernel
-        if (mode != TN_KERNEL_POPC && conv_tc_supported(cd)) return cuda_status(launch_conv_tc(cd, st), where);
+        // fused prediction in a tensor-core epilogue; otherwise conv + predict kernel
+        const int kf = pick_kernel(cd, mode);
+        if (kf == TN_KERNEL_TZ || kf == TN_KERNEL_TC) return cuda_status(launch_kernel(kf, cd, st), where);
         ConvDesc c2 = cd;
         c2.logits = nullptr;
         tn_status s2 = run_conv(c2, st, where);
@@ -210,11 +238,9 @@ tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
         const tn_dims td{cd.N, cd.K, cd.Do, cd.Ho, cd.Wo};
         return cuda_status(launch_predict(cd.yp, td, cd.pw, cd.pb, cd.nclass, cd.logits, st, cd.lstride), where);
     }
-    if (mode != TN_KERNEL_POPC && conv_tc_supported(cd)) {
-        return cuda_status(launch_conv_tc(cd, st), where);
-    }
-    if (mode == TN_KERNEL_TC) return fail(TN_EUNSUPPORTED, "%s: tcgen05 kernel does not cover this shape", where);
-    return cuda_status(launch_conv_popc(cd, st), where);
+    const int kern = pick_kernel(cd, mode);
+    if (kern < 0) return fail(TN_EUNSUPPORTED, "%s: the selected conv kernel (%d) does not cover this shape", where, mode);
+    return cuda_status(launch_kernel(kern, cd, st), where);
 }
 
 tn_status build_conv(const tn_segment* segs, int nseg, int k, tn_geom g, const int32_t* lo,
@@ -342,13 +368,19 @@ tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float
 }
 
 tn_status tn_set_conv_kernel(int32_t which) {
-    if (which != TN_KERNEL_AUTO && which != TN_KERNEL_POPC && which != TN_KERNEL_TC)
+    if (which != TN_KERNEL_AUTO && which != TN_KERNEL_POPC && which != TN_KERNEL_TC && which != TN_KERNEL_TZ)
         return fail(TN_EINVAL, "unknown kernel selector %d", which);
     g_conv_kernel = which;
     return TN_OK;
 }
 
 int32_t tn_get_conv_kernel(void) { return g_conv_kernel; }
+
+tn_status tn_set_grid_cap(int32_t max_ctas) {
+    if (max_ctas < 0) return fail(TN_EINVAL, "grid cap must be >= 0 (got %d)", max_ctas);
+    g_grid_cap = max_ctas;
+    return TN_OK;
+}
 
 int32_t tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g) {
     if (segs == nullptr) return -1;
@@ -363,10 +395,12 @@ int32_t tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_g
         if (tmp[i].wp == nullptr) tmp[i].wp = dummy;
     }
     if (build_conv(tmp, nseg, k, g, &zero, &zero, nullptr, dummy, &cd, nullptr) != TN_OK) return -1;
-    const bool tc = conv_tc_supported(cd);
-    if (g_conv_kernel == TN_KERNEL_TC) return tc ? TN_KERNEL_TC : -1;
-    if (g_conv_kernel == TN_KERNEL_POPC) return TN_KERNEL_POPC;
-    return tc ? TN_KERNEL_TC : TN_KERNEL_POPC;
+    const int kern = pick_kernel(cd, g_conv_kernel);
+    if (kern == TN_KERNEL_POPC || kern < 0) {
+        // the popc kernel covers every valid shape of a plain tn_conv3d_seg call
+        return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_POPC ? TN_KERNEL_POPC : -1;
+    }
+    return kern;
 }
 
 }  // extern "C"

@@ -33,6 +33,7 @@
 // Tiles are 4 runs of 32 rows (one per lane quadrant) overlapping by 2, so each
 // output's x-neighbours live in its own warp: 120 outputs per 128-row tile.
 #include "tn_internal.cuh"
+#include "tc_ptx.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -56,7 +57,8 @@
 #define TN_EXP_PROF 0
 #endif
 #if TN_EXP_TRACE || TN_EXP_PROF
-__device__ long long g_trace[2048];
+__device__ long long g_trace[4096];
+#define SSTAMP(i) do { if (threadIdx.x == 0) g_trace[2560 + 8 * blockIdx.x + (i)] = clock64() - k_begin; } while (0)
 #endif
 #if TN_EXP_PROF
 #define PSTAMP(v) long long v = clock64()
@@ -109,99 +111,10 @@ struct TcPlan {
     int stage_bytes;
     int ring_bytes, w_bytes;
     int ptab_floats;    // fused-prediction quad tables (0 if not fused)
+    int wstage;         // packed weights staged through the ring during setup
 };
 constexpr int kMaxSlots = 16;
 constexpr int kMaxAcc = 4;
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Wait for the phase with the given parity to complete.  The suspend-time hint
-// lets the hardware park the warp until the phase completes instead of
-// re-polling: with 17+ warps per SM, spinning waiters were ~25 % of all issued
-// instructions (ncu), stealing issue slots from the warps doing the work.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "TN_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra TN_WAIT_%=;\n\t}" ::"r"(a), "r"(parity), "r"(1000000u) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "elect.sync _|P, 0xffffffff;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}"
-        : "=r"(pred));
-    return pred != 0;
-}
-
-// UMMA shared-memory descriptor, K-major, no swizzle (canonical "interleave"
-// layout: 8-row x 16-byte core matrices; rows 16 B apart, 8-row groups SBO
-// apart, the two 16-byte K halves of a K=32 instruction LBO apart).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) |
-           (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
-           (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-// Instruction descriptor: s32 accumulate, s8 x s8, both K-major, M=128, N.
-__host__ __device__ constexpr uint32_t idesc_i8(int n) {
-    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | ((128u >> 4) << 24);
-}
-
-// 16 ternary lanes (bits sh..sh+15 of a sign / mask word pair) -> 16 int8.
-__device__ __forceinline__ uint4 expand16(uint32_t s, uint32_t m, int sh) {
-    const uint32_t mm = m >> sh, nn = (m & ~s) >> sh;
-    uint32_t o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t mb = (((mm >> (4 * i)) & 0xFu) * 0x00204081u) & 0x01010101u;
-        const uint32_t nb = (((nn >> (4 * i)) & 0xFu) * 0x00204081u) & 0x01010101u;
-        o[i] = mb + nb * 0xFEu;          // +1 -> 0x01, -1 -> 0xFF, 0 -> 0x00
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
 
 // ---------------------------------------------------------------- tile walk
 struct Walk {
@@ -305,67 +218,121 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     constexpr int slot_bytes = NCHP * kChunkBytes;
     constexpr int wdz_bytes = NCHP * N * 16;
     const bool fused = cd.yp != nullptr;
+#if TN_EXP_PROF
+    const long long k_begin = clock64();
+#endif
 
-    // ---- one-time setup: zero the ring (padding chunks stay zero), expand the
-    // packed filter bank into the B-operand image, thresholds, barriers, TMEM.
-    for (int i = threadIdx.x; i < pl.ring_bytes / 16; i += kThreadsTC)
-        reinterpret_cast<uint4*>(s_ring)[i] = make_uint4(0u, 0u, 0u, 0u);
+    // ---- one-time setup: expand the packed filter bank into the B-operand image.
+    // The packed words are first staged (cp.async, all in flight at once) in the
+    // ring, which is unused until the roles start; each (k, tap) word pair is then
+    // expanded once into its CT 16-channel units.  The ring needs no zeroing: the
+    // B rows of a padding chunk are zero, so whatever A holds there adds 0.
     {
-        const int units = 3 * NCHP * N;  // 16-byte units (dz, chunk, n)
-        for (int u = threadIdx.x; u < units; u += kThreadsTC) {
-            const int nrow = u % N;
-            const int ch = (u / N) % NCHP;
-            const int dz = u / (N * NCHP);
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (ch < 3 * CT) {
-                const int dy = ch / CT;
-                int j = ch - dy * CT;
-                const int sg = (j >= pl.cch[0]) ? 1 : 0;
-                if (sg) j -= pl.cch[0];
-                const int dx = nrow / K, k = nrow - dx * K;
-                const int tap = (dz * 3 + dy) * 3 + dx;
-                const int cw = cd.seg[sg].cw;
-                const uint32_t* src = cd.seg[sg].wp + (static_cast<int64_t>(k) * 27 + tap) * 2 * cw;
-                const int word = (16 * j) >> 5, sh = (16 * j) & 31;
-                v = expand16(__ldg(src + word), __ldg(src + cw + word), sh);
-            }
-            *reinterpret_cast<uint4*>(s_w + dz * wdz_bytes + ch * (N * 16) + nrow * 16) = v;
-        }
-    }
-    if (fused) {
-        for (int k = threadIdx.x; k < K; k += kThreadsTC) { s_lo[k] = __ldg(cd.lo + k); s_hi[k] = __ldg(cd.hi + k); }
-        if (cd.logits != nullptr) {
-            for (int i = threadIdx.x; i < cd.nclass; i += kThreadsTC) s_pred[i] = __ldg(cd.pb + i);
-            // quad tables: entry (mask nibble | sign nibble << 4) = (((t0 w0) + t1 w1) + t2 w2) + t3 w3
-            for (int e = threadIdx.x; e < cd.nclass * (K / 4) * 256; e += kThreadsTC) {
-                const int idx = e & 255, qd = (e >> 8) % (K / 4), j = e / (256 * (K / 4));
-                float part = 0.0f;
-                for (int i = 0; i < 4; ++i) {
-                    const float wv = __ldg(cd.pw + j * K + 4 * qd + i);
-                    const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
-                    part += nz ? (ps ? wv : -wv) : 0.0f;
+        int lo_r = 0, hi_r = 0;
+        if (fused && threadIdx.x < K) { lo_r = __ldg(cd.lo + threadIdx.x); hi_r = __ldg(cd.hi + threadIdx.x); }
+        const uint32_t* wsrc[kMaxSeg];
+        {
+            uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_ring);
+            int ofs = 0;
+#pragma unroll
+            for (int sg = 0; sg < NSEG; ++sg) {
+                wsrc[sg] = cd.seg[sg].wp;
+                if (pl.wstage) {
+                    const int n4 = K * 27 * 2 * cd.seg[sg].cw / 4;     // uint4 units (K % 16 == 0)
+                    const uint4* g = reinterpret_cast<const uint4*>(cd.seg[sg].wp);
+                    for (int i = threadIdx.x; i < n4; i += kThreadsTC)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_wp + ofs + 4 * i)),
+                                     "l"(g + i) : "memory");
+                    wsrc[sg] = s_wp + ofs;
+                    ofs += 4 * n4;
                 }
-                s_ptab[e] = part;
+            }
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        }
+        if (fused && threadIdx.x < K) { s_lo[threadIdx.x] = lo_r; s_hi[threadIdx.x] = hi_r; }
+        __syncthreads();
+#if TN_EXP_PROF
+        SSTAMP(0);
+#endif
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+            const int cw = cd.seg[sg].cw, cch = pl.cch[sg], choff = sg ? pl.cch[0] : 0;
+            for (int pr = threadIdx.x; pr < K * 27; pr += kThreadsTC) {
+                // consecutive threads take consecutive k of one tap: conflict-free 16-byte stores
+                const int tap = pr / K, k = pr - K * tap;
+                const int dz = tap / 9, dy = (tap / 3) % 3, dx = tap % 3;
+                const uint32_t* src = wsrc[sg] + (k * 27 + tap) * 2 * cw;
+                uint32_t sw[2], mw[2];
+                if (cw == 1) {
+                    const uint2 t = *reinterpret_cast<const uint2*>(src);
+                    sw[0] = t.x; mw[0] = t.y; sw[1] = mw[1] = 0u;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4*>(src);
+                    sw[0] = t.x; sw[1] = t.y; mw[0] = t.z; mw[1] = t.w;
+                }
+                uint8_t* dst = s_w + dz * wdz_bytes + (dy * CT + choff) * (N * 16) + (dx * K + k) * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j < cch)
+                        *reinterpret_cast<uint4*>(dst + j * (N * 16)) = expand16(sw[j >> 1], mw[j >> 1], 16 * (j & 1));
             }
         }
+        if (NCHP > 3 * CT)
+            for (int u = threadIdx.x; u < 3 * N; u += kThreadsTC)
+                *reinterpret_cast<uint4*>(s_w + (u / N) * wdz_bytes + (3 * CT) * (N * 16) + (u % N) * 16) =
+                    make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();   // the staged words in the ring are dead from here on
     }
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kMaxSlots; ++i) { mbar_init(plane_full + i, kRows); mbar_init(slot_free + i, 1); }
-        for (int i = 0; i < kMaxStage; ++i) { mbar_init(staged_full + i, kLoadWarps * 32); mbar_init(staged_empty + i, kRows); }
-        for (int i = 0; i < kMaxAcc; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, kEpiWarps * 32); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if TN_EXP_PROF
+    SSTAMP(1);
+    SSTAMP(2);
+#endif
+    if (fused && cd.logits != nullptr) {
+        for (int i = threadIdx.x; i < cd.nclass; i += kThreadsTC) s_pred[i] = __ldg(cd.pb + i);
+        // quad tables: entry (mask nibble | sign nibble << 4) = (((t0 w0) + t1 w1) + t2 w2) + t3 w3
+        for (int e = threadIdx.x; e < cd.nclass * (K / 4) * 256; e += kThreadsTC) {
+            const int idx = e & 255, qd = (e >> 8) % (K / 4), j = e / (256 * (K / 4));
+            float part = 0.0f;
+            for (int i = 0; i < 4; ++i) {
+                const float wv = __ldg(cd.pw + j * K + 4 * qd + i);
+                const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
+                part += nz ? (ps ? wv : -wv) : 0.0f;
+            }
+            s_ptab[e] = part;
+        }
     }
+    {   // one barrier per thread (a serial init loop costs ~1 us)
+        const int t = threadIdx.x;
+        if (t < kMaxSlots) { mbar_init(plane_full + t, kRows); mbar_init(slot_free + t, 1); }
+        else if (t < kMaxSlots + kMaxStage) {
+            mbar_init(staged_full + t - kMaxSlots, kLoadWarps * 32);
+            mbar_init(staged_empty + t - kMaxSlots, kRows);
+        } else if (t < kMaxSlots + kMaxStage + kMaxAcc) {
+            mbar_init(acc_full + t - kMaxSlots - kMaxStage, 1);
+            mbar_init(acc_empty + t - kMaxSlots - kMaxStage, kEpiWarps * 32);
+        }
+        if (t < kMaxSlots + kMaxStage + kMaxAcc) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+#if TN_EXP_PROF
+    SSTAMP(3);
+#endif
     constexpr uint32_t kTmemCols = (2 * ZT * N <= 128) ? 128 : (2 * ZT * N <= 256 ? 256 : 512);
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+#if TN_EXP_PROF
+    SSTAMP(4);
+#endif
     fence_proxy_async();   // ring zeros + weight image visible to the tensor core
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *s_tmem;
+#if TN_EXP_PROF
+    if (threadIdx.x == 0) g_trace[16 * blockIdx.x + 14] = clock64() - k_begin;
+#endif
 
     uint32_t total_planes = 0;
     if (warp >= kLoadWarp0 && warp < kMmaWarp) {
@@ -746,6 +713,9 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
 
     tc_fence_before();
     __syncthreads();
+#if TN_EXP_PROF
+    if (threadIdx.x == 0) g_trace[16 * blockIdx.x + 15] = clock64() - k_begin;
+#endif
     if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
@@ -800,6 +770,16 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
         else return false;
     }
     pl.ring_bytes = pl.nslot * slot_bytes;
+    {
+        int64_t wbytes = 0;
+        bool al = true;
+        for (int i = 0; i < cd.nseg; ++i) {
+            wbytes += static_cast<int64_t>(cd.K) * 27 * 2 * cd.seg[i].cw * 4;
+            al = al && (reinterpret_cast<uintptr_t>(cd.seg[i].wp) & 15) == 0;
+        }
+        pl.wstage = al && wbytes <= pl.ring_bytes;
+        if (!pl.wstage) return false;   // the setup stages the packed filter bank in the ring
+    }
     if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
         cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
         return false;
@@ -886,7 +866,8 @@ cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t st) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t grid = pl.T < g_num_sms ? pl.T : g_num_sms;
+    const int cap = persistent_grid_cap() > 0 ? std::min(persistent_grid_cap(), g_num_sms) : g_num_sms;
+    const int64_t grid = pl.T < cap ? pl.T : cap;
     if (grid <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     switch (cd.K) {
@@ -903,6 +884,6 @@ cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t st) {
 
 #if TN_EXP_TRACE || TN_EXP_PROF
 extern "C" int tn_exp_trace(long long* host, int n) {
-    return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n));
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * (n < 4096 ? n : 4096)));
 }
 #endif

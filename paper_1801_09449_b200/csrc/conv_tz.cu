@@ -1,0 +1,754 @@
+// conv_tz.cu -- ternary conv3d on the tcgen05 tensor cores with the taps folded
+// into the UMMA descriptors ("tap-offset") and the three kernel planes dz merged
+// along N ("z-merged").  Written for the layers with few channels (C, K <= 64,
+// 27*C*K small enough for the filter bank to sit in shared memory three times
+// over), where the dx-merged kernel (conv_tc.cu) is limited by issue slots.
+//
+// The arithmetic is the same integer as Eq. 9: int8 products
+// of ternary values {-1,0,+1} accumulated exactly in int32, over the 3x3x3
+// window of Sec. 2 with zero padding; the fused epilogue applies
+// the integer thresholds of reading R5/R6 and repacks into the
+// paper's 2-bit sign/mask format (Fig. 3 :130).
+//
+// Layout.  Output positions of a plane are a raster with pitch Po = Wo + 1 (one
+// separator column per row).  A CTA expands, per input plane, a strip of
+// RS = 128*T + halo consecutive raster rows into int8 (16 channels = 16 bytes per
+// row and chunk) in the canonical K-major no-swizzle UMMA layout, where row r
+// sits at byte 16*r (8-row core matrices, SBO = 128).  Tap (dy, dx) of an
+// output tile is then the same buffer at a row offset: the descriptor start moves
+// by 16*(dy*Po + dx) bytes, and the second 16-channel half of a K = 32 MMA is any
+// other (tap, chunk) slice at LBO = the byte distance between them (both checked
+// on B200 by tools/desc_test.cu: arbitrary 16-byte starts and LBOs, overlapping
+// or not, run at full rate).  So each input voxel is expanded once per plane and
+// per strip, and no shifted copies exist.  Stride 2 uses four phase images
+// (even/odd rows x even/odd columns), each in the output raster, so every tap is
+// again a plain offset.
+//
+// z-merge.  An input plane i feeds up to three output planes (z = i+1-dz).  The B
+// operand holds the filter blocks of the three dz side by side (N = 3K), and the
+// accumulators of the three outputs of a tile sit in three adjacent TMEM column
+// blocks, so one MMA per K-slice pair updates all three.  Output z lives in TMEM
+// block sigma = u mod 3 (u = the CTA's running output index); the three blocks a
+// plane touches are always {0,1,2} in a rotation, handled by three rotations of
+// the B blocks stored as the cyclic sequence [dz2 dz1 dz0 dz2 dz1].  Stride 2:
+// odd planes feed two outputs (rotations [dz2 dz0] / [dz0 dz2]), even planes one.
+// The epilogue re-initialises a block after reading it (to -hi, so the
+// accumulator holds acc - hi and the A4 compare is a sign bit), so the MMAs always
+// accumulate.
+//
+// CTA = 18 warps, persistent, one per SM:
+//   warps 0-7   epilogue, two groups of four (one warp per TMEM lane quadrant);
+//               group g takes the tiles t % 2 == g of every output plane
+//   warps 8-15  expanders: packed rows (staging) -> int8 A strip of one plane
+//   warp 16     MMA issuer (one elected lane issues; the warp walks the schedule)
+//   warp 17     loader: one elected lane issues 1-D bulk copies (cp.async.bulk)
+//               of the contiguous packed rows a strip needs, per plane and segment
+#include "tn_internal.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+namespace tn {
+namespace {
+
+constexpr int kZEpiWarps = 8;
+constexpr int kZExpWarps = 8;
+constexpr int kZExpWarp0 = kZEpiWarps;
+constexpr int kZMmaWarp = kZEpiWarps + kZExpWarps;
+constexpr int kZLoadWarp = kZMmaWarp + 1;
+constexpr int kZThreads = (kZLoadWarp + 1) * 32;
+constexpr int kZExpThreads = kZExpWarps * 32;
+constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
+constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
+constexpr int kZMaxSlot = 4;          // A ring
+constexpr int kZMaxStage = 4;         // packed staging ring
+constexpr int kZMaxClass = 8;
+
+struct TzPlan {
+    int s;                  // stride (1 or 2, all axes)
+    int RO;                 // output blocks per tile in TMEM (3 for s = 1, 2 for s = 2)
+    int Po, NPo, NT;        // output raster pitch (Wo + 1), positions per plane, 128-row tiles per plane
+    int T, nstrip;          // tiles per strip, strips per plane
+    int RS, REG;            // strip rows per (phase, chunk) region, region bytes
+    int nph;                // phase images (1 or 4)
+    int slot_bytes, nslot;  // A ring
+    int stage_bytes, nstage;
+    int seg_off[kMaxSeg];   // byte offset of each segment's rows within a stage
+    int cch[kMaxSeg];       // 16-channel chunks per segment
+    int nmma;
+    int a_off[kZMaxMma];    // per MMA: A start (bytes from the slot base) and LBO (bytes)
+    int a_lbo[kZMaxMma];
+    int8_t sl_tap[2 * kZMaxMma];    // per K-slice (sorted order): tap (dy*3+dx) and chunk, -1 = zero slice
+    int8_t sl_chunk[2 * kZMaxMma];
+    int NB;                 // B blocks (5 for s = 1, 4 for s = 2)
+    int b_bytes;
+    int64_t units;          // N * nstrip * Do
+    uint32_t po_magic;      // ceil(2^32 / Po)
+    int ptab_floats;
+};
+
+// q / Po for 0 <= q with q * Po < 2^32
+__device__ __forceinline__ int div_po(uint32_t q, uint32_t magic) { return static_cast<int>(__umulhi(q, magic)); }
+
+// Walk over a CTA's contiguous range of units (n, strip, output plane), in runs
+// of consecutive output planes of one (n, strip).
+struct ZWalk {
+    int64_t t, t_end;
+    int Do, nstrip;
+    __device__ ZWalk(int64_t U, int Do_, int nstrip_) : Do(Do_), nstrip(nstrip_) {
+        t = U * blockIdx.x / gridDim.x;
+        t_end = U * (blockIdx.x + 1) / gridDim.x;
+    }
+    __device__ bool next(int& n, int& strip, int& zf, int& zl) {
+        if (t >= t_end) return false;
+        const int64_t col = t / Do;
+        zf = static_cast<int>(t - col * Do);
+        const int64_t len = min(static_cast<int64_t>(Do - zf), t_end - t);
+        zl = zf + static_cast<int>(len) - 1;
+        n = static_cast<int>(col / nstrip);
+        strip = static_cast<int>(col - static_cast<int64_t>(n) * nstrip);
+        t += len;
+        return true;
+    }
+};
+
+// Global conv-input planes of a run of (local) output planes [zf, zl].
+__device__ __forceinline__ void run_planes(const TzPlan& pl, const ConvDesc& cd, int zf, int zl, int& i0, int& i1) {
+    i0 = max(pl.s * (cd.zo_beg + zf) - 1, 0);
+    i1 = min(pl.s * (cd.zo_beg + zl) + 1, cd.Dci - 1);
+}
+
+// Source rows of segment sg that the strip's A rows read: [ya, ya + nrows).
+__device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd, int strip, int sg, int& ya,
+                                           int& nrows) {
+    const int qa = strip * 128 * pl.T - pl.Po - 1;
+    const int qb = qa + pl.RS - 1;
+    const uint32_t two = 2u * pl.Po;
+    int ylo = div_po(static_cast<uint32_t>(qa) + two, pl.po_magic) - 2;
+    int yhi = div_po(static_cast<uint32_t>(qb) + two, pl.po_magic) - 2;
+    if (pl.s == 2) { ylo = 2 * ylo; yhi = 2 * yhi + 1; }
+    ylo = max(ylo, 0);
+    yhi = min(yhi, cd.Hci - 1);
+    const SegDesc& sd = cd.seg[sg];
+    if (sd.up) { ylo >>= 1; yhi >>= 1; }
+    yhi = min(yhi, sd.H - 1);
+    ya = ylo;
+    nrows = max(yhi - ylo + 1, 0);
+}
+
+template <int K, int CT, int NSEG, int STR, bool PRED>
+__global__ void __launch_bounds__(kZThreads, 1)
+conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
+    constexpr int RO = STR == 1 ? 3 : 2;
+    constexpr int NPH = STR == 1 ? 1 : 4;
+    constexpr int NB = STR == 1 ? 5 : 4;
+    constexpr int CWO = (K + 31) / 32;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* s_a = smem;                                         // [slot][phase][chunk][RS][16]
+    uint8_t* s_b = s_a + pl.nslot * pl.slot_bytes;               // [mma][half][NB*K][16]
+    uint8_t* s_stage = s_b + pl.b_bytes;                         // [stage] packed rows per segment
+    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes);   // [K] -hi (TMEM init)
+    int* s_lmh = s_nhi + K;                                      // [K] lo - hi
+    float* s_pred = reinterpret_cast<float*>(s_lmh + K);         // [kZMaxClass] bias, then quad tables
+    float* s_ptab = s_pred + kZMaxClass;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_ptab + pl.ptab_floats);
+    uint64_t* plane_full = bars;                                 // [kZMaxSlot]
+    uint64_t* plane_free = plane_full + kZMaxSlot;               // [kZMaxSlot]
+    uint64_t* staged_full = plane_free + kZMaxSlot;              // [kZMaxStage]
+    uint64_t* staged_empty = staged_full + kZMaxStage;           // [kZMaxStage]
+    uint64_t* acc_full = staged_empty + kZMaxStage;              // [kZMaxAcc]
+    uint64_t* acc_empty = acc_full + kZMaxAcc;                   // [kZMaxAcc]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_empty + kZMaxAcc);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const bool fused = cd.yp != nullptr;
+    const int T = pl.T;
+
+    // ---- setup: stage the packed filter bank (cp.async) in the A ring, expand it
+    // into the B image, thresholds, barriers, TMEM.
+    {
+        int hi_r = 0, lo_r = 0;
+        if (fused && threadIdx.x < K) { hi_r = __ldg(cd.hi + threadIdx.x); lo_r = __ldg(cd.lo + threadIdx.x); }
+        const uint32_t* wsrc[kMaxSeg];
+        uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_a);
+        int ofs = 0;
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+            const int n4 = K * 27 * 2 * cd.seg[sg].cw / 4;
+            const uint4* g = reinterpret_cast<const uint4*>(cd.seg[sg].wp);
+            for (int i = threadIdx.x; i < n4; i += kZThreads)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_wp + ofs + 4 * i)), "l"(g + i)
+                             : "memory");
+            wsrc[sg] = s_wp + ofs;
+            ofs += 4 * n4;
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        if (threadIdx.x < K) {
+            s_nhi[threadIdx.x] = fused ? -hi_r : 0;
+            s_lmh[threadIdx.x] = lo_r - hi_r;
+        }
+        {   // barriers, one per thread
+            const int t = threadIdx.x;
+            if (t < kZMaxSlot) { mbar_init(plane_full + t, kZExpThreads); mbar_init(plane_free + t, 1); }
+            else if (t < kZMaxSlot + kZMaxStage) {
+                mbar_init(staged_full + t - kZMaxSlot, 1);
+                mbar_init(staged_empty + t - kZMaxSlot, kZExpThreads);
+            } else if (t >= 64 && t < 64 + kZMaxAcc) {
+                mbar_init(acc_full + t - 64, 1);
+                mbar_init(acc_empty + t - 64, 128);
+            }
+            if (t < kZMaxSlot + kZMaxStage || (t >= 64 && t < 64 + kZMaxAcc))
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        // B image: MMA m, half h = K-slice j = 2m + h, block b (dz of the block
+        // sequence), row k: 16 channels of W[k][chunk][dz][dy][dx] as int8.
+        const int rows = NB * K;
+        const int total = pl.nmma * 2 * rows;
+        for (int u = threadIdx.x; u < total; u += kZThreads) {
+            const int row = u % rows;
+            const int j = u / rows;                    // slice index (2m + h)
+            const int b = row / K, k = row - b * K;
+            const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            const int tap = pl.sl_tap[j];
+            if (tap >= 0) {
+                int c = pl.sl_chunk[j];
+                const int sg = (NSEG > 1 && c >= pl.cch[0]) ? 1 : 0;
+                if (sg) c -= pl.cch[0];
+                const int cw = cd.seg[sg].cw;
+                const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
+                const int word = c >> 1, sh = 16 * (c & 1);
+                v = expand16(src[word], src[cw + word], sh);
+            }
+            *reinterpret_cast<uint4*>(s_b + static_cast<size_t>(j) * rows * 16 + row * 16) = v;
+        }
+        if (PRED) {
+            for (int i = threadIdx.x; i < cd.nclass; i += kZThreads) s_pred[i] = __ldg(cd.pb + i);
+            // quad tables: entry (mask nibble | sign nibble << 4) = (((t0 w0) + t1 w1) + t2 w2) + t3 w3
+            for (int e = threadIdx.x; e < cd.nclass * (K / 4) * 256; e += kZThreads) {
+                const int idx = e & 255, qd = (e >> 8) % (K / 4), j = e / (256 * (K / 4));
+                float part = 0.0f;
+                for (int i = 0; i < 4; ++i) {
+                    const float wv = __ldg(cd.pw + j * K + 4 * qd + i);
+                    const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
+                    part += nz ? (ps ? wv : -wv) : 0.0f;
+                }
+                s_ptab[e] = part;
+            }
+        }
+        if (warp == kZMmaWarp) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                         "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        fence_proxy_async();   // B image visible to the tensor core
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
+    const uint32_t tmem_base = *s_tmem;
+
+    if (warp < kZEpiWarps) {
+        // ---- initialise this warp's TMEM blocks (its quadrant, its tiles, all RO blocks)
+        const int q = warp & 3, g = warp >> 2;
+        int iv[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) iv[k] = s_nhi[k];
+        for (int t = g; t < T; t += 2)
+            for (int b = 0; b < RO; ++b)
+#pragma unroll
+                for (int c = 0; c < K; c += 16)
+                    tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (t * RO + b) * K + c,
+                              *reinterpret_cast<const int(*)[16]>(iv + c));
+        tmem_wait_st();
+        tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+
+    const uint32_t two_po = 2u * pl.Po;
+    if (warp == kZLoadWarp) {
+        // ================= loader: per plane and segment one bulk copy of the
+        // contiguous packed rows the strip reads (zero-size outside the buffer)
+        if (lane == 0) {
+            ZWalk wk(pl.units, cd.Do, pl.nstrip);
+            int n, strip, zf, zl;
+            uint32_t st = 0, st_r = 0;
+            while (wk.next(n, strip, zf, zl)) {
+                int i0, i1;
+                run_planes(pl, cd, zf, zl, i0, i1);
+                int ya[kMaxSeg], nr[kMaxSeg];
+#pragma unroll
+                for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
+                for (int i = i0; i <= i1; ++i) {
+                    if (st_r > 0) mbar_wait(staged_empty + st, (st_r - 1) & 1);
+                    uint32_t bytes[kMaxSeg];
+                    const uint32_t* src[kMaxSeg];
+                    uint32_t total = 0;
+#pragma unroll
+                    for (int sg = 0; sg < NSEG; ++sg) {
+                        const SegDesc& sd = cd.seg[sg];
+                        const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
+                        const bool ok = zs >= 0 && zs < sd.D && nr[sg] > 0;
+                        bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 8u * sd.cw : 0u;
+                        src[sg] = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw;
+                        total += bytes[sg];
+                    }
+                    mbar_arrive_expect_tx(staged_full + st, total);
+#pragma unroll
+                    for (int sg = 0; sg < NSEG; ++sg)
+                        if (bytes[sg]) bulk_g2s(s_stage + st * pl.stage_bytes + pl.seg_off[sg], src[sg], bytes[sg],
+                                                staged_full + st);
+                    if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
+                }
+            }
+        }
+    } else if (warp >= kZExpWarp0 && warp < kZMmaWarp) {
+        // ================= expanders: staged packed rows -> int8 strip of one plane
+        const int et = threadIdx.x - kZExpWarp0 * 32;
+        ZWalk wk(pl.units, cd.Do, pl.nstrip);
+        int n, strip, zf, zl;
+        uint32_t st = 0, st_r = 0, as = 0, as_r = 0;
+        while (wk.next(n, strip, zf, zl)) {
+            int i0, i1;
+            run_planes(pl, cd, zf, zl, i0, i1);
+            int ya[kMaxSeg], nr[kMaxSeg];
+#pragma unroll
+            for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
+            const int qa = strip * 128 * T - pl.Po - 1;
+            for (int i = i0; i <= i1; ++i) {
+                mbar_wait(staged_full + st, st_r & 1);
+                if (as_r > 0) mbar_wait(plane_free + as, (as_r - 1) & 1);
+                bool zok[kMaxSeg];
+#pragma unroll
+                for (int sg = 0; sg < NSEG; ++sg) {
+                    const SegDesc& sd = cd.seg[sg];
+                    const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
+                    zok[sg] = zs >= 0 && zs < sd.D;
+                }
+                const uint8_t* stg = s_stage + st * pl.stage_bytes;
+                uint8_t* slot = s_a + as * pl.slot_bytes;
+#pragma unroll
+                for (int ph = 0; ph < NPH; ++ph) {
+                    const int py = ph >> 1, px = ph & 1;
+                    for (int r = et; r < pl.RS; r += kZExpThreads) {
+                        const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
+                        const int y = div_po(tq, pl.po_magic) - 2;
+                        const int x = static_cast<int>(tq) - (y + 2) * pl.Po;
+                        int yi = y, xi = x;
+                        if (STR == 2) { yi = 2 * y + py; xi = 2 * x + px; }
+                        const bool v = x < cd.Wo && y >= 0 && yi < cd.Hci && xi < cd.Wci;
+                        uint8_t* dst = slot + (ph * CT) * pl.REG + r * 16;
+#pragma unroll
+                        for (int sg = 0; sg < NSEG; ++sg) {
+                            const SegDesc& sd = cd.seg[sg];
+                            const int ys = sd.up ? (yi >> 1) : yi, xs = sd.up ? (xi >> 1) : xi;
+                            const bool ok = v && zok[sg];
+                            const uint8_t* sp = stg + pl.seg_off[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
+                            const int choff = sg ? pl.cch[0] : 0;
+                            if (sd.cw == 1) {
+                                uint2 w = make_uint2(0u, 0u);
+                                if (ok) w = *reinterpret_cast<const uint2*>(sp);
+                                *reinterpret_cast<uint4*>(dst + choff * pl.REG) = expand16(w.x, w.y, 0);
+                                if (pl.cch[sg] > 1) *reinterpret_cast<uint4*>(dst + (choff + 1) * pl.REG) = expand16(w.x, w.y, 16);
+                            } else {
+                                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                                if (ok) w = *reinterpret_cast<const uint4*>(sp);
+                                const int cch = pl.cch[sg];
+                                *reinterpret_cast<uint4*>(dst + choff * pl.REG) = expand16(w.x, w.z, 0);
+                                if (cch > 1) *reinterpret_cast<uint4*>(dst + (choff + 1) * pl.REG) = expand16(w.x, w.z, 16);
+                                if (cch > 2) *reinterpret_cast<uint4*>(dst + (choff + 2) * pl.REG) = expand16(w.y, w.w, 0);
+                                if (cch > 3) *reinterpret_cast<uint4*>(dst + (choff + 3) * pl.REG) = expand16(w.y, w.w, 16);
+                            }
+                        }
+                    }
+                }
+                mbar_arrive(staged_empty + st);
+                fence_proxy_async();
+                mbar_arrive(plane_full + as);
+                if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
+                if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
+            }
+        }
+    } else if (warp == kZMmaWarp) {
+        // ================= MMA issuer
+        const bool leader = elect_one();
+        const uint32_t a_base = smem_u32(s_a), b_base = smem_u32(s_b);
+        const uint32_t b_half = NB * K * 16;          // LBO of B (bytes between the two K halves)
+        const uint32_t b_mma = 2 * b_half;            // bytes per MMA's B operand
+        ZWalk wk(pl.units, cd.Do, pl.nstrip);
+        int n, strip, zf, zl;
+        uint32_t as = 0, as_r = 0;
+        uint32_t u_run = 0;                            // running output index of the run's first plane
+        while (wk.next(n, strip, zf, zl)) {
+            int i0, i1;
+            run_planes(pl, cd, zf, zl, i0, i1);
+            const int Tv = min(T, pl.NT - strip * T);
+            const int zg0 = cd.zo_beg + zf, zg1 = cd.zo_beg + zl;
+            for (int i = i0; i <= i1; ++i) {
+                // outputs touched by plane i: up to 3 (dz = 2, 1, 0 <-> z = i-1, i, i+1)
+                int zlo, zhi;
+                if (STR == 1) { zlo = max(i - 1, zg0); zhi = min(i + 1, zg1); }
+                else { zlo = max((i - 1 + 1) >> 1, zg0); zhi = min((i + 1) >> 1, zg1); }
+                // (STR 2: outputs z with 2z-1 <= i <= 2z+1 -> (i-1)/2 <= z <= (i+1)/2)
+                const bool full = (STR == 1) ? (zhi - zlo == 2) : (zhi - zlo == 1);
+                mbar_wait(plane_full + as, as_r & 1);
+                const uint32_t a_slot = a_base + as * pl.slot_bytes;
+                for (int t = 0; t < Tv; ++t) {
+                    // first touch of an output: wait until the epilogue drained the block's previous user
+                    for (int z = zlo; z <= zhi; ++z) {
+                        const int first = max(STR * z - 1, 0);
+                        const uint32_t u = u_run + (z - zg0);
+                        if (first == i && u >= static_cast<uint32_t>(RO)) {
+                            const uint32_t sg = u % RO;
+                            mbar_wait(acc_empty + sg * T + t, ((u / RO) - 1) & 1);
+                        }
+                    }
+                    tc_fence_after();
+                    if (leader) {
+                        const uint32_t a_tile = a_slot + t * 128 * 16;
+                        const uint32_t d_tile = tmem_base + t * RO * K;
+                        if (full) {
+                            // rotation: block position p holds output with sigma = p
+                            const uint32_t u_lo = u_run + (zlo - zg0);
+                            int b0;
+                            if (STR == 1) {
+                                const int r = u_lo % 3;           // sigma of z = i-1
+                                b0 = r == 0 ? 0 : (r == 1 ? 2 : 1);
+                            } else {
+                                b0 = (u_lo & 1) ? 0 : 1;          // sigma(z) = 1 -> [dz0 dz2]; 0 -> [dz2 dz0]
+                            }
+                            const uint32_t idesc = idesc_i8(RO * K);
+#pragma unroll 1
+                            for (int m = 0; m < pl.nmma; ++m)
+                                tc_mma_i8(d_tile, umma_desc_lbo(a_tile + pl.a_off[m], pl.a_lbo[m]),
+                                          umma_desc_lbo(b_base + m * b_mma + b0 * K * 16, b_half), idesc, 1u);
+                        } else {
+                            const uint32_t idesc = idesc_i8(K);
+                            for (int z = zlo; z <= zhi; ++z) {
+                                const uint32_t u = u_run + (z - zg0);
+                                const int dz = i - STR * z + 1;
+                                // block holding dz: s1 [2 1 0 ..] -> 2 - dz; s2 [0 2 0 1] -> dz0:0 dz2:1 dz1:3
+                                const int b = STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
+#pragma unroll 1
+                                for (int m = 0; m < pl.nmma; ++m)
+                                    tc_mma_i8(d_tile + (u % RO) * K, umma_desc_lbo(a_tile + pl.a_off[m], pl.a_lbo[m]),
+                                              umma_desc_lbo(b_base + m * b_mma + b * K * 16, b_half), idesc, 1u);
+                            }
+                        }
+                        // outputs whose last plane is i are complete for this tile
+                        for (int z = zlo; z <= zhi; ++z) {
+                            const int last = min(STR * z + 1, cd.Dci - 1);
+                            if (last == i) {
+                                const uint32_t u = u_run + (z - zg0);
+                                tc_commit(acc_full + (u % RO) * T + t);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (leader) tc_commit(plane_free + as);
+                __syncwarp();
+                if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
+            }
+            u_run += zl - zf + 1;
+        }
+    } else {
+        // ================= epilogue
+        const int q = warp & 3, g = warp >> 2;
+        ZWalk wk(pl.units, cd.Do, pl.nstrip);
+        int n, strip, zf, zl;
+        uint32_t u = 0;
+        const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
+        while (wk.next(n, strip, zf, zl)) {
+            const int Tv = min(T, pl.NT - strip * T);
+            for (int z = zf; z <= zl; ++z, ++u) {
+                const uint32_t sgm = u % RO, par = (u / RO) & 1;
+                for (int t = g; t < Tv; t += 2) {
+                    mbar_wait(acc_full + sgm * T + t, par);
+                    tc_fence_after();
+                    const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
+                    const int qpos = strip * 128 * T + t * 128 + 32 * q + lane;
+                    const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
+                    const int x = qpos - y * pl.Po;
+                    const bool vpos = x < cd.Wo && y < cd.Ho;
+                    const int64_t vox = ((static_cast<int64_t>(n) * cd.Do + z) * cd.Ho + y) * cd.Wo + x;
+                    uint32_t sbits[CWO], mbits[CWO];
+#pragma unroll
+                    for (int c = 0; c < K; c += 16) {
+                        int acc[16];
+                        tmem_ld16(taddr + c, acc);
+                        tmem_wait_ld();
+                        if (fused) {
+                            // acc holds acc - hi (initialised to -hi).  A4 (reading R5):
+                            // +1 if acc >= hi; else -1 if acc <= lo; else 0.  Bit k of nhi =
+                            // (acc_k < hi_k); bit k of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).
+                            uint32_t nhi = 0u, nlo = 0u;
+#pragma unroll
+                            for (int i4 = 3; i4 >= 0; --i4) {
+                                const int4 l4 = *reinterpret_cast<const int4*>(s_lmh + c + 4 * i4);
+                                const int ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                                for (int i = 3; i >= 0; --i) {
+                                    const int d = acc[4 * i4 + i];
+                                    nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
+                                    nlo = __funnelshift_l(static_cast<uint32_t>(ll[i] - d), nlo, 1);
+                                }
+                            }
+                            const int w = c >> 5, sh = c & 31;
+                            const uint32_t sb = (~nhi & 0xFFFFu) << sh, mb = (~(nhi & nlo) & 0xFFFFu) << sh;
+                            if (sh == 0) { sbits[w] = sb; mbits[w] = mb; }
+                            else { sbits[w] |= sb; mbits[w] |= mb; }
+                        } else if (vpos) {
+                            int4* dst = reinterpret_cast<int4*>(cd.y + vox * K + c);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+                        }
+                        // re-initialise the block for the output that reuses it
+#pragma unroll
+                        for (int i4 = 0; i4 < 4; ++i4) {
+                            const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
+                            acc[4 * i4] = h4.x; acc[4 * i4 + 1] = h4.y; acc[4 * i4 + 2] = h4.z; acc[4 * i4 + 3] = h4.w;
+                        }
+                        tmem_st16(taddr + c, acc);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(acc_empty + sgm * T + t);
+                    if (fused && vpos) {
+                        if (PRED) {
+                            // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
+                            const int64_t v = (static_cast<int64_t>(z) * cd.Ho + y) * cd.Wo + x;
+                            for (int j = 0; j < cd.nclass; ++j) {
+                                float a = s_pred[j];
+                                const float* tab = s_ptab + j * (K / 4) * 256;
+#pragma unroll
+                                for (int qd = 0; qd < K / 4; ++qd) {
+                                    const uint32_t w = qd >> 3, sh = 4 * (qd & 7);
+                                    const uint32_t idx = ((mbits[w] >> sh) & 0xFu) | (((sbits[w] >> sh) & 0xFu) << 4);
+                                    a += tab[qd * 256 + idx];
+                                }
+                                cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
+                            }
+                        }
+                        uint32_t* dst = cd.yp + vox * 2 * CWO;
+                        if constexpr (CWO == 1) {
+                            *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
+                        } else {
+                            *reinterpret_cast<uint4*>(dst) = make_uint4(sbits[0], sbits[1], mbits[0], mbits[1]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kZMmaWarp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+int g_num_sms_z = 0;
+
+}  // namespace
+
+// ---------------------------------------------------------------- host plan
+static int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+static size_t tz_smem(const TzPlan& pl, int K) {
+    return static_cast<size_t>(pl.nslot) * pl.slot_bytes + pl.b_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
+           2 * K * sizeof(int) + (kZMaxClass + pl.ptab_floats) * sizeof(float) +
+           (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
+}
+
+static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
+    constexpr size_t kSmemMax = 227 * 1024;
+    if (cd.nseg < 1 || cd.nseg > 2 || cd.y_in != nullptr) return false;
+    for (int a = 0; a < 3; ++a)
+        if (cd.s[a] != cd.s[0] || cd.p[a] != 1 || cd.dl[a] != 1) return false;
+    pl.s = cd.s[0];
+    if (pl.s != 1 && !(pl.s == 2 && cd.nseg == 1 && cd.seg[0].up == 0)) return false;
+    if (cd.K != 16 && cd.K != 32 && cd.K != 64) return false;
+    if (cd.logits != nullptr && (cd.K > 32 || cd.nclass < 1 || cd.nclass > kZMaxClass || cd.yp == nullptr ||
+                                 cd.nclass * cd.K > 64))
+        return false;
+    int ct = 0;
+    pl.cch[1] = 0;
+    for (int i = 0; i < cd.nseg; ++i) {
+        const SegDesc& sd = cd.seg[i];
+        if (sd.c <= 0 || sd.c % 16 != 0 || (sd.c + 31) / 32 != sd.cw || sd.W % 2 != 0) return false;
+        if ((reinterpret_cast<uintptr_t>(sd.xp) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
+        pl.cch[i] = sd.c / 16;
+        ct += pl.cch[i];
+    }
+    if (ct > 4) return false;
+    if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
+        cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
+        return false;
+    if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
+    pl.RO = pl.s == 1 ? 3 : 2;
+    pl.nph = pl.s == 1 ? 1 : 4;
+    pl.NB = pl.s == 1 ? 5 : 4;
+    pl.Po = cd.Wo + 1;
+    const int64_t npo = static_cast<int64_t>(cd.Ho) * pl.Po;
+    if (npo + 4 * pl.Po > (1 << 22) || pl.Po > 1024) return false;   // div_po range: q * Po < 2^32
+    pl.NPo = static_cast<int>(npo);
+    pl.NT = (pl.NPo + 127) / 128;
+    pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
+
+    // K-slices: (tap, chunk) -> byte offset within an A slot (for a given REG),
+    // sorted ascending and paired into MMAs.  Offsets depend on REG, so the order
+    // is taken on phase/chunk/row keys that are REG-independent (REG > any row offset).
+    struct Sl { int ph, ch, row, tap; };
+    std::vector<Sl> sl;
+    for (int dy = 0; dy < 3; ++dy)
+        for (int dx = 0; dx < 3; ++dx) {
+            int ph = 0, oy = dy, ox = dx;
+            if (pl.s == 2) {
+                const int py = dy == 1 ? 0 : 1, px = dx == 1 ? 0 : 1;
+                oy = dy == 0 ? 0 : 1;
+                ox = dx == 0 ? 0 : 1;
+                ph = py * 2 + px;
+            }
+            for (int c = 0; c < ct; ++c) sl.push_back({ph, c, oy * pl.Po + ox, dy * 3 + dx});
+        }
+    std::sort(sl.begin(), sl.end(), [](const Sl& a, const Sl& b) {
+        if (a.ph != b.ph) return a.ph < b.ph;
+        if (a.ch != b.ch) return a.ch < b.ch;
+        return a.row < b.row;
+    });
+    pl.nmma = static_cast<int>((sl.size() + 1) / 2);
+    if (pl.nmma > kZMaxMma) return false;
+    pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
+    const int ptab = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
+    pl.ptab_floats = ptab;
+
+    // strip size: the most tiles that fit TMEM (RO*K*T <= 512) and shared memory
+    const int tmax = std::min(512 / (pl.RO * cd.K), kZMaxAcc / pl.RO);
+    bool ok = false;
+    for (int T = std::min(tmax, pl.NT); T >= 1 && !ok; --T) {
+        pl.T = T;
+        pl.nstrip = (pl.NT + T - 1) / T;
+        pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.Po + 2 : pl.Po + 1);
+        pl.REG = round_up(pl.RS * 16, 128);
+        pl.slot_bytes = pl.nph * ct * pl.REG + 256;
+        // staging: the most rows any strip reads, per segment
+        int off = 0;
+        for (int sg = 0; sg < cd.nseg; ++sg) {
+            const SegDesc& sd = cd.seg[sg];
+            int maxr = 0;
+            for (int st = 0; st < pl.nstrip; ++st) {
+                const int qa = st * 128 * T - pl.Po - 1, qb = qa + pl.RS - 1;
+                int ylo = (qa + 2 * pl.Po) / pl.Po - 2, yhi = (qb + 2 * pl.Po) / pl.Po - 2;
+                if (pl.s == 2) { ylo *= 2; yhi = 2 * yhi + 1; }
+                ylo = std::max(ylo, 0);
+                yhi = std::min(yhi, cd.Hci - 1);
+                if (sd.up) { ylo >>= 1; yhi >>= 1; }
+                yhi = std::min(yhi, sd.H - 1);
+                maxr = std::max(maxr, yhi - ylo + 1);
+            }
+            pl.seg_off[sg] = off;
+            off += round_up(maxr * sd.W * 8 * sd.cw, 128);
+        }
+        pl.stage_bytes = off;
+        // packed filter bank staged in the A ring during setup
+        int wbytes = 0;
+        for (int sg = 0; sg < cd.nseg; ++sg) wbytes += cd.K * 27 * 2 * cd.seg[sg].cw * 4;
+        for (int ns = 3; ns >= 2 && !ok; --ns)
+            for (int nst = kZMaxStage; nst >= 2 && !ok; --nst) {
+                pl.nslot = ns;
+                pl.nstage = nst;
+                if (tz_smem(pl, cd.K) <= kSmemMax && pl.nslot * pl.slot_bytes >= wbytes) ok = true;
+            }
+    }
+    if (!ok) return false;
+    for (size_t j = 0; j < 2 * static_cast<size_t>(pl.nmma); ++j) {
+        if (j < sl.size()) {
+            pl.sl_tap[j] = static_cast<int8_t>(sl[j].tap);
+            pl.sl_chunk[j] = static_cast<int8_t>(sl[j].ch);
+        } else {
+            pl.sl_tap[j] = -1;
+            pl.sl_chunk[j] = 0;
+        }
+    }
+    auto addr = [&](size_t j) { return (sl[j].ph * ct + sl[j].ch) * pl.REG + sl[j].row * 16; };
+    for (int m = 0; m < pl.nmma; ++m) {
+        const int a0 = addr(2 * m);
+        const int a1 = (2 * m + 1 < static_cast<int>(sl.size())) ? addr(2 * m + 1) : a0 + 16;   // zero-weight dummy
+        if (a1 <= a0 || a1 - a0 > 0x3FFF * 16) return false;
+        pl.a_off[m] = a0;
+        pl.a_lbo[m] = a1 - a0;
+    }
+    pl.units = static_cast<int64_t>(cd.N) * pl.nstrip * cd.Do;
+    return pl.units > 0;
+}
+
+template <int K>
+static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int grid, size_t smem, cudaStream_t st) {
+    void (*kern)(ConvDesc, TzPlan) = nullptr;
+    const bool pred = cd.logits != nullptr;
+#define TZ_PICK(CT_, NSEG_, STR_)                                                                     \
+    if (ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                                \
+        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32)> : conv_tz_kernel<K, CT_, NSEG_, STR_, false>;
+    TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(4, 1, 1)
+    TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
+    TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(4, 1, 2)
+#undef TZ_PICK
+    if (kern == nullptr) return cudaErrorNotSupported;
+    static void* configured[64] = {nullptr};
+    bool done = false;
+    for (void* f : configured) done = done || f == reinterpret_cast<void*>(kern);
+    if (!done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        for (void*& f : configured)
+            if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
+    }
+    kern<<<grid, kZThreads, smem, st>>>(cd, pl);
+    return cudaGetLastError();
+}
+
+static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
+    int ct = 0;
+    for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
+    if (pl.s == 2) return cd.nseg == 1 && (ct == 1 || ct == 2 || ct == 4);
+    if (cd.nseg == 1) return ct == 1 || ct == 2 || ct == 4;
+    return ct >= 2;
+}
+
+bool conv_tz_supported(const ConvDesc& cd) {
+    TzPlan pl{};
+    if (!plan_tz(cd, pl)) return false;
+    return tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024;
+}
+
+cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st) {
+    TzPlan pl{};
+    if (!plan_tz(cd, pl) || !tz_instantiated(cd, pl)) return cudaErrorNotSupported;
+    const size_t smem = tz_smem(pl, cd.K);
+    if (g_num_sms_z == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms_z, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int cap = persistent_grid_cap() > 0 ? std::min(persistent_grid_cap(), g_num_sms_z) : g_num_sms_z;
+    const int grid = static_cast<int>(std::min<int64_t>(pl.units, cap));
+    int ct = 0;
+    for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
+    switch (cd.K) {
+        case 16: return launch_tz_k<16>(cd, pl, ct, grid, smem, st);
+        case 32: return launch_tz_k<32>(cd, pl, ct, grid, smem, st);
+        case 64: return launch_tz_k<64>(cd, pl, ct, grid, smem, st);
+    }
+    return cudaErrorNotSupported;
+}
+
+}  // namespace tn

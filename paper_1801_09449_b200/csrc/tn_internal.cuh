@@ -93,6 +93,12 @@ cudaError_t launch_conv_first(const FirstDesc& fd, cudaStream_t s);
 // outside what the kernel handles (caller then uses the popc kernel).
 bool        conv_tc_supported(const ConvDesc& cd);
 cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
+// tcgen05 tap-offset, z-merged implicit GEMM (conv_tz.cu): C, K <= 64 with a
+// small filter bank; same contract.
+bool        conv_tz_supported(const ConvDesc& cd);
+// tn_set_grid_cap: upper bound on the persistent tensor-core grids (0 = #SMs).
+int         persistent_grid_cap();
+cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s);
 
 }  // namespace tn
 

@@ -24,22 +24,29 @@ def tn():
     return tn
 
 
-@pytest.fixture(params=["popc", "tc", "auto"])
+SELECTORS = {"popc": 1, "tc": 2, "tz": 3, "auto": 0, "tz_cap3": 3, "tc_cap3": 2}
+
+
+@pytest.fixture(params=["popc", "tc", "tz", "auto", "tz_cap3", "tc_cap3"])
 def kernel(request, tn):
-    """Run a conv test with the CUDA-core popc kernel, the tcgen05 kernel (skipped
-    for shapes it does not cover), or the automatic choice."""
-    sel = {"popc": tn.TN_KERNEL_POPC, "tc": tn.TN_KERNEL_TC, "auto": tn.TN_KERNEL_AUTO}[request.param]
-    tn.tn_set_conv_kernel(sel)
+    """Run a conv test with the CUDA-core popc kernel, one of the tcgen05 kernels
+    (skipped for shapes it does not cover), or the automatic choice.  The _cap3
+    variants cap the persistent grid at 3 CTAs, so each CTA walks long runs of
+    output planes (TMEM block rotation, ring wrap-around, run boundaries)."""
+    tn.tn_set_conv_kernel(SELECTORS[request.param])
+    tn.tn_set_grid_cap(3 if request.param.endswith("cap3") else 0)
     yield request.param
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+    tn.tn_set_grid_cap(0)
 
 
-@pytest.fixture(params=["popc", "auto"])
+@pytest.fixture(params=["popc", "tc", "auto", "auto_cap5"])
 def fcn_kernel(request, tn):
-    sel = {"popc": tn.TN_KERNEL_POPC, "auto": tn.TN_KERNEL_AUTO}[request.param]
-    tn.tn_set_conv_kernel(sel)
+    tn.tn_set_conv_kernel({"popc": 1, "tc": 2, "auto": 0, "auto_cap5": 0}[request.param])
+    tn.tn_set_grid_cap(5 if request.param.endswith("cap5") else 0)
     yield request.param
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+    tn.tn_set_grid_cap(0)
 
 
 def run_or_skip(kernel, fn, *a, **kw):
@@ -47,8 +54,8 @@ def run_or_skip(kernel, fn, *a, **kw):
     try:
         return fn(*a, **kw)
     except tn.TNError as e:
-        if kernel == "tc" and e.status == tn.TN_EUNSUPPORTED:
-            pytest.skip("shape outside the tcgen05 kernel")
+        if kernel.startswith(("tc", "tz")) and e.status == tn.TN_EUNSUPPORTED:
+            pytest.skip("shape outside this tcgen05 kernel")
         raise
 
 
@@ -144,6 +151,14 @@ CONV_CASES = [
     ((1, 128, 4, 5, 6), 16, 1, 1, 1),            # 4 words
     ((1, 16, 5, 6, 7), 7, (1, 2, 1), (0, 1, 2), (1, 1, 2)),  # anisotropic geometry
     ((1, 16, 1, 1, 1), 16, 1, 1, 1),             # a single voxel
+    # tap-offset z-merged kernel (TZ) shapes: even W, C <= 64, small filter banks
+    ((1, 16, 9, 17, 34), 16, 1, 1, 1),           # ragged tiles and strips
+    ((2, 32, 7, 10, 22), 32, 1, 1, 1),
+    ((1, 64, 6, 10, 12), 32, 1, 1, 1),           # 4 chunks, K = 32
+    ((1, 32, 5, 6, 8), 64, 1, 1, 1),             # K = 64
+    ((1, 16, 12, 18, 20), 16, 2, 1, 1),          # stride 2, phase images
+    ((2, 32, 9, 14, 10), 32, 2, 1, 1),           # stride 2, odd depth
+    ((1, 16, 3, 130, 140), 16, 1, 1, 1),         # several strips per plane
 ]
 
 
@@ -164,7 +179,7 @@ def test_conv3d_int32_matches_oracle(tn, kernel, case):
     np.testing.assert_array_equal(y.cpu().numpy(), ref.transpose(0, 2, 3, 4, 1))
 
 
-@pytest.mark.parametrize("case", CONV_CASES[:7], ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}")
+@pytest.mark.parametrize("case", CONV_CASES[:7] + CONV_CASES[11:], ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}")
 def test_conv3d_requant_matches_oracle(tn, kernel, case):
     shape, k, s, p, dl = case
     x, w = _case(shape, k, seed=7 + shape[2])
@@ -196,7 +211,8 @@ def test_requant_sentinels_and_order(tn):
 
 # --------------------------------------------------------------------------- A6 upsample + concat
 @pytest.mark.parametrize("low,cl,cs,k", [((3, 4, 5), 16, 16, 16), ((2, 3, 9), 64, 64, 64),
-                                         ((4, 4, 4), 32, 32, 32), ((1, 1, 1), 16, 16, 8)])
+                                         ((4, 4, 4), 32, 32, 32), ((1, 1, 1), 16, 16, 8),
+                                         ((5, 6, 7), 16, 16, 16), ((3, 5, 4), 32, 32, 32), ((4, 3, 6), 16, 32, 16)])
 def test_conv3d_upsample_concat_matches_oracle(tn, kernel, low, cl, cs, k):
     n = 1
     a = synth.ternary_codes((n, cl) + low, 0.5, seed=cl)
@@ -318,6 +334,48 @@ def test_c1_full_size_sampled(tn):
     # the int32 and packed outputs agree everywhere (requant of the full int32 tensor)
     y_t = torch.from_numpy(y).cuda()
     np.testing.assert_array_equal(u32(tn.tn_requant(y_t, dev(lo), dev(hi))), yp)
+
+
+# The FCN's full-resolution layers of configs[3] (1 x C x 128 x 256 x 256) through
+# every tensor-core kernel that covers them, in the persistent launch the FCN uses:
+# sampled outputs against the oracle's per-output sum + the packed/int32 agreement.
+C3_LAYER_CASES = [
+    # (C, K, stride, kernel)
+    (16, 16, 1, "tz"), (16, 16, 1, "tc"), (16, 16, 2, "tz"), (16, 16, 2, "tc"), (16, 32, 1, "tz"),
+]
+
+
+@pytest.mark.parametrize("case", C3_LAYER_CASES, ids=lambda c: f"c{c[0]}_k{c[1]}_s{c[2]}_{c[3]}")
+def test_c3_layer_full_size_sampled(tn, case):
+    c, k, s, kern = case
+    shape = (1, c, 128, 256, 256)
+    x = synth.ternary_codes(shape, 0.5, seed=31 + c + k + s)
+    w = synth.ternary_codes((k, c, 3, 3, 3), 0.6, seed=32 + c + k + s)
+    lo, hi = synth.jittered_thresholds(k, synth.threshold_base(c, 0.5), seed=33)
+    tn.tn_set_conv_kernel(SELECTORS[kern])
+    try:
+        xp = tn.tn_pack_i8(dev(x))
+        wp = tn.tn_pack_weights(dev(w))
+        xd = tn.dims(*shape)
+        yp = u32(tn.tn_conv3d_requant(xp, xd, wp, k, tn.geom(s), dev(lo), dev(hi)))
+        y = tn.tn_conv3d(xp, xd, wp, k, tn.geom(s)).cpu().numpy()
+    finally:
+        tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+    do, ho, wo = y.shape[1:4]
+    g = synth.rng(98)
+    m = 4096
+    at = np.stack([np.zeros(m, int), g.integers(0, k, m), g.integers(0, do, m), g.integers(0, ho, m),
+                   g.integers(0, wo, m)], 1).astype(np.int32)
+    at[:8, 2:] = [[0, 0, 0], [do - 1, ho - 1, wo - 1], [0, ho - 1, 0], [do - 1, 0, wo - 1], [do // 2, 0, wo // 2],
+                  [do // 2, ho - 1, wo // 2], [0, ho // 2, wo // 2], [do - 1, ho // 2, wo // 2]]
+    ref_acc = oracle.conv3d_at(x, w, at, s)
+    n_, k_, z_, y_, x_ = at.T
+    np.testing.assert_array_equal(y[n_, z_, y_, x_, k_], ref_acc)
+    ref_t = np.where(ref_acc >= hi[k_], 1, np.where(ref_acc <= lo[k_], -1, 0))
+    s_bit = (yp[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
+    m_bit = (yp[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
+    np.testing.assert_array_equal(np.where(m_bit == 1, np.where(s_bit == 1, 1, -1), 0), ref_t)
+    np.testing.assert_array_equal(u32(tn.tn_requant(torch.from_numpy(y).cuda(), dev(lo), dev(hi))), yp)
 
 
 # --------------------------------------------------------------------------- configs[4]: z-slabs
