@@ -204,10 +204,8 @@ tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int
 // TN_KERNEL_TC (dx-merged tensor-core kernel), then the CUDA-core popc kernel;
 // a forced selector only takes its own kernel.  -1 if nothing covers the shape.
 static int pick_kernel(const ConvDesc& cd, int mode) {
-    // AUTO: TZ for stride 2 (measured faster there), TC, then TZ
-    if ((mode == TN_KERNEL_TZ || (mode == TN_KERNEL_AUTO && cd.s[0] == 2)) && conv_tz_supported(cd)) return TN_KERNEL_TZ;
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ) && conv_tz_supported(cd)) return TN_KERNEL_TZ;
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TC) && conv_tc_supported(cd)) return TN_KERNEL_TC;
-    if (mode == TN_KERNEL_AUTO && conv_tz_supported(cd)) return TN_KERNEL_TZ;
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC) && cd.y_in == nullptr && cd.logits == nullptr)
         return TN_KERNEL_POPC;
     return -1;

@@ -36,12 +36,13 @@
 // accumulator holds acc - hi and the A4 compare is a sign bit), so the MMAs always
 // accumulate.
 //
-// CTA = 18 warps, persistent, one per SM:
+// CTA = 19 warps, persistent, one per SM:
 //   warps 0-7   epilogue, two groups of four (one warp per TMEM lane quadrant);
 //               group g takes the tiles t % 2 == g of every output plane
 //   warps 8-15  expanders: packed rows (staging) -> int8 A strip of one plane
-//   warp 16     MMA issuer (one elected lane issues; the warp walks the schedule)
-//   warp 17     loader: one elected lane issues 1-D bulk copies (cp.async.bulk)
+//   warps 16-17 MMA issuers: one elected lane of warp 16 + w runs the schedule of
+//               the tiles t % 2 == w (waits, tcgen05.mma, commits)
+//   warp 18     loader: one elected lane issues 1-D bulk copies (cp.async.bulk)
 //               of the contiguous packed rows a strip needs, per plane and segment
 #include "tn_internal.cuh"
 #include "tc_ptx.cuh"
@@ -50,6 +51,27 @@
 #include <climits>
 #include <vector>
 
+#ifndef TN_EXP_PROF
+#define TN_EXP_PROF 0
+#endif
+#if TN_EXP_PROF
+__device__ long long g_tztrace[148 * 16];
+#define ZSTAMP(v) long long v = clock64()
+#define ZACC(acc, t0) acc += clock64() - (t0)
+#else
+#define ZSTAMP(v) do { } while (0)
+#define ZACC(acc, t0) do { } while (0)
+#endif
+#ifndef TZ_EXP_NOEPI
+#define TZ_EXP_NOEPI 0
+#endif
+#ifndef TZ_EXP_NOEXP
+#define TZ_EXP_NOEXP 0
+#endif
+#ifndef TZ_WAIT
+#define TZ_WAIT mbar_wait
+#endif
+
 namespace tn {
 namespace {
 
@@ -57,7 +79,8 @@ constexpr int kZEpiWarps = 8;
 constexpr int kZExpWarps = 8;
 constexpr int kZExpWarp0 = kZEpiWarps;
 constexpr int kZMmaWarp = kZEpiWarps + kZExpWarps;
-constexpr int kZLoadWarp = kZMmaWarp + 1;
+constexpr int kZMmaWarps = 2;         // two issuers (tiles t % 2): one thread cannot keep up with N = 3K MMAs
+constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
 constexpr int kZThreads = (kZLoadWarp + 1) * 32;
 constexpr int kZExpThreads = kZExpWarps * 32;
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
@@ -86,6 +109,7 @@ struct TzPlan {
     int b_bytes;
     int64_t units;          // N * nstrip * Do
     uint32_t po_magic;      // ceil(2^32 / Po)
+    int step_q, step_r;     // 256 rows (one expander sweep) = step_q raster rows + step_r positions
     int ptab_floats;
 };
 
@@ -192,7 +216,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         }
         {   // barriers, one per thread
             const int t = threadIdx.x;
-            if (t < kZMaxSlot) { mbar_init(plane_full + t, kZExpThreads); mbar_init(plane_free + t, 1); }
+            if (t < kZMaxSlot) { mbar_init(plane_full + t, kZExpThreads); mbar_init(plane_free + t, kZMmaWarps); }
             else if (t < kZMaxSlot + kZMaxStage) {
                 mbar_init(staged_full + t - kZMaxSlot, 1);
                 mbar_init(staged_empty + t - kZMaxSlot, kZExpThreads);
@@ -275,6 +299,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         // ================= loader: per plane and segment one bulk copy of the
         // contiguous packed rows the strip reads (zero-size outside the buffer)
         if (lane == 0) {
+#if TN_EXP_PROF
+            long long l_wait = 0;
+            const long long l_begin = clock64();
+#endif
             ZWalk wk(pl.units, cd.Do, pl.nstrip);
             int n, strip, zf, zl;
             uint32_t st = 0, st_r = 0;
@@ -285,7 +313,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
                 for (int i = i0; i <= i1; ++i) {
-                    if (st_r > 0) mbar_wait(staged_empty + st, (st_r - 1) & 1);
+                    ZSTAMP(w0);
+                    if (st_r > 0) TZ_WAIT(staged_empty + st, (st_r - 1) & 1);
+                    ZACC(l_wait, w0);
                     uint32_t bytes[kMaxSeg];
                     const uint32_t* src[kMaxSeg];
                     uint32_t total = 0;
@@ -306,10 +336,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                 }
             }
+#if TN_EXP_PROF
+            g_tztrace[16 * blockIdx.x + 0] = clock64() - l_begin;
+            g_tztrace[16 * blockIdx.x + 1] = l_wait;
+#endif
         }
     } else if (warp >= kZExpWarp0 && warp < kZMmaWarp) {
         // ================= expanders: staged packed rows -> int8 strip of one plane
         const int et = threadIdx.x - kZExpWarp0 * 32;
+#if TN_EXP_PROF
+        long long e_w1 = 0, e_w2 = 0, e_planes = 0;
+        const long long e_begin = clock64();
+#endif
         ZWalk wk(pl.units, cd.Do, pl.nstrip);
         int n, strip, zf, zl;
         uint32_t st = 0, st_r = 0, as = 0, as_r = 0;
@@ -321,8 +359,15 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
             const int qa = strip * 128 * T - pl.Po - 1;
             for (int i = i0; i <= i1; ++i) {
-                mbar_wait(staged_full + st, st_r & 1);
-                if (as_r > 0) mbar_wait(plane_free + as, (as_r - 1) & 1);
+                ZSTAMP(x0);
+                TZ_WAIT(staged_full + st, st_r & 1);
+                ZACC(e_w1, x0);
+                ZSTAMP(x1);
+                if (as_r > 0) TZ_WAIT(plane_free + as, (as_r - 1) & 1);
+                ZACC(e_w2, x1);
+#if TN_EXP_PROF
+                ++e_planes;
+#endif
                 bool zok[kMaxSeg];
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) {
@@ -332,16 +377,22 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }
                 const uint8_t* stg = s_stage + st * pl.stage_bytes;
                 uint8_t* slot = s_a + as * pl.slot_bytes;
+                // Rows r = et + 256 j: (y, x) of the output raster tracked incrementally
+                // (256 = qd * Po + rd), all phases of a row from the same (y, x).
+                int r = TZ_EXP_NOEXP ? pl.RS : et;
+                int y, x;
+                {
+                    const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
+                    y = div_po(tq, pl.po_magic) - 2;
+                    x = static_cast<int>(tq) - (y + 2) * pl.Po;
+                }
+                for (; r < pl.RS; r += kZExpThreads) {
+                    const bool vx = x < cd.Wo && y >= 0;
 #pragma unroll
-                for (int ph = 0; ph < NPH; ++ph) {
-                    const int py = ph >> 1, px = ph & 1;
-                    for (int r = et; r < pl.RS; r += kZExpThreads) {
-                        const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
-                        const int y = div_po(tq, pl.po_magic) - 2;
-                        const int x = static_cast<int>(tq) - (y + 2) * pl.Po;
-                        int yi = y, xi = x;
-                        if (STR == 2) { yi = 2 * y + py; xi = 2 * x + px; }
-                        const bool v = x < cd.Wo && y >= 0 && yi < cd.Hci && xi < cd.Wci;
+                    for (int ph = 0; ph < NPH; ++ph) {
+                        const int py = ph >> 1, px = ph & 1;
+                        const int yi = STR == 2 ? 2 * y + py : y, xi = STR == 2 ? 2 * x + px : x;
+                        const bool v = vx && yi < cd.Hci && xi < cd.Wci;
                         uint8_t* dst = slot + (ph * CT) * pl.REG + r * 16;
 #pragma unroll
                         for (int sg = 0; sg < NSEG; ++sg) {
@@ -366,6 +417,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             }
                         }
                     }
+                    x += pl.step_r;
+                    y += pl.step_q;
+                    if (x >= pl.Po) { x -= pl.Po; ++y; }
                 }
                 mbar_arrive(staged_empty + st);
                 fence_proxy_async();
@@ -374,92 +428,140 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
             }
         }
-    } else if (warp == kZMmaWarp) {
-        // ================= MMA issuer
+#if TN_EXP_PROF
+        if (et == 0) {
+            g_tztrace[16 * blockIdx.x + 2] = clock64() - e_begin;
+            g_tztrace[16 * blockIdx.x + 3] = e_w1;
+            g_tztrace[16 * blockIdx.x + 4] = e_w2;
+            g_tztrace[16 * blockIdx.x + 5] = e_planes;
+        }
+#endif
+    } else if (warp >= kZMmaWarp && warp < kZMmaWarp + kZMmaWarps) {
+        // ================= MMA issuers (warp mw takes the tiles t % 2 == mw).  Descriptor low words are precomputed per
+        // K-slice pair (start address and LBO); per (slot, tile) only an add remains,
+        // so the issue loop stays well under the 40+ cycles one N = 3K MMA takes.
+        constexpr int NMMA = (9 * CT + 1) / 2;
         const bool leader = elect_one();
+#if TN_EXP_PROF
+        long long m_w1 = 0, m_w2 = 0;
+        const long long m_begin = clock64();
+#endif
         const uint32_t a_base = smem_u32(s_a), b_base = smem_u32(s_b);
         const uint32_t b_half = NB * K * 16;          // LBO of B (bytes between the two K halves)
-        const uint32_t b_mma = 2 * b_half;            // bytes per MMA's B operand
-        ZWalk wk(pl.units, cd.Do, pl.nstrip);
-        int n, strip, zf, zl;
-        uint32_t as = 0, as_r = 0;
-        uint32_t u_run = 0;                            // running output index of the run's first plane
-        while (wk.next(n, strip, zf, zl)) {
-            int i0, i1;
-            run_planes(pl, cd, zf, zl, i0, i1);
-            const int Tv = min(T, pl.NT - strip * T);
-            const int zg0 = cd.zo_beg + zf, zg1 = cd.zo_beg + zl;
-            for (int i = i0; i <= i1; ++i) {
-                // outputs touched by plane i: up to 3 (dz = 2, 1, 0 <-> z = i-1, i, i+1)
-                int zlo, zhi;
-                if (STR == 1) { zlo = max(i - 1, zg0); zhi = min(i + 1, zg1); }
-                else { zlo = max((i - 1 + 1) >> 1, zg0); zhi = min((i + 1) >> 1, zg1); }
-                // (STR 2: outputs z with 2z-1 <= i <= 2z+1 -> (i-1)/2 <= z <= (i+1)/2)
-                const bool full = (STR == 1) ? (zhi - zlo == 2) : (zhi - zlo == 1);
-                mbar_wait(plane_full + as, as_r & 1);
-                const uint32_t a_slot = a_base + as * pl.slot_bytes;
-                for (int t = 0; t < Tv; ++t) {
-                    // first touch of an output: wait until the epilogue drained the block's previous user
-                    for (int z = zlo; z <= zhi; ++z) {
-                        const int first = max(STR * z - 1, 0);
-                        const uint32_t u = u_run + (z - zg0);
-                        if (first == i && u >= static_cast<uint32_t>(RO)) {
+        const uint32_t b_mma16 = (2 * b_half) >> 4;   // descriptor step per MMA's B operand
+        uint32_t a_lo[NMMA];
+#pragma unroll
+        for (int m = 0; m < NMMA; ++m)
+            a_lo[m] = (((a_base + pl.a_off[m]) >> 4) & 0x3FFFu) | ((static_cast<uint32_t>(pl.a_lbo[m]) >> 4) << 16);
+        const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | ((b_half >> 4) << 16);
+        auto desc64 = [](uint32_t lo) { return (static_cast<uint64_t>(0x4008u) << 32) | lo; };   // SBO 128, v1
+        // One lane runs the whole schedule (waits, MMAs, commits are per-thread
+        // operations), so no warp-level bookkeeping sits in the per-tile loop.
+        if (leader) {
+            ZWalk wk(pl.units, cd.Do, pl.nstrip);
+            int n, strip, zf, zl;
+            uint32_t as = 0, as_r = 0;
+            uint32_t u_run = 0;                        // running output index of the run's first plane
+            while (wk.next(n, strip, zf, zl)) {
+                int i0, i1;
+                run_planes(pl, cd, zf, zl, i0, i1);
+                const int Tv = min(T, pl.NT - strip * T);
+                const int zg0 = cd.zo_beg + zf, zg1 = cd.zo_beg + zl;
+                for (int i = i0; i <= i1; ++i) {
+                    // outputs touched by plane i: STR 1: z = i-1, i, i+1 (dz = 2, 1, 0);
+                    // STR 2: z with 2z-1 <= i <= 2z+1
+                    int zlo, zhi;
+                    if (STR == 1) { zlo = max(i - 1, zg0); zhi = min(i + 1, zg1); }
+                    else { zlo = max(i >> 1, zg0); zhi = min((i + 1) >> 1, zg1); }
+                    const int nz = zhi - zlo + 1;
+                    const bool full = nz == RO;
+                    // per plane: blocks newly started (wait for the epilogue), completed
+                    // (commit), and for partial planes each output's block and B block
+                    uint32_t new_bar[3] = {0, 0, 0}, new_par[3] = {0, 0, 0}, done_bar[3] = {0, 0, 0};
+                    uint32_t sgl_d[3] = {0, 0, 0}, sgl_b[3] = {0, 0, 0};
+                    bool is_new[3] = {false, false, false}, is_done[3] = {false, false, false};
+                    const uint32_t u_lo = u_run + (zlo - zg0);
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const int z = zlo + j;
+                        if (j < nz) {
+                            const uint32_t u = u_lo + j;
                             const uint32_t sg = u % RO;
-                            mbar_wait(acc_empty + sg * T + t, ((u / RO) - 1) & 1);
+                            const int first = max(STR * z - 1, 0), last = min(STR * z + 1, cd.Dci - 1);
+                            is_new[j] = first == i && u >= static_cast<uint32_t>(RO);
+                            new_bar[j] = sg * T;
+                            new_par[j] = ((u / RO) - 1) & 1;
+                            is_done[j] = last == i;
+                            done_bar[j] = sg * T;
+                            const int dz = i - STR * z + 1;
+                            // block holding dz: s1 [2 1 0 ..] -> 2 - dz; s2 [0 2 0 1] -> dz0:0 dz2:1 dz1:3
+                            sgl_b[j] = STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
+                            sgl_d[j] = sg * K;
                         }
                     }
-                    tc_fence_after();
-                    if (leader) {
-                        const uint32_t a_tile = a_slot + t * 128 * 16;
+                    uint32_t bl_full = b_lo0;
+                    if (full) {
+                        // rotation: block position p holds the output with sigma = p
+                        const uint32_t r = u_lo % RO;                 // sigma of the lowest output
+                        const uint32_t b0 = STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
+                        bl_full = b_lo0 + b0 * K;
+                    }
+                    ZSTAMP(y0);
+                    TZ_WAIT(plane_full + as, as_r & 1);
+                    ZACC(m_w1, y0);
+                    const uint32_t a_slot16 = (as * pl.slot_bytes) >> 4;
+                    for (int t = warp - kZMmaWarp; t < Tv; t += kZMmaWarps) {
+                        ZSTAMP(y1);
+#pragma unroll
+                        for (int j = 0; j < 3; ++j)
+                            if (is_new[j]) TZ_WAIT(acc_empty + new_bar[j] + t, new_par[j]);
+                        ZACC(m_w2, y1);
+                        tc_fence_after();
+                        const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
                         if (full) {
-                            // rotation: block position p holds output with sigma = p
-                            const uint32_t u_lo = u_run + (zlo - zg0);
-                            int b0;
-                            if (STR == 1) {
-                                const int r = u_lo % 3;           // sigma of z = i-1
-                                b0 = r == 0 ? 0 : (r == 1 ? 2 : 1);
-                            } else {
-                                b0 = (u_lo & 1) ? 0 : 1;          // sigma(z) = 1 -> [dz0 dz2]; 0 -> [dz2 dz0]
-                            }
                             const uint32_t idesc = idesc_i8(RO * K);
-#pragma unroll 1
-                            for (int m = 0; m < pl.nmma; ++m)
-                                tc_mma_i8(d_tile, umma_desc_lbo(a_tile + pl.a_off[m], pl.a_lbo[m]),
-                                          umma_desc_lbo(b_base + m * b_mma + b0 * K * 16, b_half), idesc, 1u);
+#pragma unroll
+                            for (int m = 0; m < NMMA; ++m)
+                                tc_mma_i8(d_tile, desc64(a_lo[m] + a_add), desc64(bl_full + m * b_mma16), idesc, 1u);
                         } else {
                             const uint32_t idesc = idesc_i8(K);
-                            for (int z = zlo; z <= zhi; ++z) {
-                                const uint32_t u = u_run + (z - zg0);
-                                const int dz = i - STR * z + 1;
-                                // block holding dz: s1 [2 1 0 ..] -> 2 - dz; s2 [0 2 0 1] -> dz0:0 dz2:1 dz1:3
-                                const int b = STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
-#pragma unroll 1
-                                for (int m = 0; m < pl.nmma; ++m)
-                                    tc_mma_i8(d_tile + (u % RO) * K, umma_desc_lbo(a_tile + pl.a_off[m], pl.a_lbo[m]),
-                                              umma_desc_lbo(b_base + m * b_mma + b * K * 16, b_half), idesc, 1u);
+#pragma unroll
+                            for (int j = 0; j < 3; ++j) {
+                                if (j < nz) {
+                                    const uint32_t bl = b_lo0 + sgl_b[j] * K;
+#pragma unroll
+                                    for (int m = 0; m < NMMA; ++m)
+                                        tc_mma_i8(d_tile + sgl_d[j], desc64(a_lo[m] + a_add), desc64(bl + m * b_mma16),
+                                                  idesc, 1u);
+                                }
                             }
                         }
-                        // outputs whose last plane is i are complete for this tile
-                        for (int z = zlo; z <= zhi; ++z) {
-                            const int last = min(STR * z + 1, cd.Dci - 1);
-                            if (last == i) {
-                                const uint32_t u = u_run + (z - zg0);
-                                tc_commit(acc_full + (u % RO) * T + t);
-                            }
-                        }
+#pragma unroll
+                        for (int j = 0; j < 3; ++j)
+                            if (is_done[j]) tc_commit(acc_full + done_bar[j] + t);
                     }
-                    __syncwarp();
+                    tc_commit(plane_free + as);
+                    if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
                 }
-                if (leader) tc_commit(plane_free + as);
-                __syncwarp();
-                if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
+                u_run += zl - zf + 1;
             }
-            u_run += zl - zf + 1;
         }
+        __syncwarp();
+#if TN_EXP_PROF
+        if (leader && warp == kZMmaWarp) {
+            g_tztrace[16 * blockIdx.x + 6] = clock64() - m_begin;
+            g_tztrace[16 * blockIdx.x + 7] = m_w1;
+            g_tztrace[16 * blockIdx.x + 8] = m_w2;
+        }
+#endif
     } else {
         // ================= epilogue
         const int q = warp & 3, g = warp >> 2;
+#if TN_EXP_PROF
+        long long p_w = 0;
+        const long long p_begin = clock64();
+#endif
         ZWalk wk(pl.units, cd.Do, pl.nstrip);
         int n, strip, zf, zl;
         uint32_t u = 0;
@@ -469,8 +571,14 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 for (int t = g; t < Tv; t += 2) {
-                    mbar_wait(acc_full + sgm * T + t, par);
+                    ZSTAMP(p0);
+                    TZ_WAIT(acc_full + sgm * T + t, par);
+                    ZACC(p_w, p0);
                     tc_fence_after();
+#if TZ_EXP_NOEPI
+                    mbar_arrive(acc_empty + sgm * T + t);
+                    continue;
+#endif
                     const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
                     const int qpos = strip * 128 * T + t * 128 + 32 * q + lane;
                     const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
@@ -546,6 +654,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }
             }
         }
+#if TN_EXP_PROF
+        if (warp == 0 && lane == 0) {
+            g_tztrace[16 * blockIdx.x + 9] = clock64() - p_begin;
+            g_tztrace[16 * blockIdx.x + 10] = p_w;
+        }
+#endif
     }
 
     tc_fence_before();
@@ -603,6 +717,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
+    pl.step_q = kZExpThreads / pl.Po;
+    pl.step_r = kZExpThreads % pl.Po;
 
     // K-slices: (tap, chunk) -> byte offset within an A slot (for a given REG),
     // sorted ascending and paired into MMAs.  Offsets depend on REG, so the order
@@ -626,7 +742,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
         return a.row < b.row;
     });
     pl.nmma = static_cast<int>((sl.size() + 1) / 2);
-    if (pl.nmma > kZMaxMma) return false;
+    if (pl.nmma > kZMaxMma || pl.nmma != (9 * ct + 1) / 2) return false;   // the kernel unrolls (9 CT + 1) / 2
     pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
     const int ptab = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
     pl.ptab_floats = ptab;
@@ -752,3 +868,9 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st) {
 }
 
 }  // namespace tn
+
+#if TN_EXP_PROF
+extern "C" int tn_exp_tztrace(long long* host, int n) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_tztrace, sizeof(long long) * (n < 148 * 16 ? n : 148 * 16)));
+}
+#endif
