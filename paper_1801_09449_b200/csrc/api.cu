@@ -15,6 +15,7 @@ static int g_conv_kernel = TN_KERNEL_AUTO;
 static int g_grid_cap = 0;
 
 int persistent_grid_cap() { return g_grid_cap; }
+bool first_kernel_tz_allowed() { return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TZ; }
 
 void set_error(const char* fmt, ...) {
     va_list ap;

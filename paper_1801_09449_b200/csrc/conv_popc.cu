@@ -390,6 +390,8 @@ cudaError_t launch_conv_popc(const ConvDesc& cd, cudaStream_t st) {
 }
 
 cudaError_t launch_conv_first(const FirstDesc& fd, cudaStream_t st) {
+    // tensor-core path (conv_tz.cu) where it covers the shape, else the popc kernel below
+    if (first_kernel_tz_allowed() && conv_tz_first_supported(fd)) return launch_conv_tz_first(fd, st);
     const Tiling tl = make_tiling(fd.Do, fd.Ho, fd.Wo, fd.N, fd.s, fd.dl, 32);
     const int nb = tl.BX * tl.BY * tl.BZ;
     const size_t smem = sizeof(uint32_t) * ((nb + 3) / 4 + 2 * fd.K);

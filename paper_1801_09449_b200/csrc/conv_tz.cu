@@ -110,6 +110,7 @@ struct TzPlan {
     int64_t units;          // N * nstrip * Do
     uint32_t po_magic;      // ceil(2^32 / Po)
     int step_q, step_r;     // 256 rows (one expander sweep) = step_q raster rows + step_r positions
+    int code_off, code_pitch, code_bytes;   // FIRST: ternary code planes (2 buffers) after the stages
     int ptab_floats;
 };
 
@@ -162,9 +163,13 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
     nrows = max(yhi - ylo + 1, 0);
 }
 
-template <int K, int CT, int NSEG, int STR, bool PRED>
+template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST>
 __global__ void __launch_bounds__(kZThreads, 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
+    // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
+    // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
+    // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
+    // taps are the z-merged B blocks as usual.
     constexpr int RO = STR == 1 ? 3 : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
     constexpr int NB = STR == 1 ? 5 : 4;
@@ -173,7 +178,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     uint8_t* s_a = smem;                                         // [slot][phase][chunk][RS][16]
     uint8_t* s_b = s_a + pl.nslot * pl.slot_bytes;               // [mma][half][NB*K][16]
     uint8_t* s_stage = s_b + pl.b_bytes;                         // [stage] packed rows per segment
-    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes);   // [K] -hi (TMEM init)
+    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes);   // [K] -hi
     int* s_lmh = s_nhi + K;                                      // [K] lo - hi
     float* s_pred = reinterpret_cast<float*>(s_lmh + K);         // [kZMaxClass] bias, then quad tables
     float* s_ptab = s_pred + kZMaxClass;
@@ -201,7 +206,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         int ofs = 0;
 #pragma unroll
         for (int sg = 0; sg < NSEG; ++sg) {
-            const int n4 = K * 27 * 2 * cd.seg[sg].cw / 4;
+            const int n4 = K * 27 * 2 * (FIRST ? 1 : cd.seg[sg].cw) / 4;
             const uint4* g = reinterpret_cast<const uint4*>(cd.seg[sg].wp);
             for (int i = threadIdx.x; i < n4; i += kZThreads)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_wp + ofs + 4 * i)), "l"(g + i)
@@ -239,7 +244,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
             const int tap = pl.sl_tap[j];
-            if (tap >= 0) {
+            if (FIRST) {
+                if (j == 0) {   // byte (dy*3 + dx) = w[k][0][dz][dy][dx]
+                    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                    for (int t9 = 0; t9 < 9; ++t9) {
+                        const uint32_t* src = wsrc[0] + (k * 27 + dz * 9 + t9) * 2;
+                        const uint32_t sb = src[0] & 1u, mb = src[1] & 1u;
+                        const uint32_t byte = mb ? (sb ? 0x01u : 0xFFu) : 0u;
+                        wv[t9 >> 2] |= byte << (8 * (t9 & 3));
+                    }
+                    v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+            } else if (tap >= 0) {
                 int c = pl.sl_chunk[j];
                 const int sg = (NSEG > 1 && c >= pl.cch[0]) ? 1 : 0;
                 if (sg) c -= pl.cch[0];
@@ -324,8 +340,14 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         const SegDesc& sd = cd.seg[sg];
                         const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
                         const bool ok = zs >= 0 && zs < sd.D && nr[sg] > 0;
-                        bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 8u * sd.cw : 0u;
-                        src[sg] = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw;
+                        if (FIRST) {
+                            bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 4u : 0u;
+                            src[sg] = reinterpret_cast<const uint32_t*>(
+                                cd.xf + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W);
+                        } else {
+                            bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 8u * sd.cw : 0u;
+                            src[sg] = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw;
+                        }
                         total += bytes[sg];
                     }
                     mbar_arrive_expect_tx(staged_full + st, total);
@@ -351,6 +373,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         ZWalk wk(pl.units, cd.Do, pl.nstrip);
         int n, strip, zf, zl;
         uint32_t st = 0, st_r = 0, as = 0, as_r = 0;
+        uint32_t e_par = 0;    // FIRST: code-plane double buffer parity (planes processed)
+        (void)e_par;
         while (wk.next(n, strip, zf, zl)) {
             int i0, i1;
             run_planes(pl, cd, zf, zl, i0, i1);
@@ -377,6 +401,60 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }
                 const uint8_t* stg = s_stage + st * pl.stage_bytes;
                 uint8_t* slot = s_a + as * pl.slot_bytes;
+                if constexpr (FIRST) {
+                    // step 1: Eq. 6 on the staged float rows -> int8 codes (zero border of
+                    // 4 columns and one row each side); non-finite -> d_bad
+                    const SegDesc& sd = cd.seg[0];
+                    uint8_t* code = s_stage + pl.code_off + (e_par & 1) * pl.code_bytes;
+                    ++e_par;
+                    const int W = sd.W, CP = pl.code_pitch, nrr = nr[0] + 2;
+                    const int zb = i - sd.zbeg;
+                    for (int e = et; e < nrr * (CP / 4); e += kZExpThreads) {
+                        const int row = e / (CP / 4), c4 = e - row * (CP / 4);
+                        const int x0 = 4 * c4 - 4;               // first of 4 voxels in this word
+                        uint32_t wv = 0u;
+                        if (zok[0] && row >= 1 && row <= nr[0] && x0 >= 0 && x0 < W) {
+                            const float4 f = *reinterpret_cast<const float4*>(stg + ((row - 1) * W + x0) * 4);
+                            const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const float v = fv[b];
+                                if (!isfinite(v) && cd.d_bad != nullptr)
+                                    atomicMin(reinterpret_cast<long long*>(cd.d_bad),
+                                              static_cast<long long>(static_cast<int64_t>(n) * cd.bad_nstride + cd.bad_base +
+                                                                     (static_cast<int64_t>(zb) * sd.H + ya[0] + row - 1) * W + x0 + b));
+                                const uint32_t c = v > cd.t_hi ? 0x01u : (v < cd.t_lo ? 0xFFu : 0u);
+                                wv |= c << (8 * b);
+                            }
+                        }
+                        *reinterpret_cast<uint32_t*>(code + row * CP + 4 * c4) = wv;
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"r"(kZExpThreads) : "memory");
+                    // step 2: one 16-byte A row per output position of the strip: the 3x3
+                    // in-plane window (bytes dy*3+dx), zero for separator / outside rows
+                    const int q0 = strip * 128 * T;
+                    for (int r = et; r < 128 * T; r += kZExpThreads) {
+                        const int q = q0 + r;
+                        const int y = div_po(static_cast<uint32_t>(q), pl.po_magic);
+                        const int x = q - y * pl.Po;
+                        uint4 a = make_uint4(0u, 0u, 0u, 0u);
+                        if (x < W && y < sd.H) {
+                            const int c0 = x + 3;                // code column of x - 1
+                            const uint32_t sel = 0x3210u + (c0 & 3) * 0x1111u;
+                            const uint8_t* rp = code + (y - ya[0]) * CP + (c0 & ~3);   // code row of y - 1
+                            uint32_t rw[3];
+#pragma unroll
+                            for (int dy = 0; dy < 3; ++dy) {
+                                const uint32_t* wp4 = reinterpret_cast<const uint32_t*>(rp + dy * CP);
+                                rw[dy] = __byte_perm(wp4[0], wp4[1], sel);
+                            }
+                            a.x = __byte_perm(rw[0], rw[1], 0x4210u);
+                            a.y = __byte_perm(rw[1], rw[2], 0x5421u);
+                            a.z = rw[2] >> 16 & 0xFFu;
+                        }
+                        *reinterpret_cast<uint4*>(slot + r * 16) = a;
+                    }
+                } else {
                 // Rows r = et + 256 j: (y, x) of the output raster tracked incrementally
                 // (256 = qd * Po + rd), all phases of a row from the same (y, x).
                 int r = TZ_EXP_NOEXP ? pl.RS : et;
@@ -421,6 +499,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     y += pl.step_q;
                     if (x >= pl.Po) { x -= pl.Po; ++y; }
                 }
+                }   // !FIRST
                 mbar_arrive(staged_empty + st);
                 fence_proxy_async();
                 mbar_arrive(plane_full + as);
@@ -440,7 +519,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         // ================= MMA issuers (warp mw takes the tiles t % 2 == mw).  Descriptor low words are precomputed per
         // K-slice pair (start address and LBO); per (slot, tile) only an add remains,
         // so the issue loop stays well under the 40+ cycles one N = 3K MMA takes.
-        constexpr int NMMA = (9 * CT + 1) / 2;
+        constexpr int NMMA = FIRST ? 1 : (9 * CT + 1) / 2;
         const bool leader = elect_one();
 #if TN_EXP_PROF
         long long m_w1 = 0, m_w2 = 0;
@@ -679,11 +758,12 @@ static int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
 static size_t tz_smem(const TzPlan& pl, int K) {
     return static_cast<size_t>(pl.nslot) * pl.slot_bytes + pl.b_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
+           2 * static_cast<size_t>(pl.code_bytes) +
            2 * K * sizeof(int) + (kZMaxClass + pl.ptab_floats) * sizeof(float) +
            (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
 }
 
-static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
+static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
     constexpr size_t kSmemMax = 227 * 1024;
     if (cd.nseg < 1 || cd.nseg > 2 || cd.y_in != nullptr) return false;
     for (int a = 0; a < 3; ++a)
@@ -696,12 +776,19 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
         return false;
     int ct = 0;
     pl.cch[1] = 0;
-    for (int i = 0; i < cd.nseg; ++i) {
+    for (int i = 0; i < cd.nseg && !first; ++i) {
         const SegDesc& sd = cd.seg[i];
         if (sd.c <= 0 || sd.c % 16 != 0 || (sd.c + 31) / 32 != sd.cw || sd.W % 2 != 0) return false;
         if ((reinterpret_cast<uintptr_t>(sd.xp) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
         pl.cch[i] = sd.c / 16;
         ct += pl.cch[i];
+    }
+    if (first) {   // one float input channel; 9 in-plane taps per 16-byte A row
+        const SegDesc& sd = cd.seg[0];
+        if (cd.nseg != 1 || pl.s != 1 || sd.up || sd.c != 1 || sd.W % 4 != 0 || cd.K > 32 || cd.logits != nullptr) return false;
+        if ((reinterpret_cast<uintptr_t>(cd.xf) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
+        pl.cch[0] = 1;
+        ct = 1;
     }
     if (ct > 4) return false;
     if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
@@ -741,8 +828,9 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
         if (a.ch != b.ch) return a.ch < b.ch;
         return a.row < b.row;
     });
+    if (first) sl.assign(1, Sl{0, 0, 0, 0});   // the whole 3x3 window is one row
     pl.nmma = static_cast<int>((sl.size() + 1) / 2);
-    if (pl.nmma > kZMaxMma || pl.nmma != (9 * ct + 1) / 2) return false;   // the kernel unrolls (9 CT + 1) / 2
+    if (pl.nmma > kZMaxMma || pl.nmma != (first ? 1 : (9 * ct + 1) / 2)) return false;   // the kernel unrolls
     pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
     const int ptab = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
     pl.ptab_floats = ptab;
@@ -755,7 +843,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
         pl.nstrip = (pl.NT + T - 1) / T;
         pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.Po + 2 : pl.Po + 1);
         pl.REG = round_up(pl.RS * 16, 128);
-        pl.slot_bytes = pl.nph * ct * pl.REG + 256;
+        pl.slot_bytes = first ? 128 * T * 16 + 256 : pl.nph * ct * pl.REG + 256;
         // staging: the most rows any strip reads, per segment
         int off = 0;
         for (int sg = 0; sg < cd.nseg; ++sg) {
@@ -772,12 +860,18 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
                 maxr = std::max(maxr, yhi - ylo + 1);
             }
             pl.seg_off[sg] = off;
-            off += round_up(maxr * sd.W * 8 * sd.cw, 128);
+            off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw), 128);
+            if (first) {   // ternary code planes: maxr + 2 rows of W + 8 bytes (4 zero columns each side)
+                pl.code_pitch = sd.W + 8;
+                pl.code_bytes = round_up((maxr + 2) * pl.code_pitch, 128);
+            }
         }
         pl.stage_bytes = off;
+        if (!first) pl.code_bytes = pl.code_pitch = 0;
+        pl.code_off = 0;
         // packed filter bank staged in the A ring during setup
         int wbytes = 0;
-        for (int sg = 0; sg < cd.nseg; ++sg) wbytes += cd.K * 27 * 2 * cd.seg[sg].cw * 4;
+        for (int sg = 0; sg < cd.nseg; ++sg) wbytes += cd.K * 27 * 2 * (first ? 1 : cd.seg[sg].cw) * 4;
         for (int ns = 3; ns >= 2 && !ok; --ns)
             for (int nst = kZMaxStage; nst >= 2 && !ok; --nst) {
                 pl.nslot = ns;
@@ -786,6 +880,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
             }
     }
     if (!ok) return false;
+    pl.code_off = pl.nstage * pl.stage_bytes;    // relative to the staging base
     for (size_t j = 0; j < 2 * static_cast<size_t>(pl.nmma); ++j) {
         if (j < sl.size()) {
             pl.sl_tap[j] = static_cast<int8_t>(sl[j].tap);
@@ -795,7 +890,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl) {
             pl.sl_chunk[j] = 0;
         }
     }
-    auto addr = [&](size_t j) { return (sl[j].ph * ct + sl[j].ch) * pl.REG + sl[j].row * 16; };
+    auto addr = [&](size_t j) { return first ? 0 : (sl[j].ph * ct + sl[j].ch) * pl.REG + sl[j].row * 16; };
     for (int m = 0; m < pl.nmma; ++m) {
         const int a0 = addr(2 * m);
         const int a1 = (2 * m + 1 < static_cast<int>(sl.size())) ? addr(2 * m + 1) : a0 + 16;   // zero-weight dummy
@@ -813,7 +908,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     const bool pred = cd.logits != nullptr;
 #define TZ_PICK(CT_, NSEG_, STR_)                                                                     \
     if (ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                                \
-        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32)> : conv_tz_kernel<K, CT_, NSEG_, STR_, false>;
+        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false> : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false>;
     TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(4, 1, 1)
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
     TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(4, 1, 2)
@@ -838,6 +933,68 @@ static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
     if (pl.s == 2) return cd.nseg == 1 && (ct == 1 || ct == 2 || ct == 4);
     if (cd.nseg == 1) return ct == 1 || ct == 2 || ct == 4;
     return ct >= 2;
+}
+
+static ConvDesc first_desc(const FirstDesc& fd) {
+    ConvDesc cd{};
+    cd.nseg = 1;
+    SegDesc& sd = cd.seg[0];
+    sd.xp = nullptr;
+    sd.wp = fd.wp;
+    sd.c = 1;
+    sd.cw = 1;
+    sd.D = fd.D; sd.H = fd.H; sd.W = fd.W;
+    sd.zbeg = fd.zbeg;
+    sd.up = 0;
+    cd.N = fd.N;
+    cd.K = fd.K;
+    for (int a = 0; a < 3; ++a) { cd.s[a] = fd.s[a]; cd.p[a] = fd.p[a]; cd.dl[a] = fd.dl[a]; }
+    cd.Do = fd.Do; cd.Ho = fd.Ho; cd.Wo = fd.Wo;
+    cd.zo_beg = fd.zo_beg;
+    cd.Dci = fd.Dg; cd.Hci = fd.H; cd.Wci = fd.W;
+    cd.yp = fd.yp;
+    cd.lo = fd.lo;
+    cd.hi = fd.hi;
+    cd.cwo = 1;
+    cd.xf = fd.x;
+    cd.t_lo = fd.t_lo;
+    cd.t_hi = fd.t_hi;
+    cd.d_bad = fd.d_bad;
+    cd.bad_base = fd.bad_base;
+    cd.bad_nstride = fd.bad_nstride;
+    return cd;
+}
+
+bool conv_tz_first_supported(const FirstDesc& fd) {
+    if (fd.K != 16 && fd.K != 32) return false;
+    const ConvDesc cd = first_desc(fd);
+    TzPlan pl{};
+    return plan_tz(cd, pl, true) && tz_smem(pl, cd.K) <= 227 * 1024;
+}
+
+cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
+    const ConvDesc cd = first_desc(fd);
+    TzPlan pl{};
+    if ((fd.K != 16 && fd.K != 32) || !plan_tz(cd, pl, true)) return cudaErrorNotSupported;
+    const size_t smem = tz_smem(pl, cd.K);
+    if (smem > 227 * 1024) return cudaErrorNotSupported;
+    if (g_num_sms_z == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms_z, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int cap = persistent_grid_cap() > 0 ? std::min(persistent_grid_cap(), g_num_sms_z) : g_num_sms_z;
+    const int grid = static_cast<int>(std::min<int64_t>(pl.units, cap));
+    void (*kern)(ConvDesc, TzPlan) =
+        fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true> : conv_tz_kernel<32, 1, 1, 1, false, true>;
+    static bool configured[2] = {false, false};
+    if (!configured[fd.K == 32]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        configured[fd.K == 32] = true;
+    }
+    kern<<<grid, kZThreads, smem, st>>>(cd, pl);
+    return cudaGetLastError();
 }
 
 bool conv_tz_supported(const ConvDesc& cd) {

@@ -53,6 +53,13 @@ struct ConvDesc {
     const float* pw;
     const float* pb;
     int nclass;
+    // First layer (A7) on the tensor-core TZ kernel: seg[0] describes the float
+    // input (c = 1, xp unused); Eq. 6 band (t_lo, t_hi); non-finite inputs are
+    // reported through d_bad (flat index n * bad_nstride + bad_base + (zb*H+y)*W+x).
+    const float* xf;
+    float t_lo, t_hi;
+    int64_t* d_bad;
+    int64_t bad_base, bad_nstride;
 };
 
 struct FirstDesc {
@@ -96,8 +103,14 @@ cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
 // tcgen05 tap-offset, z-merged implicit GEMM (conv_tz.cu): C, K <= 64 with a
 // small filter bank; same contract.
 bool        conv_tz_supported(const ConvDesc& cd);
+// A7 on the TZ kernel (stride 1, pad 1, K in {16, 32}, W % 4 == 0); false if the
+// shape is outside it (the caller then uses conv_first_kernel).
+bool        conv_tz_first_supported(const FirstDesc& fd);
+cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t s);
 // tn_set_grid_cap: upper bound on the persistent tensor-core grids (0 = #SMs).
 int         persistent_grid_cap();
+// The first layer may use the TZ kernel under the current selector (AUTO or TZ).
+bool        first_kernel_tz_allowed();
 cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s);
 
 }  // namespace tn

@@ -234,8 +234,11 @@ def test_conv3d_upsample_concat_matches_oracle(tn, kernel, low, cl, cs, k):
 
 
 # --------------------------------------------------------------------------- A7 first layer
-@pytest.mark.parametrize("shape,stride", [((1, 1, 16, 24, 40), 1), ((2, 1, 7, 9, 33), 1), ((1, 1, 12, 16, 16), 2)])
-def test_conv3d_first_matches_oracle(tn, shape, stride):
+@pytest.mark.parametrize("shape,stride", [((1, 1, 16, 24, 40), 1), ((2, 1, 7, 9, 33), 1), ((1, 1, 12, 16, 16), 2),
+                                          ((2, 1, 9, 13, 20), 1), ((1, 1, 21, 35, 132), 1)])
+def test_conv3d_first_matches_oracle(tn, kernel, shape, stride):
+    """A7 + A3 + A4 of the first layer; under AUTO / TZ the tensor-core first-layer
+    mode runs where it covers the shape (stride 1, W % 4 == 0), else the popc kernel."""
     x = synth.ct_volume(shape, seed=shape[3])
     w = synth.ternary_codes((16, 1, 3, 3, 3), 0.6, seed=5)
     lo, hi = synth.jittered_thresholds(16, synth.threshold_base(1, 0.38), seed=6)
