@@ -409,6 +409,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     ++e_par;
                     const int W = sd.W, CP = pl.code_pitch, nrr = nr[0] + 2;
                     const int zb = i - sd.zbeg;
+#pragma unroll 4
                     for (int e = et; e < nrr * (CP / 4); e += kZExpThreads) {
                         const int row = e / (CP / 4), c4 = e - row * (CP / 4);
                         const int x0 = 4 * c4 - 4;               // first of 4 voxels in this word
@@ -433,6 +434,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     // step 2: one 16-byte A row per output position of the strip: the 3x3
                     // in-plane window (bytes dy*3+dx), zero for separator / outside rows
                     const int q0 = strip * 128 * T;
+#pragma unroll 4
                     for (int r = et; r < 128 * T; r += kZExpThreads) {
                         const int q = q0 + r;
                         const int y = div_po(static_cast<uint32_t>(q), pl.po_magic);
