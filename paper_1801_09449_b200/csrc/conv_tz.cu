@@ -76,13 +76,12 @@ namespace tn {
 namespace {
 
 constexpr int kZEpiWarps = 8;
-constexpr int kZExpWarps = 8;
 constexpr int kZExpWarp0 = kZEpiWarps;
-constexpr int kZMmaWarp = kZEpiWarps + kZExpWarps;
 constexpr int kZMmaWarps = 2;         // two issuers (tiles t % 2): one thread cannot keep up with N = 3K MMAs
-constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-constexpr int kZThreads = (kZLoadWarp + 1) * 32;
-constexpr int kZExpThreads = kZExpWarps * 32;
+// Expander warps: the expansion is latency-bound per warp, so as many as the
+// register budget allows (the fused-prediction variants need more registers).
+__host__ __device__ constexpr int tz_exp_warps(bool pred) { return pred ? 8 : 12; }
+__host__ __device__ constexpr int tz_threads(bool pred) { return (kZEpiWarps + tz_exp_warps(pred) + kZMmaWarps + 1) * 32; }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
 constexpr int kZMaxSlot = 4;          // A ring
@@ -164,15 +163,23 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST>
-__global__ void __launch_bounds__(kZThreads, 1)
+__global__ void __launch_bounds__(tz_threads(PRED), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
+    constexpr int kZExpThreads = tz_exp_warps(PRED) * 32;
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(PRED);
+    constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
+    constexpr int kZThreads = tz_threads(PRED);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
     // taps are the z-merged B blocks as usual.
-    constexpr int RO = STR == 1 ? 3 : 2;
+    // K = 64 (stride 1): four blocks per tile, the B blocks in plain order and a
+    // plane's MMAs split in two where its outputs wrap around the block ring
+    // (the rotated-B sequence would not fit shared memory next to C = 64 strips).
+    constexpr bool SPLIT = STR == 1 && K == 64;
+    constexpr int RO = STR == 1 ? (SPLIT ? 4 : 3) : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
-    constexpr int NB = STR == 1 ? 5 : 4;
+    constexpr int NB = STR == 1 ? (SPLIT ? 3 : 5) : 4;
     constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_a = smem;                                         // [slot][phase][chunk][RS][16]
@@ -477,7 +484,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                         for (int sg = 0; sg < NSEG; ++sg) {
                             const SegDesc& sd = cd.seg[sg];
-                            const int ys = sd.up ? (yi >> 1) : yi, xs = sd.up ? (xi >> 1) : xi;
+                            constexpr bool kUp0 = NSEG == 2;      // plan: two segments = [up, skip]
+                            const bool up = sg == 0 && kUp0;
+                            const int ys = up ? (yi >> 1) : yi, xs = up ? (xi >> 1) : xi;
                             const bool ok = v && zok[sg];
                             const uint8_t* sp = stg + pl.seg_off[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
                             const int choff = sg ? pl.cch[0] : 0;
@@ -581,7 +590,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         }
                     }
                     uint32_t bl_full = b_lo0;
-                    if (full) {
+                    // SPLIT: blocks sigma(u_lo) .. in up to two contiguous groups
+                    uint32_t g_n1 = 0, g_n2 = 0, g_d1 = 0, g_b1 = 0, g_b2 = 0;
+                    if constexpr (SPLIT) {
+                        const uint32_t s0 = u_lo % RO;
+                        const uint32_t blk0 = static_cast<uint32_t>(zlo - (i - 1));
+                        g_n1 = min(static_cast<uint32_t>(nz), RO - s0);
+                        g_n2 = nz - g_n1;
+                        g_d1 = s0 * K;
+                        g_b1 = b_lo0 + blk0 * K;
+                        g_b2 = b_lo0 + (blk0 + g_n1) * K;
+                    }
+                    if (!SPLIT && full) {
                         // rotation: block position p holds the output with sigma = p
                         const uint32_t r = u_lo % RO;                 // sigma of the lowest output
                         const uint32_t b0 = STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
@@ -600,7 +620,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         tc_fence_after();
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
-                        if (full) {
+                        if constexpr (SPLIT) {
+                            const uint32_t idesc1 = idesc_i8(g_n1 * K);
+#pragma unroll
+                            for (int m = 0; m < NMMA; ++m)
+                                tc_mma_i8(d_tile + g_d1, desc64(a_lo[m] + a_add), desc64(g_b1 + m * b_mma16), idesc1, 1u);
+                            if (g_n2) {
+                                const uint32_t idesc2 = idesc_i8(g_n2 * K);
+#pragma unroll
+                                for (int m = 0; m < NMMA; ++m)
+                                    tc_mma_i8(d_tile, desc64(a_lo[m] + a_add), desc64(g_b2 + m * b_mma16), idesc2, 1u);
+                            }
+                        } else if (full) {
                             const uint32_t idesc = idesc_i8(RO * K);
 #pragma unroll
                             for (int m = 0; m < NMMA; ++m)
@@ -647,10 +678,19 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         int n, strip, zf, zl;
         uint32_t u = 0;
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
+        // K = 16: thresholds and the re-init values live in registers
+        constexpr bool REGT = K == 16;
+        int r_lmh[REGT ? 16 : 1], r_nhi[REGT ? 16 : 1];
+        if constexpr (REGT) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) { r_lmh[k] = s_lmh[k]; r_nhi[k] = s_nhi[k]; }
+        }
         while (wk.next(n, strip, zf, zl)) {
             const int Tv = min(T, pl.NT - strip * T);
+            const int q_lane = strip * 128 * T + 32 * q + lane;
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
+                const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
                 for (int t = g; t < Tv; t += 2) {
                     ZSTAMP(p0);
                     TZ_WAIT(acc_full + sgm * T + t, par);
@@ -661,50 +701,53 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     continue;
 #endif
                     const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
-                    const int qpos = strip * 128 * T + t * 128 + 32 * q + lane;
+                    const int qpos = q_lane + t * 128;
                     const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
                     const int x = qpos - y * pl.Po;
                     const bool vpos = x < cd.Wo && y < cd.Ho;
-                    const int64_t vox = ((static_cast<int64_t>(n) * cd.Do + z) * cd.Ho + y) * cd.Wo + x;
+                    const int voff = y * cd.Wo + x;
                     uint32_t sbits[CWO], mbits[CWO];
 #pragma unroll
                     for (int c = 0; c < K; c += 16) {
                         int acc[16];
                         tmem_ld16(taddr + c, acc);
                         tmem_wait_ld();
+                        int lmh[16], nhv[16];
+                        if constexpr (REGT) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) { lmh[i] = r_lmh[i]; nhv[i] = r_nhi[i]; }
+                        } else {
+#pragma unroll
+                            for (int i4 = 0; i4 < 4; ++i4) {
+                                const int4 l4 = *reinterpret_cast<const int4*>(s_lmh + c + 4 * i4);
+                                const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
+                                lmh[4 * i4] = l4.x; lmh[4 * i4 + 1] = l4.y; lmh[4 * i4 + 2] = l4.z; lmh[4 * i4 + 3] = l4.w;
+                                nhv[4 * i4] = h4.x; nhv[4 * i4 + 1] = h4.y; nhv[4 * i4 + 2] = h4.z; nhv[4 * i4 + 3] = h4.w;
+                            }
+                        }
                         if (fused) {
                             // acc holds acc - hi (initialised to -hi).  A4 (reading R5):
                             // +1 if acc >= hi; else -1 if acc <= lo; else 0.  Bit k of nhi =
                             // (acc_k < hi_k); bit k of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).
                             uint32_t nhi = 0u, nlo = 0u;
 #pragma unroll
-                            for (int i4 = 3; i4 >= 0; --i4) {
-                                const int4 l4 = *reinterpret_cast<const int4*>(s_lmh + c + 4 * i4);
-                                const int ll[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                                for (int i = 3; i >= 0; --i) {
-                                    const int d = acc[4 * i4 + i];
-                                    nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
-                                    nlo = __funnelshift_l(static_cast<uint32_t>(ll[i] - d), nlo, 1);
-                                }
+                            for (int i = 15; i >= 0; --i) {
+                                const int d = acc[i];
+                                nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
+                                nlo = __funnelshift_l(static_cast<uint32_t>(lmh[i] - d), nlo, 1);
                             }
                             const int w = c >> 5, sh = c & 31;
                             const uint32_t sb = (~nhi & 0xFFFFu) << sh, mb = (~(nhi & nlo) & 0xFFFFu) << sh;
                             if (sh == 0) { sbits[w] = sb; mbits[w] = mb; }
                             else { sbits[w] |= sb; mbits[w] |= mb; }
                         } else if (vpos) {
-                            int4* dst = reinterpret_cast<int4*>(cd.y + vox * K + c);
+                            int4* dst = reinterpret_cast<int4*>(cd.y + (vplane + voff) * K + c);
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
                                 dst[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
                         }
                         // re-initialise the block for the output that reuses it
-#pragma unroll
-                        for (int i4 = 0; i4 < 4; ++i4) {
-                            const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
-                            acc[4 * i4] = h4.x; acc[4 * i4 + 1] = h4.y; acc[4 * i4 + 2] = h4.z; acc[4 * i4 + 3] = h4.w;
-                        }
-                        tmem_st16(taddr + c, acc);
+                        tmem_st16(taddr + c, nhv);
                     }
                     tmem_wait_st();
                     tc_fence_before();
@@ -712,7 +755,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     if (fused && vpos) {
                         if (PRED) {
                             // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
-                            const int64_t v = (static_cast<int64_t>(z) * cd.Ho + y) * cd.Wo + x;
+                            const int64_t v = static_cast<int64_t>(z) * cd.Ho * cd.Wo + voff;
                             for (int j = 0; j < cd.nclass; ++j) {
                                 float a = s_pred[j];
                                 const float* tab = s_ptab + j * (K / 4) * 256;
@@ -725,7 +768,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
                             }
                         }
-                        uint32_t* dst = cd.yp + vox * 2 * CWO;
+                        uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
                         if constexpr (CWO == 1) {
                             *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
                         } else {
@@ -772,6 +815,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
         if (cd.s[a] != cd.s[0] || cd.p[a] != 1 || cd.dl[a] != 1) return false;
     pl.s = cd.s[0];
     if (pl.s != 1 && !(pl.s == 2 && cd.nseg == 1 && cd.seg[0].up == 0)) return false;
+    // the kernel fixes the segment pattern: one plain segment, or [nearest-x2 upsampled, plain]
+    if (cd.nseg == 1 ? cd.seg[0].up != 0 : (cd.seg[0].up != 1 || cd.seg[1].up != 0)) return false;
     if (cd.K != 16 && cd.K != 32 && cd.K != 64) return false;
     if (cd.logits != nullptr && (cd.K > 32 || cd.nclass < 1 || cd.nclass > kZMaxClass || cd.yp == nullptr ||
                                  cd.nclass * cd.K > 64))
@@ -797,17 +842,19 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
         cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    pl.RO = pl.s == 1 ? 3 : 2;
+    const bool split = pl.s == 1 && cd.K == 64;
+    pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
-    pl.NB = pl.s == 1 ? 5 : 4;
+    pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
     pl.Po = cd.Wo + 1;
     const int64_t npo = static_cast<int64_t>(cd.Ho) * pl.Po;
     if (npo + 4 * pl.Po > (1 << 22) || pl.Po > 1024) return false;   // div_po range: q * Po < 2^32
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    pl.step_q = kZExpThreads / pl.Po;
-    pl.step_r = kZExpThreads % pl.Po;
+    const int exp_threads = tz_exp_warps(cd.logits != nullptr) * 32;
+    pl.step_q = exp_threads / pl.Po;
+    pl.step_r = exp_threads % pl.Po;
 
     // K-slices: (tap, chunk) -> byte offset within an A slot (for a given REG),
     // sorted ascending and paired into MMAs.  Offsets depend on REG, so the order
@@ -925,7 +972,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
         for (void*& f : configured)
             if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
     }
-    kern<<<grid, kZThreads, smem, st>>>(cd, pl);
+    kern<<<grid, tz_threads(pred && K <= 32), smem, st>>>(cd, pl);
     return cudaGetLastError();
 }
 
@@ -995,7 +1042,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    kern<<<grid, kZThreads, smem, st>>>(cd, pl);
+    kern<<<grid, tz_threads(false), smem, st>>>(cd, pl);
     return cudaGetLastError();
 }
 

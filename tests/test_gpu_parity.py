@@ -159,6 +159,8 @@ CONV_CASES = [
     ((1, 16, 12, 18, 20), 16, 2, 1, 1),          # stride 2, phase images
     ((2, 32, 9, 14, 10), 32, 2, 1, 1),           # stride 2, odd depth
     ((1, 16, 3, 130, 140), 16, 1, 1, 1),         # several strips per plane
+    ((1, 64, 11, 20, 30), 64, 1, 1, 1),          # C = K = 64: four TMEM blocks, wrap-split MMAs
+    ((2, 64, 6, 9, 128), 64, 1, 1, 1),
 ]
 
 
