@@ -292,14 +292,15 @@ def main():
     # ---- roofline of the dominant kernel (the conv)
     conv_avg_s = float(np.mean(conv_ms)) / 1e3
     kernel = tn.tn_conv_kernel_for([xd], 64, g)
-    uses_tc = kernel == tn.TN_KERNEL_TC
+    uses_tc = kernel in (tn.TN_KERNEL_TC, tn.TN_KERNEL_TZ)
     clocks = clk.summary()
     if uses_tc:
         bf16 = peaks.get("bf16_tflops", 1590.0)
         peak = 2.0 * bf16          # int8 dense = 2 x bf16 dense (nominal 4.5 vs 2.25 PFLOP/s)
         achieved = 2.0 * C1_MACS / conv_avg_s / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                "frac": achieved / peak, "traffic": tn_peaks.get("c1_tc_conv_dram_bytes"),
+                "frac": achieved / peak,
+                "traffic": tn_peaks.get("c1_tz_conv_dram_bytes" if kernel == tn.TN_KERNEL_TZ else "c1_tc_conv_dram_bytes"),
                 "peak_source": "2 x MEASURED_PEAKS.bf16_tflops (int8/bf16 nominal ratio)"}
     else:
         popc_per_clk = tn_peaks.get("popc_per_clk_per_sm", 16.0)
@@ -351,7 +352,10 @@ def main():
                                    "integer-threshold requant, P(0)=0.5 act / 0.6 weights (BASELINE configs[1])",
                        "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
                        "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
-                       "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)", 2: "tcgen05 kind::i8 implicit GEMM"}.get(kernel, "?"),
+                       "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)",
+                                       2: "tcgen05 kind::i8 implicit GEMM, dx taps merged along N (conv_tc)",
+                                       3: "tcgen05 kind::i8 implicit GEMM, taps as UMMA descriptor offsets, "
+                                          "kernel planes merged along N (conv_tz)"}.get(kernel, "?"),
                        "l2": "256 MiB buffer zeroed between timed steps, outside the events",
                        "parallelism": f"replicas x{world}", "parity": parity},
             "roofline": roof,
