@@ -80,8 +80,12 @@ constexpr int kZExpWarp0 = kZEpiWarps;
 constexpr int kZMmaWarps = 2;         // two issuers (tiles t % 2): one thread cannot keep up with N = 3K MMAs
 // Expander warps: the expansion is latency-bound per warp, so as many as the
 // register budget allows (the fused-prediction variants need more registers).
-__host__ __device__ constexpr int tz_exp_warps(bool pred) { return pred ? 8 : 12; }
-__host__ __device__ constexpr int tz_threads(bool pred) { return (kZEpiWarps + tz_exp_warps(pred) + kZMmaWarps + 1) * 32; }
+// Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
+// strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
+__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
+__host__ __device__ constexpr int tz_threads(bool pred, int ct) {
+    return (kZEpiWarps + tz_exp_warps(pred, ct) + kZMmaWarps + 1) * 32;
+}
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
 constexpr int kZMaxSlot = 4;          // A ring
@@ -163,12 +167,12 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST>
-__global__ void __launch_bounds__(tz_threads(PRED), 1)
+__global__ void __launch_bounds__(tz_threads(PRED, CT), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
-    constexpr int kZExpThreads = tz_exp_warps(PRED) * 32;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(PRED);
+    constexpr int kZExpThreads = tz_exp_warps(PRED, CT) * 32;
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(PRED, CT);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(PRED);
+    constexpr int kZThreads = tz_threads(PRED, CT);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -852,7 +856,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(cd.logits != nullptr) * 32;
+    const int exp_threads = tz_exp_warps(cd.logits != nullptr && !first, ct) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -972,7 +976,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
         for (void*& f : configured)
             if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
     }
-    kern<<<grid, tz_threads(pred && K <= 32), smem, st>>>(cd, pl);
+    kern<<<grid, tz_threads(pred && K <= 32, ct), smem, st>>>(cd, pl);
     return cudaGetLastError();
 }
 
@@ -1042,7 +1046,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    kern<<<grid, tz_threads(false), smem, st>>>(cd, pl);
+    kern<<<grid, tz_threads(false, 1), smem, st>>>(cd, pl);
     return cudaGetLastError();
 }
 
