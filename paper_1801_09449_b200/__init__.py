@@ -382,7 +382,7 @@ class TernaryFCN:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:   # lib is None during interpreter shutdown
             lib.tn_fcn_destroy(h)
             self.handle = None
 

@@ -288,7 +288,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
                     part += nz ? (ps ? wv : -wv) : 0.0f;
                 }
-                s_ptab[e] = part;
+                // two classes: both classes' entries side by side (one 8-byte lookup per quad)
+                s_ptab[(cd.nclass == 2 && K == 16) ? ((qd * 256 + idx) * 2 + j) : e] = part;
             }
         }
         if (warp == kZMmaWarp) {
@@ -760,16 +761,33 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         if (PRED) {
                             // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
                             const int64_t v = static_cast<int64_t>(z) * cd.Ho * cd.Wo + voff;
-                            for (int j = 0; j < cd.nclass; ++j) {
-                                float a = s_pred[j];
-                                const float* tab = s_ptab + j * (K / 4) * 256;
+                            if (cd.nclass == 2 && K == 16) {
+                                // quad indices (mask nibble | sign nibble << 4): bytes of q02 = quads 0, 2;
+                                // bytes of q13 = quads 1, 3
+                                const uint32_t q02 = (mbits[0] & 0x0F0Fu) | ((sbits[0] & 0x0F0Fu) << 4);
+                                const uint32_t q13 = ((mbits[0] >> 4) & 0x0F0Fu) | (sbits[0] & 0xF0F0u);
+                                const uint32_t idx[4] = {q02 & 0xFFu, q13 & 0xFFu, (q02 >> 8) & 0xFFu, (q13 >> 8) & 0xFFu};
+                                float a0 = s_pred[0], a1 = s_pred[1];
 #pragma unroll
-                                for (int qd = 0; qd < K / 4; ++qd) {
-                                    const uint32_t w = qd >> 3, sh = 4 * (qd & 7);
-                                    const uint32_t idx = ((mbits[w] >> sh) & 0xFu) | (((sbits[w] >> sh) & 0xFu) << 4);
-                                    a += tab[qd * 256 + idx];
+                                for (int qd = 0; qd < 4; ++qd) {
+                                    const float2 e2 = *reinterpret_cast<const float2*>(s_ptab + (qd * 256 + idx[qd]) * 2);
+                                    a0 += e2.x;
+                                    a1 += e2.y;
                                 }
-                                cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
+                                cd.logits[(static_cast<int64_t>(n) * 2) * cd.lstride + v] = a0;
+                                cd.logits[(static_cast<int64_t>(n) * 2 + 1) * cd.lstride + v] = a1;
+                            } else {
+                                for (int j = 0; j < cd.nclass; ++j) {
+                                    float a = s_pred[j];
+                                    const float* tab = s_ptab + j * (K / 4) * 256;
+#pragma unroll
+                                    for (int qd = 0; qd < K / 4; ++qd) {
+                                        const uint32_t w = qd >> 3, sh = 4 * (qd & 7);
+                                        const uint32_t ix = ((mbits[w] >> sh) & 0xFu) | (((sbits[w] >> sh) & 0xFu) << 4);
+                                        a += tab[qd * 256 + ix];
+                                    }
+                                    cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
+                                }
                             }
                         }
                         uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
