@@ -75,16 +75,27 @@ __device__ long long g_tztrace[148 * 16];
 namespace tn {
 namespace {
 
-constexpr int kZEpiWarps = 8;
-constexpr int kZExpWarp0 = kZEpiWarps;
-constexpr int kZMmaWarps = 2;         // two issuers (tiles t % 2): one thread cannot keep up with N = 3K MMAs
+// MMA issuers (tiles t % kZMmaWarps): one thread's per-tile wait / commit
+// overhead exceeds the 5 x 44 cycles a K = 16 tile keeps the tensor pipe busy.
+#ifndef TZ_MMA_WARPS
+#define TZ_MMA_WARPS 2
+#endif
+constexpr int kZMmaWarps = TZ_MMA_WARPS;
 // Expander warps: the expansion is latency-bound per warp, so as many as the
 // register budget allows (the fused-prediction variants need more registers).
 // Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
 // strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
-__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
+#ifndef TZ_EPI_GROUPS1
+#define TZ_EPI_GROUPS1 2
+#endif
+#ifndef TZ_EXP_WARPS1
+#define TZ_EXP_WARPS1 12
+#endif
+__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : (ct == 1 ? TZ_EXP_WARPS1 : 12); }
+// epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
+__host__ __device__ constexpr int tz_epi_groups(bool pred, int ct) { return (!pred && ct == 1) ? TZ_EPI_GROUPS1 : 2; }
 __host__ __device__ constexpr int tz_threads(bool pred, int ct) {
-    return (kZEpiWarps + tz_exp_warps(pred, ct) + kZMmaWarps + 1) * 32;
+    return (4 * tz_epi_groups(pred, ct) + tz_exp_warps(pred, ct) + kZMmaWarps + 1) * 32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
@@ -170,6 +181,9 @@ template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST>
 __global__ void __launch_bounds__(tz_threads(PRED, CT), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     constexpr int kZExpThreads = tz_exp_warps(PRED, CT) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(PRED, CT);
+    constexpr int kZEpiWarps = 4 * kZEpiGroups;
+    constexpr int kZExpWarp0 = kZEpiWarps;
     constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(PRED, CT);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
     constexpr int kZThreads = tz_threads(PRED, CT);
@@ -206,6 +220,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     const int lane = threadIdx.x & 31;
     const bool fused = cd.yp != nullptr;
     const int T = pl.T;
+#if TN_EXP_PROF
+    const long long k_begin = clock64();
+    long long k_gstart = 0;
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_gstart));
+#endif
 
     // ---- setup: stage the packed filter bank (cp.async) in the A ring, expand it
     // into the B image, thresholds, barriers, TMEM.
@@ -310,7 +329,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         int iv[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) iv[k] = s_nhi[k];
-        for (int t = g; t < T; t += 2)
+        for (int t = g; t < T; t += kZEpiGroups)
             for (int b = 0; b < RO; ++b)
 #pragma unroll
                 for (int c = 0; c < K; c += 16)
@@ -322,6 +341,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     __syncthreads();
     tc_fence_after();
 
+#if TN_EXP_PROF
+    if (threadIdx.x == 0) g_tztrace[16 * blockIdx.x + 11] = clock64() - k_begin;
+#endif
     const uint32_t two_po = 2u * pl.Po;
     if (warp == kZLoadWarp) {
         // ================= loader: per plane and segment one bulk copy of the
@@ -696,7 +718,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
-                for (int t = g; t < Tv; t += 2) {
+                for (int t = g; t < Tv; t += kZEpiGroups) {
                     ZSTAMP(p0);
                     TZ_WAIT(acc_full + sgm * T + t, par);
                     ZACC(p_w, p0);
@@ -810,6 +832,15 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 
     tc_fence_before();
     __syncthreads();
+#if TN_EXP_PROF
+    if (threadIdx.x == 0) {
+        long long g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        g_tztrace[16 * blockIdx.x + 12] = clock64() - k_begin;
+        g_tztrace[16 * blockIdx.x + 13] = k_gstart;
+        g_tztrace[16 * blockIdx.x + 14] = g_end;
+    }
+#endif
     if (warp == kZMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
@@ -943,7 +974,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
         // packed filter bank staged in the A ring during setup
         int wbytes = 0;
         for (int sg = 0; sg < cd.nseg; ++sg) wbytes += cd.K * 27 * 2 * (first ? 1 : cd.seg[sg].cw) * 4;
-        for (int ns = 3; ns >= 2 && !ok; --ns)
+        for (int ns = kZMaxSlot; ns >= 2 && !ok; --ns)
             for (int nst = kZMaxStage; nst >= 2 && !ok; --nst) {
                 pl.nslot = ns;
                 pl.nstage = nst;

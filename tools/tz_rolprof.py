@@ -37,7 +37,14 @@ for _ in range(3):
     run(); torch.cuda.synchronize()
 buf = (ctypes.c_longlong * (148 * 16))()
 tn.lib.tn_exp_tztrace(buf, 148 * 16)
-m = np.array(buf[:]).reshape(148, 16).astype(float).mean(0)
+A = np.array(buf[:]).reshape(148, 16).astype(float)
+os.makedirs("gpurun_out", exist_ok=True)
+np.save(f"gpurun_out/tzprof_{mode}_{'_'.join(map(str, args))}.npy", A)
+m = A.mean(0)
+gs, ge = A[:, 13], A[:, 14]
+print(f"  kernel cycles mean {m[12]:.0f} max {A[:,12].max():.0f}; setup mean {m[11]:.0f}; "
+      f"globaltimer span {(ge.max() - gs.min()) / 1e3:.1f} us, CTA start spread {(gs.max() - gs.min()) / 1e3:.1f} us, "
+      f"end spread {(ge.max() - ge.min()) / 1e3:.1f} us")
 print(f"{mode} {args}: planes/CTA {m[5]:.1f}")
 print(f"  loader   total {m[0]:9.0f}  staged_empty-wait {m[1]:9.0f}")
 print(f"  expander total {m[2]:9.0f}  staged_full-wait {m[3]:9.0f}  plane_free-wait {m[4]:9.0f}")
