@@ -68,6 +68,9 @@ __device__ long long g_tztrace[148 * 16];
 #ifndef TZ_EXP_NOEXP
 #define TZ_EXP_NOEXP 0
 #endif
+#ifndef TZ_EXP_NOACCWAIT
+#define TZ_EXP_NOACCWAIT 0
+#endif
 #ifndef TZ_WAIT
 #define TZ_WAIT mbar_wait
 #endif
@@ -638,11 +641,37 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     TZ_WAIT(plane_full + as, as_r & 1);
                     ZACC(m_w1, y0);
                     const uint32_t a_slot16 = (as * pl.slot_bytes) >> 4;
+                    // steady-state fast path (stride 1, rotated B): the plane starts output
+                    // i+1 (one wait per tile) and completes output i-1 (one commit per tile);
+                    // descriptors precomputed per plane, so a tile is ~2 + 2*NMMA instructions
+                    const bool fast = !SPLIT && STR == 1 && full && is_new[2] && !is_new[0] && !is_new[1] &&
+                                      is_done[0] && !is_done[1] && !is_done[2];
+                    if (fast) {
+                        uint32_t a_pl[NMMA], b_pl[NMMA];
+#pragma unroll
+                        for (int m = 0; m < NMMA; ++m) { a_pl[m] = a_lo[m] + a_slot16; b_pl[m] = bl_full + m * b_mma16; }
+                        const uint32_t idesc = idesc_i8(RO * K);
+                        const int t0 = warp - kZMmaWarp;
+                        const uint32_t wbar = smem_u32(acc_empty + new_bar[2] + t0), wpar = new_par[2];
+                        const uint32_t cbar = smem_u32(acc_full + done_bar[0] + t0);
+                        constexpr uint32_t kBarStep = 8 * kZMmaWarps;
+                        int k = 0;
+                        for (int t = t0; t < Tv; t += kZMmaWarps, ++k) {
+                            if (!TZ_EXP_NOACCWAIT) mbar_wait_addr(wbar + k * kBarStep, wpar);
+                            tc_fence_after();
+                            const uint32_t a_add = t * 128;
+                            const uint32_t d_tile = tmem_base + t * RO * K;
+#pragma unroll
+                            for (int m = 0; m < NMMA; ++m)
+                                tc_mma_i8(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc, 1u);
+                            tc_commit_addr(cbar + k * kBarStep);
+                        }
+                    } else
                     for (int t = warp - kZMmaWarp; t < Tv; t += kZMmaWarps) {
                         ZSTAMP(y1);
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (is_new[j]) TZ_WAIT(acc_empty + new_bar[j] + t, new_par[j]);
+                            if (is_new[j] && !TZ_EXP_NOACCWAIT) TZ_WAIT(acc_empty + new_bar[j] + t, new_par[j]);
                         ZACC(m_w2, y1);
                         tc_fence_after();
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4

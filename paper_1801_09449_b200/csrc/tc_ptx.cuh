@@ -38,6 +38,17 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra TN_WAITS_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
 }
+// Waits / commits on a barrier given by its shared-memory address.
+__device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TN_WAITA_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra TN_WAITA_%=;\n\t}" ::"r"(a), "r"(parity), "r"(1000000u) : "memory");
+}
+__device__ __forceinline__ void tc_commit_addr(uint32_t a) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

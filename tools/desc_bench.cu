@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(128, 1) kern(int n, int align, int reps, int n
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
     long long t0 = 0, t1 = 0;
     const int nw = dstride >= 3 ? 2 : 1;
+    const bool exact = dstride == 4;
     if (threadIdx.x < 32 * nw) {
         const int w = threadIdx.x >> 5;
         uint32_t pred = 0;
@@ -58,8 +59,8 @@ __global__ void __launch_bounds__(128, 1) kern(int n, int align, int reps, int n
                     for (int m = 0; m < 5; ++m)
                         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                                     ::"r"(d + (t % 2) * 256 * (dstride == 0) + (t % 8) * 48 * (dstride == 1) + (t % 4) * 128 * (dstride == 2)), "l"(desc(sa + t * 2048 + offs[m] * 16, lbos[m] * 16)),
-                                     "l"(desc(sb + m * 2 * n * 16, n * 16)), "r"(idesc), "r"(1) : "memory");
+                                     ::"r"(exact ? d + t * 48 : d + (t % 2) * 256 * (dstride == 0) + (t % 8) * 48 * (dstride == 1) + (t % 4) * 128 * (dstride == 2)), "l"(desc(sa + t * 2048 + offs[m] * 16, lbos[m] * 16)),
+                                     "l"(exact ? desc(sb + m * 2560, 1280) : desc(sb + m * 2 * n * 16, n * 16)), "r"(idesc), "r"(1) : "memory");
                     if (commit_every != 0 && (commit_every < 0 || (t % commit_every) == 0))
                         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                                      ::"r"(smem_u32(&bar2[1 + (t & 3)])) : "memory");
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(128, 1) kern(int n, int align, int reps, int n
 int main() {
     long long* dc; cudaMalloc(&dc, 148 * 8);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    for (int n : {48, 96}) for (int ds : {0, 3}) for (int ce : {0, 1, -1}) { const int align = 0;
+    for (int n : {48}) for (int ds : {3, 4}) for (int ce : {0, 1, -1}) { const int align = 0;
         const int reps = 40, ntile = 10;
         kern<<<148, 128, SMEM>>>(n, align, reps, ntile, dc, ce, ds);
         cudaError_t e = cudaDeviceSynchronize();
