@@ -212,11 +212,14 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
 /* Kernel selection for the ternary conv (all exact; parity tests run each).
  *   TN_KERNEL_POPC  CUDA-core XOR/AND/POPC form of Eq. 9 (any geometry)
  *   TN_KERNEL_TC    tcgen05 kind::i8, dx taps merged along N (stride 1, C <= 64)
- *   TN_KERNEL_TZ    tcgen05 kind::i8, taps as descriptor offsets and the three
- *                   kernel planes merged along N (stride 1/2, C <= 64, small
- *                   27*C*K filter bank; W even)
+ *   TN_KERNEL_TZ    tcgen05, taps as descriptor offsets and the three kernel
+ *                   planes merged along N (stride 1/2, C <= 64, small 27*C*K
+ *                   filter bank; W even); ternary operands as FP4 E2M1
+ *                   (kind::mxf4, unit block scales: exact) where they fit, else
+ *                   int8 (kind::i8)
+ *   TN_KERNEL_TZ8   like AUTO, with the TZ kernel restricted to int8 operands
  * TN_KERNEL_AUTO picks TZ, else TC, else POPC per shape.  Host, process-wide. */
-enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2, TN_KERNEL_TZ = 3 };
+enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2, TN_KERNEL_TZ = 3, TN_KERNEL_TZ8 = 4 };
 tn_status tn_set_conv_kernel(int32_t which);
 int32_t   tn_get_conv_kernel(void);
 /* Upper bound on the CTAs of the persistent tensor-core conv grids (0 = one per

@@ -15,7 +15,9 @@ static int g_conv_kernel = TN_KERNEL_AUTO;
 static int g_grid_cap = 0;
 
 int persistent_grid_cap() { return g_grid_cap; }
-bool first_kernel_tz_allowed() { return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TZ; }
+bool first_kernel_tz_allowed() {
+    return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TZ || g_conv_kernel == TN_KERNEL_TZ8;
+}
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -189,7 +191,7 @@ static bool split_tc_possible(const ConvDesc& cd) {
 
 tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch) {
     if (scratch != nullptr && (g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TC) &&
-        !(g_conv_kernel == TN_KERNEL_AUTO && conv_tz_supported(cd)) && split_tc_possible(cd)) {
+        !(g_conv_kernel == TN_KERNEL_AUTO && conv_tz_supported(cd, true)) && split_tc_possible(cd)) {
         ConvDesc a = cd, b = cd;
         a.nseg = 1; a.yp = nullptr; a.y = scratch; a.logits = nullptr; a.lo = a.hi = nullptr;
         tn_status s1 = cuda_status(launch_conv_tc(a, st), where);
@@ -205,16 +207,21 @@ tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int
 // TN_KERNEL_TC (dx-merged tensor-core kernel), then the CUDA-core popc kernel;
 // a forced selector only takes its own kernel.  -1 if nothing covers the shape.
 static int pick_kernel(const ConvDesc& cd, int mode) {
-    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ) && conv_tz_supported(cd)) return TN_KERNEL_TZ;
-    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TC) && conv_tc_supported(cd)) return TN_KERNEL_TC;
-    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC) && cd.y_in == nullptr && cd.logits == nullptr)
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ || mode == TN_KERNEL_TZ8) &&
+        conv_tz_supported(cd, mode != TN_KERNEL_TZ8))
+        return TN_KERNEL_TZ;
+    // TZ8 = AUTO with int8 TZ operands (falls back like AUTO)
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TC || mode == TN_KERNEL_TZ8) && conv_tc_supported(cd))
+        return TN_KERNEL_TC;
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC || mode == TN_KERNEL_TZ8) && cd.y_in == nullptr &&
+        cd.logits == nullptr)
         return TN_KERNEL_POPC;
     return -1;
 }
 
 static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st) {
     switch (kernel) {
-        case TN_KERNEL_TZ: return launch_conv_tz(cd, st);
+        case TN_KERNEL_TZ: return launch_conv_tz(cd, st, g_conv_kernel != TN_KERNEL_TZ8);
         case TN_KERNEL_TC: return launch_conv_tc(cd, st);
         case TN_KERNEL_POPC: return launch_conv_popc(cd, st);
     }
@@ -367,7 +374,7 @@ tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float
 }
 
 tn_status tn_set_conv_kernel(int32_t which) {
-    if (which != TN_KERNEL_AUTO && which != TN_KERNEL_POPC && which != TN_KERNEL_TC && which != TN_KERNEL_TZ)
+    if (which < TN_KERNEL_AUTO || which > TN_KERNEL_TZ8)
         return fail(TN_EINVAL, "unknown kernel selector %d", which);
     g_conv_kernel = which;
     return TN_OK;
@@ -397,7 +404,8 @@ int32_t tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_g
     const int kern = pick_kernel(cd, g_conv_kernel);
     if (kern == TN_KERNEL_POPC || kern < 0) {
         // the popc kernel covers every valid shape of a plain tn_conv3d_seg call
-        return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_POPC ? TN_KERNEL_POPC : -1;
+        return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_POPC || g_conv_kernel == TN_KERNEL_TZ8
+                   ? TN_KERNEL_POPC : -1;
     }
     return kern;
 }

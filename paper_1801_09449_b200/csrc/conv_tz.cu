@@ -122,6 +122,11 @@ struct TzPlan {
     int a_lbo[kZMaxMma];
     int8_t sl_tap[2 * kZMaxMma];    // per K-slice (sorted order): tap (dy*3+dx) and chunk, -1 = zero slice
     int8_t sl_chunk[2 * kZMaxMma];
+    int8_t sl_tapb[2 * kZMaxMma];   // F4 two-position slices (C = 16): second tap, -1 = none
+    int8_t sl_seg[2 * kZMaxMma];    // F4: segment of the slice
+    int f4;                 // FP4 (kind::mxf4) operands
+    int nreg;               // F4: 16-byte A regions per phase (per position); reg0[seg] = first region of seg
+    int reg0[kMaxSeg];
     int NB;                 // B blocks (5 for s = 1, 4 for s = 2)
     int b_bytes;
     int64_t units;          // N * nstrip * Do
@@ -180,7 +185,7 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
     nrows = max(yhi - ylo + 1, 0);
 }
 
-template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST>
+template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
 __global__ void __launch_bounds__(tz_threads(PRED, CT), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     constexpr int kZExpThreads = tz_exp_warps(PRED, CT) * 32;
@@ -197,7 +202,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // K = 64 (stride 1): four blocks per tile, the B blocks in plain order and a
     // plane's MMAs split in two where its outputs wrap around the block ring
     // (the rotated-B sequence would not fit shared memory next to C = 64 strips).
-    constexpr bool SPLIT = STR == 1 && K == 64;
+    // F4: ternary operands as FP4 E2M1 (kind::mxf4, unit UE8M0 block scales in TMEM
+    // columns 480..511): exact (f32 accumulation of integers < 2^24), half the
+    // shared-memory bytes per MAC and twice the int8 MMA rate.  C = 16 segments
+    // hold two consecutive positions per 16-byte row (taps dx, dx+1 in one K-half).
+    constexpr bool SPLIT = STR == 1 && K == 64 && !F4;
     constexpr int RO = STR == 1 ? (SPLIT ? 4 : 3) : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
     constexpr int NB = STR == 1 ? (SPLIT ? 3 : 5) : 4;
@@ -249,8 +258,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
         if (threadIdx.x < K) {
-            s_nhi[threadIdx.x] = fused ? -hi_r : 0;
-            s_lmh[threadIdx.x] = lo_r - hi_r;
+            if (F4) {   // f32 accumulators: the same integers as floats (exact, +0.0 for 0)
+                s_nhi[threadIdx.x] = __float_as_int(fused ? static_cast<float>(-hi_r) : 0.0f);
+                s_lmh[threadIdx.x] = __float_as_int(static_cast<float>(lo_r - hi_r));
+            } else {
+                s_nhi[threadIdx.x] = fused ? -hi_r : 0;
+                s_lmh[threadIdx.x] = lo_r - hi_r;
+            }
         }
         {   // barriers, one per thread
             const int t = threadIdx.x;
@@ -287,6 +301,27 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         wv[t9 >> 2] |= byte << (8 * (t9 & 3));
                     }
                     v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+            } else if (F4) {
+                if (tap >= 0) {
+                    const int sg = pl.sl_seg[j];
+                    const int cw = cd.seg[sg].cw;
+                    const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
+                    if (cd.seg[sg].c == 16) {       // [tap a ch 0-15 | tap b ch 0-15]
+                        const uint2 a2 = expand16_f4(src[0], src[cw], 0);
+                        uint2 b2 = make_uint2(0u, 0u);
+                        const int tb = pl.sl_tapb[j];
+                        if (tb >= 0) {
+                            const uint32_t* s2 = wsrc[sg] + (k * 27 + dz * 9 + tb) * 2 * cw;
+                            b2 = expand16_f4(s2[0], s2[cw], 0);
+                        }
+                        v = make_uint4(a2.x, a2.y, b2.x, b2.y);
+                    } else {                        // 32 channels 32c .. 32c+31
+                        const int c = pl.sl_chunk[j];
+                        const uint2 a2 = expand16_f4(src[c], src[cw + c], 0);
+                        const uint2 b2 = expand16_f4(src[c], src[cw + c], 16);
+                        v = make_uint4(a2.x, a2.y, b2.x, b2.y);
+                    }
                 }
             } else if (tap >= 0) {
                 int c = pl.sl_chunk[j];
@@ -338,6 +373,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 for (int c = 0; c < K; c += 16)
                     tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (t * RO + b) * K + c,
                               *reinterpret_cast<const int(*)[16]>(iv + c));
+        if (F4 && g == 0) {   // unit block scales (UE8M0 0x7F = 2^0) in columns 480..511
+            int sf[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sf[i] = 0x7F7F7F7F;
+            tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + 480, sf);
+            tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + 496, sf);
+        }
         tmem_wait_st();
         tc_fence_before();
     }
@@ -494,6 +536,59 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         *reinterpret_cast<uint4*>(slot + r * 16) = a;
                     }
                 } else {
+                if constexpr (F4) {
+                // FP4 rows: C = 16 segments write the position into the low half of
+                // row r and the high half of row r-1 (a 16-byte guard row precedes each
+                // region); C = 32 / 64 segments write one / two 16-byte rows.
+                int r = TZ_EXP_NOEXP ? pl.RS : et;
+                int y, x;
+                {
+                    const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
+                    y = div_po(tq, pl.po_magic) - 2;
+                    x = static_cast<int>(tq) - (y + 2) * pl.Po;
+                }
+                for (; r < pl.RS; r += kZExpThreads) {
+                    const bool vx = x < cd.Wo && y >= 0;
+#pragma unroll
+                    for (int ph = 0; ph < NPH; ++ph) {
+                        const int py = ph >> 1, px = ph & 1;
+                        const int yi = STR == 2 ? 2 * y + py : y, xi = STR == 2 ? 2 * x + px : x;
+                        const bool v = vx && yi < cd.Hci && xi < cd.Wci;
+#pragma unroll
+                        for (int sg = 0; sg < NSEG; ++sg) {
+                            const SegDesc& sd = cd.seg[sg];
+                            constexpr bool kUp0 = NSEG == 2;
+                            const bool up = sg == 0 && kUp0;
+                            const int ys = up ? (yi >> 1) : yi, xs = up ? (xi >> 1) : xi;
+                            const bool ok = v && zok[sg];
+                            const uint8_t* sp = stg + pl.seg_off[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
+                            uint8_t* rb = slot + (ph * pl.nreg + pl.reg0[sg]) * pl.REG + 16 + r * 16;
+                            if (sd.c == 16) {
+                                uint2 w = make_uint2(0u, 0u);
+                                if (ok) w = *reinterpret_cast<const uint2*>(sp);
+                                const uint2 e = expand16_f4(w.x, w.y, 0);
+                                *reinterpret_cast<uint2*>(rb) = e;
+                                *reinterpret_cast<uint2*>(rb - 8) = e;
+                            } else if (sd.cw == 1) {
+                                uint2 w = make_uint2(0u, 0u);
+                                if (ok) w = *reinterpret_cast<const uint2*>(sp);
+                                const uint2 e0 = expand16_f4(w.x, w.y, 0), e1 = expand16_f4(w.x, w.y, 16);
+                                *reinterpret_cast<uint4*>(rb) = make_uint4(e0.x, e0.y, e1.x, e1.y);
+                            } else {
+                                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                                if (ok) w = *reinterpret_cast<const uint4*>(sp);
+                                const uint2 e0 = expand16_f4(w.x, w.z, 0), e1 = expand16_f4(w.x, w.z, 16);
+                                const uint2 e2 = expand16_f4(w.y, w.w, 0), e3 = expand16_f4(w.y, w.w, 16);
+                                *reinterpret_cast<uint4*>(rb) = make_uint4(e0.x, e0.y, e1.x, e1.y);
+                                *reinterpret_cast<uint4*>(rb + pl.REG) = make_uint4(e2.x, e2.y, e3.x, e3.y);
+                            }
+                        }
+                    }
+                    x += pl.step_r;
+                    y += pl.step_q;
+                    if (x >= pl.Po) { x -= pl.Po; ++y; }
+                }
+                } else {
                 // Rows r = et + 256 j: (y, x) of the output raster tracked incrementally
                 // (256 = qd * Po + rd), all phases of a row from the same (y, x).
                 int r = TZ_EXP_NOEXP ? pl.RS : et;
@@ -540,6 +635,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     y += pl.step_q;
                     if (x >= pl.Po) { x -= pl.Po; ++y; }
                 }
+                }   // !F4
                 }   // !FIRST
                 mbar_arrive(staged_empty + st);
                 fence_proxy_async();
@@ -560,7 +656,15 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         // ================= MMA issuers (warp mw takes the tiles t % 2 == mw).  Descriptor low words are precomputed per
         // K-slice pair (start address and LBO); per (slot, tile) only an add remains,
         // so the issue loop stays well under the 40+ cycles one N = 3K MMA takes.
-        constexpr int NMMA = FIRST ? 1 : (9 * CT + 1) / 2;
+        // F4 slices: 6 per C = 16 segment (two-position rows), 9 per 32 channels
+        constexpr int NMMA = F4 ? (NSEG == 1 ? (CT == 1 ? 3 : (CT == 2 ? 5 : 9)) : (CT == 2 ? 6 : (CT == 3 ? 8 : 9)))
+                                : (FIRST ? 1 : (9 * CT + 1) / 2);
+        const uint32_t sfa = tmem_base + 480, sfb = tmem_base + 496;
+        auto idesc_n = [](uint32_t n) { return F4 ? idesc_mxf4(static_cast<int>(n)) : idesc_i8(static_cast<int>(n)); };
+        auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id) {
+            if constexpr (F4) tc_mma_mxf4(d, a, b, id, sfa, sfb);
+            else tc_mma_i8(d, a, b, id, 1u);
+        };
         const bool leader = elect_one();
 #if TN_EXP_PROF
         long long m_w1 = 0, m_w2 = 0;
@@ -650,7 +754,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         uint32_t a_pl[NMMA], b_pl[NMMA];
 #pragma unroll
                         for (int m = 0; m < NMMA; ++m) { a_pl[m] = a_lo[m] + a_slot16; b_pl[m] = bl_full + m * b_mma16; }
-                        const uint32_t idesc = idesc_i8(RO * K);
+                        const uint32_t idesc = idesc_n(RO * K);
                         const int t0 = warp - kZMmaWarp;
                         const uint32_t wbar = smem_u32(acc_empty + new_bar[2] + t0), wpar = new_par[2];
                         const uint32_t cbar = smem_u32(acc_full + done_bar[0] + t0);
@@ -663,7 +767,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const uint32_t d_tile = tmem_base + t * RO * K;
 #pragma unroll
                             for (int m = 0; m < NMMA; ++m)
-                                tc_mma_i8(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc, 1u);
+                                mma(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc);
                             tc_commit_addr(cbar + k * kBarStep);
                         }
                     } else
@@ -677,31 +781,31 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
                         if constexpr (SPLIT) {
-                            const uint32_t idesc1 = idesc_i8(g_n1 * K);
+                            const uint32_t idesc1 = idesc_n(g_n1 * K);
 #pragma unroll
                             for (int m = 0; m < NMMA; ++m)
-                                tc_mma_i8(d_tile + g_d1, desc64(a_lo[m] + a_add), desc64(g_b1 + m * b_mma16), idesc1, 1u);
+                                mma(d_tile + g_d1, desc64(a_lo[m] + a_add), desc64(g_b1 + m * b_mma16), idesc1);
                             if (g_n2) {
-                                const uint32_t idesc2 = idesc_i8(g_n2 * K);
+                                const uint32_t idesc2 = idesc_n(g_n2 * K);
 #pragma unroll
                                 for (int m = 0; m < NMMA; ++m)
-                                    tc_mma_i8(d_tile, desc64(a_lo[m] + a_add), desc64(g_b2 + m * b_mma16), idesc2, 1u);
+                                    mma(d_tile, desc64(a_lo[m] + a_add), desc64(g_b2 + m * b_mma16), idesc2);
                             }
                         } else if (full) {
-                            const uint32_t idesc = idesc_i8(RO * K);
+                            const uint32_t idesc = idesc_n(RO * K);
 #pragma unroll
                             for (int m = 0; m < NMMA; ++m)
-                                tc_mma_i8(d_tile, desc64(a_lo[m] + a_add), desc64(bl_full + m * b_mma16), idesc, 1u);
+                                mma(d_tile, desc64(a_lo[m] + a_add), desc64(bl_full + m * b_mma16), idesc);
                         } else {
-                            const uint32_t idesc = idesc_i8(K);
+                            const uint32_t idesc = idesc_n(K);
 #pragma unroll
                             for (int j = 0; j < 3; ++j) {
                                 if (j < nz) {
                                     const uint32_t bl = b_lo0 + sgl_b[j] * K;
 #pragma unroll
                                     for (int m = 0; m < NMMA; ++m)
-                                        tc_mma_i8(d_tile + sgl_d[j], desc64(a_lo[m] + a_add), desc64(bl + m * b_mma16),
-                                                  idesc, 1u);
+                                        mma(d_tile + sgl_d[j], desc64(a_lo[m] + a_add), desc64(bl + m * b_mma16),
+                                                  idesc);
                                 }
                             }
                         }
@@ -790,13 +894,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             for (int i = 15; i >= 0; --i) {
                                 const int d = acc[i];
                                 nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
-                                nlo = __funnelshift_l(static_cast<uint32_t>(lmh[i] - d), nlo, 1);
+                                const int e = F4 ? __float_as_int(__int_as_float(lmh[i]) - __int_as_float(d)) : lmh[i] - d;
+                                nlo = __funnelshift_l(static_cast<uint32_t>(e), nlo, 1);
                             }
                             const int w = c >> 5, sh = c & 31;
                             const uint32_t sb = (~nhi & 0xFFFFu) << sh, mb = (~(nhi & nlo) & 0xFFFFu) << sh;
                             if (sh == 0) { sbits[w] = sb; mbits[w] = mb; }
                             else { sbits[w] |= sb; mbits[w] |= mb; }
                         } else if (vpos) {
+                            if (F4) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) acc[i] = __float2int_rn(__int_as_float(acc[i]));
+                            }
                             int4* dst = reinterpret_cast<int4*>(cd.y + (vplane + voff) * K + c);
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
@@ -890,7 +999,7 @@ static size_t tz_smem(const TzPlan& pl, int K) {
            (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
 }
 
-static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
+static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 = false) {
     constexpr size_t kSmemMax = 227 * 1024;
     if (cd.nseg < 1 || cd.nseg > 2 || cd.y_in != nullptr) return false;
     for (int a = 0; a < 3; ++a)
@@ -920,11 +1029,18 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
         ct = 1;
     }
     if (ct > 4) return false;
+    if (f4 && first) return false;
+    pl.f4 = f4;
+    pl.nreg = 0;
+    for (int i = 0; i < cd.nseg; ++i) {
+        pl.reg0[i] = pl.nreg;
+        pl.nreg += f4 ? std::max(1, cd.seg[i].c / 32) : 0;
+    }
     if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
         cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    const bool split = pl.s == 1 && cd.K == 64;
+    const bool split = pl.s == 1 && cd.K == 64 && !f4;
     pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
@@ -960,21 +1076,69 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
         return a.row < b.row;
     });
     if (first) sl.assign(1, Sl{0, 0, 0, 0});   // the whole 3x3 window is one row
-    pl.nmma = static_cast<int>((sl.size() + 1) / 2);
-    if (pl.nmma > kZMaxMma || pl.nmma != (first ? 1 : (9 * ct + 1) / 2)) return false;   // the kernel unrolls
+    // F4 slices: (segment, region, row offset, tap a, tap b).  C = 16 segments pair
+    // the taps of one (dy, phase) whose column offsets differ by one (a row holds
+    // positions r and r+1); C >= 32 segments take one 32-channel region per tap.
+    struct Sl4 { int ph, reg, row, tap, tapb, seg, c32; };
+    std::vector<Sl4> sl4;
+    if (f4) {
+        for (int sg = 0; sg < cd.nseg; ++sg) {
+            const int C = cd.seg[sg].c;
+            for (int dy = 0; dy < 3; ++dy) {
+                struct Tp { int ph, oy, ox, tap; };
+                std::vector<Tp> tp;
+                for (int dx = 0; dx < 3; ++dx) {
+                    int ph = 0, oy = dy, ox = dx;
+                    if (pl.s == 2) {
+                        const int py = dy == 1 ? 0 : 1, px = dx == 1 ? 0 : 1;
+                        oy = dy == 0 ? 0 : 1;
+                        ox = dx == 0 ? 0 : 1;
+                        ph = py * 2 + px;
+                    }
+                    tp.push_back({ph, oy, ox, dy * 3 + dx});
+                }
+                std::sort(tp.begin(), tp.end(), [](const Tp& a, const Tp& b) {
+                    return a.ph != b.ph ? a.ph < b.ph : a.ox < b.ox;
+                });
+                if (C == 16) {
+                    for (size_t i = 0; i < tp.size();) {
+                        const bool pair = i + 1 < tp.size() && tp[i + 1].ph == tp[i].ph && tp[i + 1].ox == tp[i].ox + 1;
+                        sl4.push_back({tp[i].ph, pl.reg0[sg], tp[i].oy * pl.Po + tp[i].ox, tp[i].tap,
+                                       pair ? tp[i + 1].tap : -1, sg, 0});
+                        i += pair ? 2 : 1;
+                    }
+                } else {
+                    for (const Tp& t : tp)
+                        for (int c = 0; c < C / 32; ++c)
+                            sl4.push_back({t.ph, pl.reg0[sg] + c, t.oy * pl.Po + t.ox, t.tap, -1, sg, c});
+                }
+            }
+        }
+        std::sort(sl4.begin(), sl4.end(), [](const Sl4& a, const Sl4& b) {
+            if (a.ph != b.ph) return a.ph < b.ph;
+            if (a.reg != b.reg) return a.reg < b.reg;
+            return a.row < b.row;
+        });
+    }
+    const size_t nsl = f4 ? sl4.size() : sl.size();
+    pl.nmma = static_cast<int>((nsl + 1) / 2);
+    {
+        const int nmma_f4 = cd.nseg == 1 ? (ct == 1 ? 3 : (ct == 2 ? 5 : 9)) : (ct == 2 ? 6 : (ct == 3 ? 8 : 9));
+        if (pl.nmma > kZMaxMma || pl.nmma != (f4 ? nmma_f4 : first ? 1 : (9 * ct + 1) / 2)) return false;   // kernel unrolls
+    }
     pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
     const int ptab = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
     pl.ptab_floats = ptab;
 
     // strip size: the most tiles that fit TMEM (RO*K*T <= 512) and shared memory
-    const int tmax = std::min(512 / (pl.RO * cd.K), kZMaxAcc / pl.RO);
+    const int tmax = std::min((f4 ? 480 : 512) / (pl.RO * cd.K), kZMaxAcc / pl.RO);   // F4: scales at 480..511
     bool ok = false;
     for (int T = std::min(tmax, pl.NT); T >= 1 && !ok; --T) {
         pl.T = T;
         pl.nstrip = (pl.NT + T - 1) / T;
         pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.Po + 2 : pl.Po + 1);
-        pl.REG = round_up(pl.RS * 16, 128);
-        pl.slot_bytes = first ? 128 * T * 16 + 256 : pl.nph * ct * pl.REG + 256;
+        pl.REG = round_up((pl.RS + (f4 ? 1 : 0)) * 16, 128);    // F4: a 16-byte guard row first
+        pl.slot_bytes = first ? 128 * T * 16 + 256 : pl.nph * (f4 ? pl.nreg : ct) * pl.REG + 256;
         // staging: the most rows any strip reads, per segment
         int off = 0;
         for (int sg = 0; sg < cd.nseg; ++sg) {
@@ -1013,18 +1177,30 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false) {
     if (!ok) return false;
     pl.code_off = pl.nstage * pl.stage_bytes;    // relative to the staging base
     for (size_t j = 0; j < 2 * static_cast<size_t>(pl.nmma); ++j) {
-        if (j < sl.size()) {
-            pl.sl_tap[j] = static_cast<int8_t>(sl[j].tap);
-            pl.sl_chunk[j] = static_cast<int8_t>(sl[j].ch);
+        pl.sl_tapb[j] = -1;
+        pl.sl_seg[j] = 0;
+        if (j < nsl) {
+            if (f4) {
+                pl.sl_tap[j] = static_cast<int8_t>(sl4[j].tap);
+                pl.sl_tapb[j] = static_cast<int8_t>(sl4[j].tapb);
+                pl.sl_chunk[j] = static_cast<int8_t>(sl4[j].c32);
+                pl.sl_seg[j] = static_cast<int8_t>(sl4[j].seg);
+            } else {
+                pl.sl_tap[j] = static_cast<int8_t>(sl[j].tap);
+                pl.sl_chunk[j] = static_cast<int8_t>(sl[j].ch);
+            }
         } else {
             pl.sl_tap[j] = -1;
             pl.sl_chunk[j] = 0;
         }
     }
-    auto addr = [&](size_t j) { return first ? 0 : (sl[j].ph * ct + sl[j].ch) * pl.REG + sl[j].row * 16; };
+    auto addr = [&](size_t j) {
+        if (f4) return (sl4[j].ph * pl.nreg + sl4[j].reg) * pl.REG + 16 + sl4[j].row * 16;
+        return first ? 0 : (sl[j].ph * ct + sl[j].ch) * pl.REG + sl[j].row * 16;
+    };
     for (int m = 0; m < pl.nmma; ++m) {
         const int a0 = addr(2 * m);
-        const int a1 = (2 * m + 1 < static_cast<int>(sl.size())) ? addr(2 * m + 1) : a0 + 16;   // zero-weight dummy
+        const int a1 = (2 * m + 1 < static_cast<int>(nsl)) ? addr(2 * m + 1) : a0 + 16;   // zero-weight dummy
         if (a1 <= a0 || a1 - a0 > 0x3FFF * 16) return false;
         pl.a_off[m] = a0;
         pl.a_lbo[m] = a1 - a0;
@@ -1038,14 +1214,23 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     void (*kern)(ConvDesc, TzPlan) = nullptr;
     const bool pred = cd.logits != nullptr;
 #define TZ_PICK(CT_, NSEG_, STR_)                                                                     \
-    if (ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                                \
-        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false> : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false>;
+    if (!pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                      \
+        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, false>                     \
+                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, false>;
+#define TZ_PICK4(CT_, NSEG_, STR_)                                                                    \
+    if (pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                       \
+        kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, true>                      \
+                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, true>;
     TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(4, 1, 1)
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
     TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(4, 1, 2)
+    TZ_PICK4(1, 1, 1) TZ_PICK4(2, 1, 1) TZ_PICK4(4, 1, 1)
+    TZ_PICK4(2, 2, 1) TZ_PICK4(4, 2, 1)
+    TZ_PICK4(1, 1, 2) TZ_PICK4(2, 1, 2) TZ_PICK4(4, 1, 2)
 #undef TZ_PICK
+#undef TZ_PICK4
     if (kern == nullptr) return cudaErrorNotSupported;
-    static void* configured[64] = {nullptr};
+    static void* configured[128] = {nullptr};
     bool done = false;
     for (void* f : configured) done = done || f == reinterpret_cast<void*>(kern);
     if (!done) {
@@ -1061,6 +1246,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
 static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
     int ct = 0;
     for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
+    if (pl.f4 && cd.nseg == 2 && ct == 3) return false;
     if (pl.s == 2) return cd.nseg == 1 && (ct == 1 || ct == 2 || ct == 4);
     if (cd.nseg == 1) return ct == 1 || ct == 2 || ct == 4;
     return ct >= 2;
@@ -1117,7 +1303,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
     const int cap = persistent_grid_cap() > 0 ? std::min(persistent_grid_cap(), g_num_sms_z) : g_num_sms_z;
     const int grid = static_cast<int>(std::min<int64_t>(pl.units, cap));
     void (*kern)(ConvDesc, TzPlan) =
-        fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true> : conv_tz_kernel<32, 1, 1, 1, false, true>;
+        fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true, false> : conv_tz_kernel<32, 1, 1, 1, false, true, false>;
     static bool configured[2] = {false, false};
     if (!configured[fd.K == 32]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1128,15 +1314,34 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-bool conv_tz_supported(const ConvDesc& cd) {
-    TzPlan pl{};
-    if (!plan_tz(cd, pl)) return false;
-    return tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024;
+// F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
+static bool plan_any(const ConvDesc& cd, TzPlan& pl, bool allow_f4) {
+    // Measured (tools/conv_time.py, configs[3] layer shapes): FP4 wins for stride-1
+    // layers with K <= 32 (#4 -10 %, #10 -21 %, #12 -23 %, #13 -2 %); at C = K = 64 the
+    // FP4 kernel is bound by shared-memory operand bandwidth (10 KB per 96-cycle MMA)
+    // and only 4 % faster, and at stride 2 with C = 32 it is slower.
+    int c_tot = 0;
+    for (int i = 0; i < cd.nseg; ++i) c_tot += cd.seg[i].c;
+    allow_f4 = allow_f4 && cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16);
+    if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024)
+        return true;
+    pl = TzPlan{};
+    return plan_tz(cd, pl, false, false) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024;
 }
 
-cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st) {
+bool conv_tz_supported(const ConvDesc& cd, bool allow_f4) {
     TzPlan pl{};
-    if (!plan_tz(cd, pl) || !tz_instantiated(cd, pl)) return cudaErrorNotSupported;
+    return plan_any(cd, pl, allow_f4);
+}
+
+bool conv_tz_uses_f4(const ConvDesc& cd, bool allow_f4) {
+    TzPlan pl{};
+    return plan_any(cd, pl, allow_f4) && pl.f4;
+}
+
+cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
+    TzPlan pl{};
+    if (!plan_any(cd, pl, allow_f4)) return cudaErrorNotSupported;
     const size_t smem = tz_smem(pl, cd.K);
     if (g_num_sms_z == 0) {
         int dev = 0;

@@ -38,6 +38,37 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra TN_WAITS_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
 }
+// 8 ternary lanes (bits of a mask / negative byte) -> 8 FP4 E2M1 nibbles:
+// +1 -> 0x2 (1.0), -1 -> 0xA (-1.0), 0 -> 0x0; nibble k = lane k (k even in the
+// low nibble of byte k/2, the element order of packed e2m1 operands).
+__device__ __forceinline__ uint32_t spread8_nib(uint32_t t) {
+    t &= 0xFFu;
+    t = (t | (t << 12)) & 0x000F000Fu;
+    t = (t | (t << 6)) & 0x03030303u;
+    t = (t | (t << 3)) & 0x11111111u;
+    return t;
+}
+// 16 ternary lanes (bits sh..sh+15 of a sign / mask word pair) -> 16 FP4 nibbles
+__device__ __forceinline__ uint2 expand16_f4(uint32_t s, uint32_t m, int sh) {
+    const uint32_t mm = m >> sh, nn = (m & ~s) >> sh;
+    const uint32_t lo = (spread8_nib(mm) << 1) | (spread8_nib(nn) << 3);
+    const uint32_t hi = (spread8_nib(mm >> 8) << 1) | (spread8_nib(nn >> 8) << 3);
+    return make_uint2(lo, hi);
+}
+__device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+// Instruction descriptor for kind::mxf4: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N, K = 64.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
+    return (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+}
+
 // Waits / commits on a barrier given by its shared-memory address.
 __device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
     asm volatile(

@@ -102,7 +102,9 @@ bool        conv_tc_supported(const ConvDesc& cd);
 cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
 // tcgen05 tap-offset, z-merged implicit GEMM (conv_tz.cu): C, K <= 64 with a
 // small filter bank; same contract.
-bool        conv_tz_supported(const ConvDesc& cd);
+// allow_f4: may use FP4 E2M1 operands (kind::mxf4; exact, twice the int8 rate).
+bool        conv_tz_supported(const ConvDesc& cd, bool allow_f4 = true);
+bool        conv_tz_uses_f4(const ConvDesc& cd, bool allow_f4 = true);
 // A7 on the TZ kernel (stride 1, pad 1, K in {16, 32}, W % 4 == 0); false if the
 // shape is outside it (the caller then uses conv_first_kernel).
 bool        conv_tz_first_supported(const FirstDesc& fd);
@@ -111,7 +113,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t s);
 int         persistent_grid_cap();
 // The first layer may use the TZ kernel under the current selector (AUTO or TZ).
 bool        first_kernel_tz_allowed();
-cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s);
+cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s, bool allow_f4 = true);
 
 }  // namespace tn
 

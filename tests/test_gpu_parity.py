@@ -24,13 +24,14 @@ def tn():
     return tn
 
 
-SELECTORS = {"popc": 1, "tc": 2, "tz": 3, "auto": 0, "tz_cap3": 3, "tc_cap3": 2}
+SELECTORS = {"popc": 1, "tc": 2, "tz": 3, "tz8": 4, "auto": 0, "tz_cap3": 3, "tz8_cap3": 4, "tc_cap3": 2}
 
 
-@pytest.fixture(params=["popc", "tc", "tz", "auto", "tz_cap3", "tc_cap3"])
+@pytest.fixture(params=["popc", "tc", "tz", "tz8", "auto", "tz_cap3", "tz8_cap3", "tc_cap3"])
 def kernel(request, tn):
     """Run a conv test with the CUDA-core popc kernel, one of the tcgen05 kernels
-    (skipped for shapes it does not cover), or the automatic choice.  The _cap3
+    (tz = FP4 operands where they fit, tz8 = int8 operands; skipped for shapes a
+    kernel does not cover), or the automatic choice.  The _cap3
     variants cap the persistent grid at 3 CTAs, so each CTA walks long runs of
     output planes (TMEM block rotation, ring wrap-around, run boundaries)."""
     tn.tn_set_conv_kernel(SELECTORS[request.param])
@@ -40,9 +41,9 @@ def kernel(request, tn):
     tn.tn_set_grid_cap(0)
 
 
-@pytest.fixture(params=["popc", "tc", "auto", "auto_cap5"])
+@pytest.fixture(params=["popc", "tc", "tz8", "auto", "auto_cap5"])
 def fcn_kernel(request, tn):
-    tn.tn_set_conv_kernel({"popc": 1, "tc": 2, "auto": 0, "auto_cap5": 0}[request.param])
+    tn.tn_set_conv_kernel({"popc": 1, "tc": 2, "tz8": 4, "auto": 0, "auto_cap5": 0}[request.param])
     tn.tn_set_grid_cap(5 if request.param.endswith("cap5") else 0)
     yield request.param
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
@@ -346,7 +347,8 @@ def test_c1_full_size_sampled(tn):
 # sampled outputs against the oracle's per-output sum + the packed/int32 agreement.
 C3_LAYER_CASES = [
     # (C, K, stride, kernel)
-    (16, 16, 1, "tz"), (16, 16, 1, "tc"), (16, 16, 2, "tz"), (16, 16, 2, "tc"), (16, 32, 1, "tz"),
+    (16, 16, 1, "tz"), (16, 16, 1, "tz8"), (16, 16, 1, "tc"), (16, 16, 2, "tz"), (16, 16, 2, "tz8"),
+    (16, 16, 2, "tc"), (16, 32, 1, "tz"), (32, 16, 1, "tz"), (64, 32, 1, "tz"),
 ]
 
 
