@@ -68,6 +68,12 @@ __device__ long long g_tztrace[148 * 16];
 #ifndef TZ_EXP_NOEXP
 #define TZ_EXP_NOEXP 0
 #endif
+#ifndef TZ_EXP_NOFENCE
+#define TZ_EXP_NOFENCE 0
+#endif
+#ifndef TZ_EXP_NOMMA
+#define TZ_EXP_NOMMA 0
+#endif
 #ifndef TZ_EXP_NOACCWAIT
 #define TZ_EXP_NOACCWAIT 0
 #endif
@@ -103,7 +109,10 @@ __host__ __device__ constexpr int tz_threads(bool pred, int ct) {
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
 constexpr int kZMaxSlot = 4;          // A ring
-constexpr int kZMaxStage = 4;         // packed staging ring
+#ifndef TZ_MAX_STAGE
+#define TZ_MAX_STAGE 4
+#endif
+constexpr int kZMaxStage = TZ_MAX_STAGE;         // packed staging ring
 constexpr int kZMaxClass = 8;
 
 struct TzPlan {
@@ -638,7 +647,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }   // !F4
                 }   // !FIRST
                 mbar_arrive(staged_empty + st);
-                fence_proxy_async();
+                if (!TZ_EXP_NOFENCE) fence_proxy_async();
                 mbar_arrive(plane_full + as);
                 if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                 if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
@@ -662,6 +671,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         const uint32_t sfa = tmem_base + 480, sfb = tmem_base + 496;
         auto idesc_n = [](uint32_t n) { return F4 ? idesc_mxf4(static_cast<int>(n)) : idesc_i8(static_cast<int>(n)); };
         auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id) {
+            if (TZ_EXP_NOMMA) return;
             if constexpr (F4) tc_mma_mxf4(d, a, b, id, sfa, sfb);
             else tc_mma_i8(d, a, b, id, 1u);
         };
