@@ -330,6 +330,8 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *s_tmem;
+    pdl_launch_dependents();
+    pdl_wait();   // activations of the previous layer are complete and visible from here on
 #if TN_EXP_PROF
     if (threadIdx.x == 0) g_trace[16 * blockIdx.x + 14] = clock64() - k_begin;
 #endif
@@ -786,7 +788,7 @@ static bool plan_full(const ConvDesc& cd, TcPlan& pl) {
     return true;
 }
 
-// Launched as (trivial) 1-CTA clusters: st.async addresses shared::cluster.
+// Launched with programmatic stream serialisation (PDL): the setup overlaps the previous kernel's tail.
 static cudaError_t launch_one(void (*kern)(ConvDesc, TcPlan), const ConvDesc& cd, const TcPlan& pl, int64_t grid,
                               size_t smem, cudaStream_t st) {
     // cudaFuncSetAttribute is a slow host call: raise the kernel's smem limit once
@@ -806,12 +808,10 @@ static cudaError_t launch_one(void (*kern)(ConvDesc, TcPlan), const ConvDesc& cd
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait in the kernel
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 0;   // plain launch (no cluster needed)
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, cd, pl);
 }
 

@@ -369,6 +369,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         tc_fence_after();
     }
     const uint32_t tmem_base = *s_tmem;
+    pdl_launch_dependents();
+    pdl_wait();   // activations of the previous layer are complete and visible from here on
 
     if (warp < kZEpiWarps) {
         // ---- initialise this warp's TMEM blocks (its quadrant, its tiles, all RO blocks)
@@ -1002,6 +1004,23 @@ int g_num_sms_z = 0;
 // ---------------------------------------------------------------- host plan
 static int round_up(int v, int a) { return (v + a - 1) / a * a; }
 
+// Launch with programmatic stream serialisation (see pdl_wait in the kernel).
+static cudaError_t launch_pdl(void (*kern)(ConvDesc, TzPlan), int grid, int threads, size_t smem, cudaStream_t st,
+                              const ConvDesc& cd, const TzPlan& pl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, cd, pl);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 static size_t tz_smem(const TzPlan& pl, int K) {
     return static_cast<size_t>(pl.nslot) * pl.slot_bytes + pl.b_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
            2 * static_cast<size_t>(pl.code_bytes) +
@@ -1249,8 +1268,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
         for (void*& f : configured)
             if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
     }
-    kern<<<grid, tz_threads(pred && K <= 32, ct), smem, st>>>(cd, pl);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, tz_threads(pred && K <= 32, ct), smem, st, cd, pl);
 }
 
 static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
@@ -1320,8 +1338,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    kern<<<grid, tz_threads(false, 1), smem, st>>>(cd, pl);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, tz_threads(false, 1), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.

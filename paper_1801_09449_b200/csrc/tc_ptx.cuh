@@ -69,6 +69,13 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
     return (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
 }
 
+// Programmatic dependent launch: the conv kernels are launched with
+// programmatic stream serialisation, so a layer's setup (filter-bank expansion,
+// barriers, TMEM) overlaps the previous layer's tail; every thread waits for
+// the previous grid (and its memory) before touching activations.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Waits / commits on a barrier given by its shared-memory address.
 __device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
     asm volatile(
