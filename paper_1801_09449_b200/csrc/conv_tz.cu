@@ -215,7 +215,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // columns 480..511): exact (f32 accumulation of integers < 2^24), half the
     // shared-memory bytes per MAC and twice the int8 MMA rate.  C = 16 segments
     // hold two consecutive positions per 16-byte row (taps dx, dx+1 in one K-half).
-    constexpr bool SPLIT = STR == 1 && K == 64 && !F4;
+    constexpr bool SPLIT = STR == 1 && K == 64;
     constexpr int RO = STR == 1 ? (SPLIT ? 4 : 3) : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
     constexpr int NB = STR == 1 ? (SPLIT ? 3 : 5) : 4;
@@ -668,7 +668,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         // K-slice pair (start address and LBO); per (slot, tile) only an add remains,
         // so the issue loop stays well under the 40+ cycles one N = 3K MMA takes.
         // F4 slices: 6 per C = 16 segment (two-position rows), 9 per 32 channels
-        constexpr int NMMA = F4 ? (NSEG == 1 ? (CT == 1 ? 3 : (CT == 2 ? 5 : 9)) : (CT == 2 ? 6 : (CT == 3 ? 8 : 9)))
+        constexpr int NMMA = F4 ? (NSEG == 1 ? (CT == 1 ? 3 : (CT == 2 ? 5 : 9))
+                                             : (CT == 2 ? 6 : (CT == 3 ? 8 : (CT == 4 ? 9 : 18))))
                                 : (FIRST ? 1 : (9 * CT + 1) / 2);
         const uint32_t sfa = tmem_base + 480, sfb = tmem_base + 496;
         auto idesc_n = [](uint32_t n) { return F4 ? idesc_mxf4(static_cast<int>(n)) : idesc_i8(static_cast<int>(n)); };
@@ -1057,7 +1058,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         pl.cch[0] = 1;
         ct = 1;
     }
-    if (ct > 4) return false;
+    if (ct > (f4 ? 8 : 4)) return false;   // F4: two 64-channel segments (the 64+64 -> 64 decoder block)
     if (f4 && first) return false;
     pl.f4 = f4;
     pl.nreg = 0;
@@ -1069,7 +1070,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    const bool split = pl.s == 1 && cd.K == 64 && !f4;
+    const bool split = pl.s == 1 && cd.K == 64;
     pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
@@ -1152,7 +1153,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     const size_t nsl = f4 ? sl4.size() : sl.size();
     pl.nmma = static_cast<int>((nsl + 1) / 2);
     {
-        const int nmma_f4 = cd.nseg == 1 ? (ct == 1 ? 3 : (ct == 2 ? 5 : 9)) : (ct == 2 ? 6 : (ct == 3 ? 8 : 9));
+        const int nmma_f4 =
+            cd.nseg == 1 ? (ct == 1 ? 3 : (ct == 2 ? 5 : 9)) : (ct == 2 ? 6 : (ct == 3 ? 8 : (ct == 4 ? 9 : 18)));
         if (pl.nmma > kZMaxMma || pl.nmma != (f4 ? nmma_f4 : first ? 1 : (9 * ct + 1) / 2)) return false;   // kernel unrolls
     }
     pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
@@ -1254,7 +1256,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
     TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(4, 1, 2)
     TZ_PICK4(1, 1, 1) TZ_PICK4(2, 1, 1) TZ_PICK4(4, 1, 1)
-    TZ_PICK4(2, 2, 1) TZ_PICK4(4, 2, 1)
+    TZ_PICK4(2, 2, 1) TZ_PICK4(4, 2, 1) if (K == 64) { TZ_PICK4(8, 2, 1) }
     TZ_PICK4(1, 1, 2) TZ_PICK4(2, 1, 2) TZ_PICK4(4, 1, 2)
 #undef TZ_PICK
 #undef TZ_PICK4
@@ -1275,6 +1277,7 @@ static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
     int ct = 0;
     for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
     if (pl.f4 && cd.nseg == 2 && ct == 3) return false;
+    if (ct == 8) return pl.f4 && cd.K == 64 && pl.s == 1 && cd.nseg == 2;
     if (pl.s == 2) return cd.nseg == 1 && (ct == 1 || ct == 2 || ct == 4);
     if (cd.nseg == 1) return ct == 1 || ct == 2 || ct == 4;
     return ct >= 2;
@@ -1343,17 +1346,23 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
 static bool plan_any(const ConvDesc& cd, TzPlan& pl, bool allow_f4) {
+    const bool allow_any_f4 = allow_f4;
     // Measured (tools/conv_time.py, configs[3] layer shapes): FP4 wins for stride-1
     // layers with K <= 32 (#4 -10 %, #10 -21 %, #12 -23 %, #13 -2 %); at C = K = 64 the
     // FP4 kernel is bound by shared-memory operand bandwidth (10 KB per 96-cycle MMA)
     // and only 4 % faster, and at stride 2 with C = 32 it is slower.
     int c_tot = 0;
     for (int i = 0; i < cd.nseg; ++i) c_tot += cd.seg[i].c;
-    allow_f4 = allow_f4 && cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16);
+    // C > 64 (the 64 + 64 -> 64 decoder block) only fits with FP4 operands (half the B bytes)
+    allow_f4 = allow_f4 && ((cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16)) || c_tot > 64);
     if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024)
         return true;
     pl = TzPlan{};
-    return plan_tz(cd, pl, false, false) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024;
+    if (plan_tz(cd, pl, false, false) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024) return true;
+    // shapes the int8 operands do not fit (e.g. 64 -> 64 at stride 2): FP4 if allowed at all
+    pl = TzPlan{};
+    return allow_any_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) &&
+           tz_smem(pl, cd.K) <= 227 * 1024;
 }
 
 bool conv_tz_supported(const ConvDesc& cd, bool allow_f4) {

@@ -215,7 +215,8 @@ def test_requant_sentinels_and_order(tn):
 # --------------------------------------------------------------------------- A6 upsample + concat
 @pytest.mark.parametrize("low,cl,cs,k", [((3, 4, 5), 16, 16, 16), ((2, 3, 9), 64, 64, 64),
                                          ((4, 4, 4), 32, 32, 32), ((1, 1, 1), 16, 16, 8),
-                                         ((5, 6, 7), 16, 16, 16), ((3, 5, 4), 32, 32, 32), ((4, 3, 6), 16, 32, 16)])
+                                         ((5, 6, 7), 16, 16, 16), ((3, 5, 4), 32, 32, 32), ((4, 3, 6), 16, 32, 16),
+                                         ((4, 5, 6), 64, 64, 64)])
 def test_conv3d_upsample_concat_matches_oracle(tn, kernel, low, cl, cs, k):
     n = 1
     a = synth.ternary_codes((n, cl) + low, 0.5, seed=cl)
