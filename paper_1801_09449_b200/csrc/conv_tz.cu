@@ -551,6 +551,19 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 // FP4 rows: C = 16 segments write the position into the low half of
                 // row r and the high half of row r-1 (a 16-byte guard row precedes each
                 // region); C = 32 / 64 segments write one / two 16-byte rows.
+                // A nearest-x2 upsampled C = 16 segment feeds 4 positions per source
+                // voxel and plane: its staged words are converted to FP4 in place first
+                // (packed 16 channels and FP4 16 channels are both 8 bytes).
+                const bool up_conv = NSEG == 2 && cd.seg[0].c == 16;
+                if (up_conv) {
+                    uint2* p0 = reinterpret_cast<uint2*>(const_cast<uint8_t*>(stg) + pl.seg_off[0]);
+                    const int nv = nr[0] * cd.seg[0].W;
+                    for (int e = et; e < nv; e += kZExpThreads) {
+                        const uint2 w = p0[e];
+                        p0[e] = expand16_f4(w.x, w.y, 0);
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"r"(kZExpThreads) : "memory");
+                }
                 int r = TZ_EXP_NOEXP ? pl.RS : et;
                 int y, x;
                 {
@@ -577,7 +590,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             if (sd.c == 16) {
                                 uint2 w = make_uint2(0u, 0u);
                                 if (ok) w = *reinterpret_cast<const uint2*>(sp);
-                                const uint2 e = expand16_f4(w.x, w.y, 0);
+                                const uint2 e = (up && up_conv) ? w : expand16_f4(w.x, w.y, 0);
                                 *reinterpret_cast<uint2*>(rb) = e;
                                 *reinterpret_cast<uint2*>(rb - 8) = e;
                             } else if (sd.cw == 1) {
