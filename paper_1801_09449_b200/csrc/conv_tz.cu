@@ -68,6 +68,14 @@ __device__ long long g_tztrace[148 * 16];
 #ifndef TZ_EXP_NOEXP
 #define TZ_EXP_NOEXP 0
 #endif
+// Tiles per synchronisation unit: the MMA issuers and the epilogue hand TMEM
+// blocks over per unit of TU consecutive tiles (one mbarrier wait / commit /
+// arrive per unit instead of per tile).  Measured: 3 for the one-segment K = 16
+// layers (#1 -4 %, #2 -5 %), 1 elsewhere (C1 with two tiles per strip needs the
+// per-tile hand-over).
+#ifndef TZ_TU
+#define TZ_TU ((K == 16 && NSEG == 1) ? 3 : 1)
+#endif
 #ifndef TZ_EXP_NOFENCE
 #define TZ_EXP_NOFENCE 0
 #endif
@@ -241,6 +249,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     const int lane = threadIdx.x & 31;
     const bool fused = cd.yp != nullptr;
     const int T = pl.T;
+    const int NU = (T + TZ_TU - 1) / TZ_TU;   // synchronisation units per strip
 #if TN_EXP_PROF
     const long long k_begin = clock64();
     long long k_gstart = 0;
@@ -378,7 +387,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         int iv[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) iv[k] = s_nhi[k];
-        for (int t = g; t < T; t += kZEpiGroups)
+        for (int t = 0; t < T; ++t)
+            if ((t / TZ_TU) % kZEpiGroups == g)
             for (int b = 0; b < RO; ++b)
 #pragma unroll
                 for (int c = 0; c < K; c += 16)
@@ -739,10 +749,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const uint32_t sg = u % RO;
                             const int first = max(STR * z - 1, 0), last = min(STR * z + 1, cd.Dci - 1);
                             is_new[j] = first == i && u >= static_cast<uint32_t>(RO);
-                            new_bar[j] = sg * T;
+                            new_bar[j] = sg * NU;
                             new_par[j] = ((u / RO) - 1) & 1;
                             is_done[j] = last == i;
-                            done_bar[j] = sg * T;
+                            done_bar[j] = sg * NU;
                             const int dz = i - STR * z + 1;
                             // block holding dz: s1 [2 1 0 ..] -> 2 - dz; s2 [0 2 0 1] -> dz0:0 dz2:1 dz1:3
                             sgl_b[j] = STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
@@ -781,29 +791,34 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                         for (int m = 0; m < NMMA; ++m) { a_pl[m] = a_lo[m] + a_slot16; b_pl[m] = bl_full + m * b_mma16; }
                         const uint32_t idesc = idesc_n(RO * K);
-                        const int t0 = warp - kZMmaWarp;
-                        const uint32_t wbar = smem_u32(acc_empty + new_bar[2] + t0), wpar = new_par[2];
-                        const uint32_t cbar = smem_u32(acc_full + done_bar[0] + t0);
+                        const int v0 = warp - kZMmaWarp;
+                        const uint32_t wbar = smem_u32(acc_empty + new_bar[2] + v0), wpar = new_par[2];
+                        const uint32_t cbar = smem_u32(acc_full + done_bar[0] + v0);
                         constexpr uint32_t kBarStep = 8 * kZMmaWarps;
                         int k = 0;
-                        for (int t = t0; t < Tv; t += kZMmaWarps, ++k) {
+                        for (int v = v0; v * TZ_TU < Tv; v += kZMmaWarps, ++k) {
                             if (!TZ_EXP_NOACCWAIT) mbar_wait_addr(wbar + k * kBarStep, wpar);
                             tc_fence_after();
-                            const uint32_t a_add = t * 128;
-                            const uint32_t d_tile = tmem_base + t * RO * K;
+                            const int t1 = min((v + 1) * TZ_TU, Tv);
+                            for (int t = v * TZ_TU; t < t1; ++t) {
+                                const uint32_t a_add = t * 128;
+                                const uint32_t d_tile = tmem_base + t * RO * K;
 #pragma unroll
-                            for (int m = 0; m < NMMA; ++m)
-                                mma(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc);
+                                for (int m = 0; m < NMMA; ++m)
+                                    mma(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc);
+                            }
                             tc_commit_addr(cbar + k * kBarStep);
                         }
                     } else
-                    for (int t = warp - kZMmaWarp; t < Tv; t += kZMmaWarps) {
+                    for (int v = warp - kZMmaWarp; v * TZ_TU < Tv; v += kZMmaWarps) {
                         ZSTAMP(y1);
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (is_new[j] && !TZ_EXP_NOACCWAIT) TZ_WAIT(acc_empty + new_bar[j] + t, new_par[j]);
+                            if (is_new[j] && !TZ_EXP_NOACCWAIT) TZ_WAIT(acc_empty + new_bar[j] + v, new_par[j]);
                         ZACC(m_w2, y1);
                         tc_fence_after();
+                        const int t1 = min((v + 1) * TZ_TU, Tv);
+                        for (int t = v * TZ_TU; t < t1; ++t) {
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
                         if constexpr (SPLIT) {
@@ -835,9 +850,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 }
                             }
                         }
+                        }   // tiles of the unit
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (is_done[j]) tc_commit(acc_full + done_bar[j] + t);
+                            if (is_done[j]) tc_commit(acc_full + done_bar[j] + v);
                     }
                     tc_commit(plane_free + as);
                     if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
@@ -877,15 +893,17 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
-                for (int t = g; t < Tv; t += kZEpiGroups) {
+                for (int v = g; v * TZ_TU < Tv; v += kZEpiGroups) {
                     ZSTAMP(p0);
-                    TZ_WAIT(acc_full + sgm * T + t, par);
+                    TZ_WAIT(acc_full + sgm * NU + v, par);
                     ZACC(p_w, p0);
                     tc_fence_after();
 #if TZ_EXP_NOEPI
-                    mbar_arrive(acc_empty + sgm * T + t);
+                    mbar_arrive(acc_empty + sgm * NU + v);
                     continue;
 #endif
+                    const int t1 = min((v + 1) * TZ_TU, Tv);
+                    for (int t = v * TZ_TU; t < t1; ++t) {
                     const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
                     const int qpos = q_lane + t * 128;
                     const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
@@ -940,9 +958,6 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         // re-initialise the block for the output that reuses it
                         tmem_st16(taddr + c, nhv);
                     }
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(acc_empty + sgm * T + t);
                     if (fused && vpos) {
                         if (PRED) {
                             // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
@@ -983,6 +998,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             *reinterpret_cast<uint4*>(dst) = make_uint4(sbits[0], sbits[1], mbits[0], mbits[1]);
                         }
                     }
+                    }   // tiles of the unit
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(acc_empty + sgm * NU + v);
                 }
             }
         }
