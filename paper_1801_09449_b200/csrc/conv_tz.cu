@@ -1061,6 +1061,17 @@ static size_t tz_smem(const TzPlan& pl, int K) {
            (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
 }
 
+static int tz_num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0, v = 0;
+        n = (cudaGetDevice(&dev) == cudaSuccess &&
+             cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) ? v : 148;
+        cudaGetLastError();   // no device (CPU-side planning): clear the error, assume B200
+    }
+    return n;
+}
+
 static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 = false) {
     constexpr size_t kSmemMax = 227 * 1024;
     if (cd.nseg < 1 || cd.nseg > 2 || cd.y_in != nullptr) return false;
@@ -1196,7 +1207,14 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     // strip size: the most tiles that fit TMEM (RO*K*T <= 512) and shared memory
     const int tmax = std::min((f4 ? 480 : 512) / (pl.RO * cd.K), kZMaxAcc / pl.RO);   // F4: scales at 480..511
     bool ok = false;
-    for (int T = std::min(tmax, pl.NT); T >= 1 && !ok; --T) {
+    // smaller strips when the layer would otherwise give fewer units than SMs (the
+    // R3 layers: 16 planes of 9 tiles), so every SM gets work
+    int tstart = std::min(tmax, pl.NT);
+    {
+        const int nsm = tz_num_sms();
+        while (tstart > 1 && static_cast<int64_t>(cd.N) * ((pl.NT + tstart - 1) / tstart) * cd.Do < nsm) --tstart;
+    }
+    for (int T = tstart; T >= 1 && !ok; --T) {
         pl.T = T;
         pl.nstrip = (pl.NT + T - 1) / T;
         pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.Po + 2 : pl.Po + 1);
