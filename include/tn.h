@@ -209,6 +209,34 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
                                      float* logits, void* ws, size_t ws_bytes, int64_t* d_bad,
                                      tn_stream stream);
 
+/* ---- Model preparation (host, not on the hot path) ---------
+ * tn_ternarize_weights: Eq. 4 per output filter f of a float
+ * filter bank w[k][n] (host, row-major; n = C_in * 27): Delta = 0.7/n sum|W_i|,
+ * code +1 if W_i > Delta, 0 if |W_i| <= Delta, -1 else; alpha[f] = mean |W_i|
+ * over the nonzero codes (0 if none).  sparsity in [0, 1) instead fixes the
+ * zeros per filter: exactly ceil(sparsity * n) zeros at the
+ * smallest |W_i| (stable by index), the rest sign(W_i); sparsity < 0 selects
+ * Eq. 4.  Double precision.  codes[k][n] int8 and alpha[k] are host buffers.
+ * TN_EDOMAIN on a non-finite weight (*bad_index = its flat index) or
+ * sparsity >= 1; TN_EINVAL on NULL / empty arguments.
+ * tn_fold_thresholds: per channel the conv output alpha * acc goes through
+ * batch norm y = gamma * (alpha*acc - mean) / sqrt(var + eps) + beta and Eq. 6
+ * (+1 if y > 0.5, -1 if y < -0.5, 0 else).  With
+ * a = gamma*alpha/sqrt(var+eps), b = beta - gamma*mean/sqrt(var+eps) (double,
+ * y = a*acc + b evaluated without FMA), the integer rule the epilogues apply
+ * (+1 if acc >= hi; else -1 if acc <= lo; else 0) reproduces tern(y) for every
+ * acc in [-max_abs_acc, max_abs_acc] (27 * C_in bounds |acc|).  If a < 0,
+ * negate[c] = 1 and the thresholds are for the negated filter (the caller
+ * negates that filter's codes); a == 0 gives the constant sentinels (hi =
+ * INT32_MIN: always +1; lo = hi = INT32_MAX: always -1; lo = INT32_MIN, hi =
+ * INT32_MAX: always 0).  All pointers host, k entries each.  TN_EDOMAIN on
+ * non-finite parameters or var + eps <= 0.                                    */
+tn_status tn_ternarize_weights(const float* w, int32_t k, int32_t n, float sparsity, int8_t* codes, float* alpha,
+                               int64_t* bad_index);
+tn_status tn_fold_thresholds(const float* alpha, const float* gamma, const float* beta, const float* mean,
+                             const float* var, float eps, int32_t k, int32_t max_abs_acc, int32_t* lo, int32_t* hi,
+                             int8_t* negate);
+
 /* Kernel selection for the ternary conv (all exact; parity tests run each).
  *   TN_KERNEL_POPC  CUDA-core XOR/AND/POPC form of Eq. 9 (any geometry)
  *   TN_KERNEL_TC    tcgen05 kind::i8, dx taps merged along N (stride 1, C <= 64)

@@ -257,3 +257,51 @@ def fcn_forward(x, t_lo, t_hi, weights, lo, hi, pred_w, pred_b, want_acts=False)
         np.ascontiguousarray(pred_w, dtype=np.float32), np.ascontiguousarray(pred_b, dtype=np.float32),
         logits, acts_arg)
     return logits, acts, int(bad)
+
+
+# --------------------------------------------------------------------------- model preparation (NEXT-3)
+def ternarize_weights(w, sparsity=None):
+    """Eq. 4 (PAPER.md:79-84): per output filter (axis 0), Delta = 0.7/n * sum|W_i|;
+    code +1 if W_i > Delta, 0 if |W_i| <= Delta, -1 else; alpha = mean |W_i| over the
+    nonzero codes (0 if none).  With sparsity in [0, 1):
+    exactly ceil(sparsity*n) zeros at the smallest |W_i| (stable by index), the rest
+    sign(W_i).  Plain float64 loops over filters."""
+    w = np.asarray(w, dtype=np.float32)
+    k = w.shape[0]
+    flat = w.reshape(k, -1).astype(np.float64)
+    n = flat.shape[1]
+    codes = np.zeros(flat.shape, np.int8)
+    alpha = np.zeros(k, np.float64)
+    for f in range(k):
+        row = flat[f]
+        if sparsity is None:
+            delta = 0.7 / n * float(np.sum(np.abs(row)))
+            for i in range(n):
+                v = row[i]
+                codes[f, i] = 1 if v > delta else (0 if abs(v) <= delta else -1)
+        else:
+            nz = int(np.ceil(float(np.float32(sparsity)) * n))
+            order = np.argsort(np.abs(row), kind="stable")
+            codes[f] = np.where(row > 0, 1, -1)
+            codes[f, order[:nz]] = 0
+        sel = codes[f] != 0
+        alpha[f] = float(np.sum(np.abs(row[sel]))) / int(sel.sum()) if sel.any() else 0.0
+    return codes.reshape(w.shape), alpha.astype(np.float32)
+
+
+def fold_table(alpha, gamma, beta, mean, var, eps, max_abs_acc):
+    """The definition the folded thresholds must reproduce (readings R5/R6): for every
+    channel c and every integer accumulator acc in [-A, A], the ternary output
+    tern(y) of Eq. 6 with y = a*acc + b, a = gamma*alpha/sqrt(var+eps),
+    b = beta - gamma*mean/sqrt(var+eps) in float64 (the conv output alpha*acc through
+    batch norm).  Returns int8 [K, 2A+1] (column j <-> acc = j - A)."""
+    k = len(alpha)
+    acc = np.arange(-max_abs_acc, max_abs_acc + 1, dtype=np.float64)
+    out = np.zeros((k, acc.size), np.int8)
+    for c in range(k):
+        sd = np.sqrt(np.float64(var[c]) + np.float64(np.float32(eps)))
+        a = np.float64(gamma[c]) * np.float64(alpha[c]) / sd
+        b = np.float64(beta[c]) - np.float64(gamma[c]) * np.float64(mean[c]) / sd
+        y = a * acc + b
+        out[c] = np.where(y > 0.5, 1, np.where(y < -0.5, -1, 0))
+    return out

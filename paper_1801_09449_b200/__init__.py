@@ -91,6 +91,8 @@ SIGNATURES = {
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
     "tn_get_conv_kernel": (_I32, []),
     "tn_set_grid_cap": (ctypes.c_int, [_I32]),
+    "tn_ternarize_weights": (ctypes.c_int, [_P, _I32, _I32, ctypes.c_float, _P, _P, _P]),
+    "tn_fold_thresholds": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_float, _I32, _I32, _P, _P, _P]),
     "tn_conv_kernel_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
     "tn_comm_unique_id": (ctypes.c_int, [_P]),
     "tn_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_P)]),
@@ -280,6 +282,36 @@ def tn_set_conv_kernel(which: int):
 
 def tn_get_conv_kernel() -> int:
     return int(lib.tn_get_conv_kernel())
+
+
+def tn_ternarize_weights(w, sparsity: float = -1.0):
+    """Eq. 4 (PAPER.md:79-84) per output filter of a float filter bank w [K, ...] (host numpy);
+    sparsity in [0, 1) fixes the zeros per filter instead.  Returns (codes int8
+    of w's shape, alpha float32 [K])."""
+    import numpy as np
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    k = w.shape[0]
+    n = int(w.size // k)
+    codes = np.empty(w.shape, np.int8)
+    alpha = np.empty(k, np.float32)
+    bad = ctypes.c_int64(-1)
+    st = lib.tn_ternarize_weights(w.ctypes.data_as(_P), k, n, float(sparsity), codes.ctypes.data_as(_P),
+                                  alpha.ctypes.data_as(_P), ctypes.byref(bad))
+    _check(st, "tn_ternarize_weights")
+    return codes, alpha
+
+
+def tn_fold_thresholds(alpha, gamma, beta, mean, var, eps: float, max_abs_acc: int):
+    """Fold alpha, batch norm and Eq. 6 into integer thresholds (host numpy, K each).
+    Returns (lo int32, hi int32, negate int8)."""
+    import numpy as np
+    arrs = [np.ascontiguousarray(v, dtype=np.float32) for v in (alpha, gamma, beta, mean, var)]
+    k = arrs[0].shape[0]
+    lo, hi, neg = np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k, np.int8)
+    st = lib.tn_fold_thresholds(*[a.ctypes.data_as(_P) for a in arrs], float(eps), k, int(max_abs_acc),
+                                lo.ctypes.data_as(_P), hi.ctypes.data_as(_P), neg.ctypes.data_as(_P))
+    _check(st, "tn_fold_thresholds")
+    return lo, hi, neg
 
 
 def tn_set_grid_cap(max_ctas: int):

@@ -419,3 +419,40 @@ def test_fcn_slab_nccl_single_rank(tn):
     # a non-multiple-of-8 slab is rejected before any work is queued
     with pytest.raises(tn.TNError):
         net.forward_slab(comm, xd, shape, 0, 12)
+
+
+# --------------------------------------------------------------------------- NEXT-3: a float model prepared
+def test_fcn_from_float_model_prepared_on_host(tn):
+    """A float U-Net (random float filters + batch-norm statistics) prepared with the
+    library's model-preparation calls -- Eq. 4 ternary weights (tn_ternarize_weights),
+    alpha/BN/Eq. 6 folded into integer thresholds (tn_fold_thresholds), negated filters
+    where the BN scale is negative -- then run by the FCN on the GPU: every layer's packed
+    activations equal the oracle's with the same prepared parameters."""
+    g = synth.rng(77)
+    base = synth.fcn_params()
+    weights, lo, hi = [], [], []
+    for i, wt in enumerate(base["weights"]):
+        k, c = wt.shape[:2]
+        wf = (g.standard_normal(wt.shape) * g.uniform(0.02, 0.3)).astype(np.float32)
+        codes, alpha = tn.tn_ternarize_weights(wf)
+        o_codes, o_alpha = oracle.ternarize_weights(wf)
+        np.testing.assert_array_equal(codes, o_codes)
+        A = 27 * c
+        sd_acc = np.sqrt(27 * c * 0.5 * (np.abs(codes.reshape(k, -1)) != 0).mean(1) + 1e-3)
+        gamma = (g.standard_normal(k) * 0.8 + 0.2).astype(np.float32)
+        beta = (g.standard_normal(k) * 0.3).astype(np.float32)
+        mean = (g.standard_normal(k) * 0.3 * alpha * sd_acc).astype(np.float32)
+        var = ((alpha * sd_acc) ** 2 * g.uniform(0.5, 2.0, k)).astype(np.float32)
+        l, h, neg = tn.tn_fold_thresholds(alpha, gamma, beta, mean, var, 1e-5, A)
+        tab = oracle.fold_table(alpha, gamma, beta, mean, var, 1e-5, A)
+        acc = np.arange(-A, A + 1)
+        for ch in range(k):
+            a_eff = -acc if neg[ch] else acc
+            assert np.array_equal(np.where(a_eff >= h[ch], 1, np.where(a_eff <= l[ch], -1, 0)), tab[ch])
+        codes = np.where(neg.reshape((k,) + (1,) * (codes.ndim - 1)) == 1, -codes, codes).astype(np.int8)
+        weights.append(codes)
+        lo.append(l)
+        hi.append(h)
+    p = dict(base, weights=weights, lo=lo, hi=hi)
+    x = synth.ct_volume((1, 1, 16, 24, 32), seed=78)
+    _fcn_compare(tn, x, p)
