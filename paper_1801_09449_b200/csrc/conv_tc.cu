@@ -229,7 +229,10 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
     // B rows of a padding chunk are zero, so whatever A holds there adds 0.
     {
         int lo_r = 0, hi_r = 0;
-        if (fused && threadIdx.x < K) { lo_r = __ldg(cd.lo + threadIdx.x); hi_r = __ldg(cd.hi + threadIdx.x); }
+        if (fused && threadIdx.x < K) {
+            lo_r = clamp_threshold(__ldg(cd.lo + threadIdx.x));
+            hi_r = clamp_threshold(__ldg(cd.hi + threadIdx.x));
+        }
         const uint32_t* wsrc[kMaxSeg];
         {
             uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_ring);

@@ -260,7 +260,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // into the B image, thresholds, barriers, TMEM.
     {
         int hi_r = 0, lo_r = 0;
-        if (fused && threadIdx.x < K) { hi_r = __ldg(cd.hi + threadIdx.x); lo_r = __ldg(cd.lo + threadIdx.x); }
+        if (fused && threadIdx.x < K) {
+            lo_r = clamp_threshold(__ldg(cd.lo + threadIdx.x));
+            hi_r = clamp_threshold(__ldg(cd.hi + threadIdx.x));
+        }
         const uint32_t* wsrc[kMaxSeg];
         uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_a);
         int ofs = 0;

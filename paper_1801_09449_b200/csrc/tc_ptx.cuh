@@ -76,6 +76,11 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Thresholds clamped to +-2^20: |acc| <= 27 * 64 < 2^12, so a threshold beyond that
+// acts exactly like the INT32 sentinels (always / never), while acc - hi, lo - hi
+// and their float images stay exact and cannot overflow.
+__device__ __forceinline__ int clamp_threshold(int t) { return max(-(1 << 20), min(t, 1 << 20)); }
+
 // Waits / commits on a barrier given by its shared-memory address.
 __device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
     asm volatile(

@@ -199,6 +199,26 @@ def test_conv3d_requant_matches_oracle(tn, kernel, case):
     np.testing.assert_array_equal(u32(tn.tn_requant(y, dev(lo), dev(hi))), ref)
 
 
+def test_conv3d_requant_sentinel_thresholds(tn, kernel):
+    """INT32 sentinel thresholds (always +1 / always -1 / always 0) and lo >= hi through
+    the fused epilogues of every conv kernel (no overflow in acc - hi or lo - hi)."""
+    i32 = np.iinfo(np.int32)
+    shape, k = (1, 16, 6, 10, 12), 16
+    x, w = _case(shape, k, seed=91)
+    lo = np.full(k, -3, np.int32)
+    hi = np.full(k, 3, np.int32)
+    lo[0], hi[0] = i32.min, i32.min
+    lo[1], hi[1] = i32.max, i32.max
+    lo[2], hi[2] = i32.min, i32.max
+    lo[3], hi[3] = 5, 0
+    lo[4], hi[4] = i32.max, 0
+    lo[5], hi[5] = i32.min, 1
+    ref, _ = oracle.pack(oracle.requant(oracle.conv3d(x, w), lo, hi))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, tn.tn_pack_i8(dev(x)), tn.dims(*shape),
+                     tn.tn_pack_weights(dev(w)), k, tn.geom(), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+
+
 def test_requant_sentinels_and_order(tn):
     i32 = np.iinfo(np.int32)
     y = np.arange(-40, 40, dtype=np.int32).reshape(1, 1, 1, 80, 1).repeat(40, axis=4)
