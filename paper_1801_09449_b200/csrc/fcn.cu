@@ -213,7 +213,10 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
         cd.Do = o.d; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = 0;
         cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
         cd.cwo = (ly.c_out + 31) / 32;
-        if (i == L - 1) {   // A8 fused into the last block's epilogue
+#ifndef TN_EXP_NOFUSEPRED
+#define TN_EXP_NOFUSEPRED 0
+#endif
+        if (i == L - 1 && !TN_EXP_NOFUSEPRED) {   // A8 fused into the last block's epilogue
             cd.logits = logits;
             cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
             cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
@@ -221,7 +224,7 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
         st = run_conv_scratch(cd, s, "tn_fcn_forward", reinterpret_cast<int32_t*>(base + soff));
         if (st != TN_OK) return st;
     }
-    if (net->layers[L - 1].kind == TN_LAYER_FIRST) {
+    if (net->layers[L - 1].kind == TN_LAYER_FIRST || TN_EXP_NOFUSEPRED) {
         const LayerPlan& last = P[L - 1];
         cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(base + last.off), last.out,
                                        net->pred_w, net->pred_b, net->nclass, logits, s);
