@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fcn", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-binary", action="store_true")
     return ap.parse_args()
 
 
@@ -337,6 +338,11 @@ def main():
     if not args.no_fcn:
         fcn = bench_fcn(args, tn, torch, dist, world, rank, dev, stream)
 
+    # ---- NEXT-4 binary network (Eq. 8): C1 shape with {-1,+1} codes and a sign requant
+    binary = None
+    if not args.no_binary:
+        binary = bench_binary(args, tn, torch, dist, world, rank, dev, stream, flush)
+
     # ---- configs[4]: one 256x512x512 volume, z-slabs over the ranks (NCCL halos)
     c4 = None
     if not args.no_c4:
@@ -383,11 +389,77 @@ def main():
             "pack_ms": float(np.mean(pack_ms)),
             "fcn": fcn,
             "fcn_slab": c4,
+            "binary": binary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_binary(args, tn, torch, dist, world, rank, dev, stream, flush):
+    """Binary XNOR variant (Eq. 8): C1's shape with binary
+    activations and weights (ternary codes with all-ones masks) and the sign activation
+    lo = hi - 1; the same pack + fused conv/requant step, sampled parity against the oracle."""
+    shape = (1, 64, 64, 128, 128)
+    x = synth.ternary_codes(shape, 0.0, seed=13)
+    w = synth.ternary_codes((64, 64, 3, 3, 3), 0.0, seed=14)
+    hi = (2 * synth.rng(15).integers(-1, 2, size=64)).astype(np.int32)
+    lo = hi - 1
+    x_d = torch.from_numpy(x).to(dev)
+    lo_d, hi_d = torch.from_numpy(lo).to(dev), torch.from_numpy(hi).to(dev)
+    wp = tn.tn_pack_weights(torch.from_numpy(w).to(dev))
+    xd, g = tn.dims(*shape), tn.geom(1, 1, 1)
+    xp = tn.packed_empty(*shape, device=dev)
+    yp = tn.packed_empty(*shape, device=dev)
+
+    def step():
+        tn.tn_pack_i8(x_d, xp)
+        tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+
+    step()
+    torch.cuda.synchronize()
+    parity = "skipped"
+    if rank == 0:
+        import oracle
+        gen = synth.rng(4321)
+        m = 128
+        at = np.stack([np.zeros(m, int), gen.integers(0, 64, m), gen.integers(0, 64, m),
+                       gen.integers(0, 128, m), gen.integers(0, 128, m)], 1).astype(np.int32)
+        acc = oracle.conv3d_at(x, w, at)
+        n_, k_, z_, y_, x_ = at.T
+        ref = np.where(acc >= hi[k_], 1, -1)
+        ypn = yp.cpu().numpy().view(np.uint32)
+        sb = (ypn[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
+        mb = (ypn[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
+        got = np.where(mb == 1, np.where(sb == 1, 1, -1), 0)
+        if not np.array_equal(got, ref):
+            print(json.dumps({"error": "binary parity check failed; refusing to report"}), flush=True)
+            sys.exit(1)
+        parity = f"passed ({m} sampled outputs vs oracle)"
+    for _ in range(max(3, args.warmup)):
+        step()
+    steps = max(5, min(args.steps, 20))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"metric": "binary conv3d effective GMAC/s", "unit": "GMAC/s",
+            "value": world * steps * C1_MACS / (ms / 1e3) / 1e9, "ms_per_step": ms / steps, "steps": steps,
+            "config": "C1 shape, binary {-1,+1} activations and weights (all-ones masks), sign requant "
+                      "lo = hi - 1, pack + fused conv/requant, L2 flushed between steps",
+            "parity": parity}
 
 
 def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):

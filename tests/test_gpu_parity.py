@@ -219,6 +219,29 @@ def test_conv3d_requant_sentinel_thresholds(tn, kernel):
     np.testing.assert_array_equal(u32(yp), ref)
 
 
+@pytest.mark.parametrize("case", [((1, 16, 9, 17, 34), 16, 1), ((1, 64, 6, 10, 12), 64, 1),
+                                  ((1, 32, 12, 18, 20), 32, 2), ((1, 33, 5, 6, 7), 5, 1)],
+                         ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}_s{c[2]}")
+def test_conv3d_binary_eq8(tn, kernel, case):
+    """NEXT-4 binary network (Eq. 8): {-1,+1} activations and weights are
+    ternary codes with all-ones masks, and a binary sign activation is the requant with
+    lo = hi - 1.  Every kernel runs them unchanged; outputs stay binary and match the oracle."""
+    shape, k, s = case
+    x = synth.ternary_codes(shape, 0.0, seed=shape[1] + k)
+    w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.0, seed=shape[1] + k + 1)
+    hi = synth.rng(k).integers(-3, 4, size=k).astype(np.int32)
+    lo = hi - 1
+    acc = oracle.conv3d(x, w, s)
+    t = oracle.requant(acc, lo, hi)
+    assert np.all(t != 0)
+    ref, _ = oracle.pack(t)
+    xp, wp = tn.tn_pack_i8(dev(x)), tn.tn_pack_weights(dev(w))
+    y = run_or_skip(kernel, tn.tn_conv3d, xp, tn.dims(*shape), wp, k, tn.geom(s))
+    np.testing.assert_array_equal(y.cpu().numpy(), acc.transpose(0, 2, 3, 4, 1))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, tn.dims(*shape), wp, k, tn.geom(s), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+
+
 def test_requant_sentinels_and_order(tn):
     i32 = np.iinfo(np.int32)
     y = np.arange(-40, 40, dtype=np.int32).reshape(1, 1, 1, 80, 1).repeat(40, axis=4)

@@ -366,3 +366,49 @@ def test_predict_matches_torch_float64():
     got = oracle.predict(t, w, b)
     # the double sum of 17 float32 terms is exact, so rounding once gives float32(ref)
     np.testing.assert_array_equal(got, ref.astype(np.float32))
+
+
+# --------------------------------------------------------------------------- Eq. 8 (binary XNOR)
+def test_eq8_binary_xnor_popcount():
+    """Eq. 8: for I, W in {-1,+1}^c, I.W = c - 2 popc(I xor W).  Binary
+    codes pack with all-ones masks (popc(mask) = c), and Eq. 9 then reduces to Eq. 8;
+    the oracle's dot / conv agree with the XOR count."""
+    for c in range(1, 9):
+        vecs = np.array(list(itertools.product((-1, 1), repeat=c)), dtype=np.int8)
+        xp, _ = oracle.pack(vecs.T.reshape(1, c, 1, 1, len(vecs)))
+        s, m = xp[0, 0, 0, :, 0, 0].astype(np.int64), xp[0, 0, 0, :, 1, 0].astype(np.int64)
+        assert np.all(_popc(m) == c)
+        eq8 = c - 2 * _popc(s[:, None] ^ s[None, :])
+        np.testing.assert_array_equal(eq8, vecs.astype(np.int64) @ vecs.T.astype(np.int64))
+        np.testing.assert_array_equal(eq9(s[:, None], m[:, None], s[None, :], m[None, :]), eq8)
+    for c in (27, 432, 1728):               # 3x3x3 windows of 1, 16, 64 channels
+        a = synth.ternary_codes((64, c), 0.0, seed=c)
+        b = synth.ternary_codes((64, c), 0.0, seed=c + 1)
+        assert np.all(a != 0) and np.all(b != 0)
+        dis = (a != b).sum(1)
+        np.testing.assert_array_equal((a.astype(np.int64) * b).sum(1), c - 2 * dis)
+
+
+def test_conv3d_binary_windows_eq8():
+    """Binary input and weights: every output equals n_valid - 2 * #sign disagreements over
+    its window (n_valid = 27 C inside, fewer at the zero-padded border), counted by brute
+    force; the binary requant (lo = hi - 1) keeps the activations binary."""
+    c, k = 3, 2
+    x = synth.ternary_codes((1, c, 4, 5, 6), 0.0, seed=31)
+    w = synth.ternary_codes((k, c, 3, 3, 3), 0.0, seed=32)
+    y = oracle.conv3d(x, w)
+    D, H, W = x.shape[2:]
+    for kk in range(k):
+        for z, yy, xx in itertools.product(range(D), range(H), range(W)):
+            nv = dis = 0
+            for dz, dy, dx in itertools.product(range(3), repeat=3):
+                zi, yi, xi = z + dz - 1, yy + dy - 1, xx + dx - 1
+                if 0 <= zi < D and 0 <= yi < H and 0 <= xi < W:
+                    nv += c
+                    dis += int((x[0, :, zi, yi, xi] != w[kk, :, dz, dy, dx]).sum())
+            assert y[0, kk, z, yy, xx] == nv - 2 * dis
+    assert y[0, 0, 2, 2, 2] % 2 == (27 * c) % 2         # interior parity of Eq. 8
+    hi = np.array([1, -2], np.int32)
+    t = oracle.requant(y, hi - 1, hi)
+    assert np.all(t != 0)
+    np.testing.assert_array_equal(t, np.where(y >= hi[None, :, None, None, None], 1, -1))
