@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-fcn", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-binary", action="store_true")
+    ap.add_argument("--no-slab-schedules", action="store_true")
+    ap.add_argument("--c4-halo", choices=("nccl", "p2p"), default="nccl",
+                    help="configs[4] halo exchange at N > 1: NCCL send/recv, or NEXT-1 epilogue stores + flags")
     return ap.parse_args()
 
 
@@ -512,8 +515,14 @@ def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
         nb = int(tn.lib.tn_fcn_slab_workspace_bytes(net.handle, tn.dims(*shape), z0, z1))
         ws = torch.empty(nb, dtype=torch.uint8, device=dev)
         logits = torch.empty((1, 2, z1 - z0, H, W), dtype=torch.float32, device=dev)
-        run = lambda: net.forward_slab(comm, x, shape, z0, z1, logits=logits, ws=ws)
-        mode = f"z-slabs of {D // world} planes per rank, NCCL halo exchange per layer"
+        if args.c4_halo == "p2p":
+            halo = tn.HaloP2P(net, shape, rank, world)
+            run = lambda: halo.forward(x, logits=logits)
+            mode = (f"z-slabs of {D // world} planes per rank, halos stored by the conv epilogues into the "
+                    "neighbours' memory (CUDA IPC / NVLink) + device flags (NEXT-1)")
+        else:
+            run = lambda: net.forward_slab(comm, x, shape, z0, z1, logits=logits, ws=ws)
+            mode = f"z-slabs of {D // world} planes per rank, NCCL halo exchange per layer"
     else:
         ws = net.workspace(shape, dev)
         logits = torch.empty((1, 2, D, H, W), dtype=torch.float32, device=dev)
@@ -536,7 +545,33 @@ def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     vox = D * H * W
+    sched = None
+    if world == 1 and not args.no_slab_schedules:
+        # single-GPU view of the two halo schedules: 8 slabs run layer-major on this device
+        # (the same kernels and halo traffic as 8 ranks, serialised), copies vs NEXT-1
+        del ws
+        nsl = 8
+        nb = int(tn.lib.tn_fcn_slabs_local_workspace_bytes(net.handle, tn.dims(*shape), nsl))
+        wsl = torch.empty(nb, dtype=torch.uint8, device=dev)
+        whole = logits.clone()
+        sched = {"slabs": nsl}
+        for name, fn in (("copies", net.forward_slabs_local), ("p2p_epilogue", net.forward_slabs_local_p2p)):
+            fn(x, nsl, logits=logits, ws=wsl)
+            torch.cuda.synchronize()
+            if not torch.equal(logits, whole):
+                print(json.dumps({"error": f"slab schedule {name} differs from the whole volume"}), flush=True)
+                sys.exit(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(steps):
+                fn(x, nsl, logits=logits, ws=wsl)
+            b.record(stream)
+            torch.cuda.synchronize()
+            sched[name + "_ms_per_volume"] = a.elapsed_time(b) / steps
+        sched["note"] = "bit-identical to the whole-volume logits (checked before timing)"
+        del wsl
     return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s",
+            "slab_schedules_1gpu": sched,
             "config": f"C4: one CT-like volume 1x1x{D}x{H}x{W} (BASELINE configs[4]); {mode}",
             "ms_per_volume": ms, "effective_gmacs": vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
             "steps": steps, "scaling": "strong (fixed volume)"}

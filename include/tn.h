@@ -209,6 +209,43 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
                                      float* logits, void* ws, size_t ws_bytes, int64_t* d_bad,
                                      tn_stream stream);
 
+/* ---- NEXT-1: epilogue-fused halos over NVLink P2P, no NCCL -----
+ * The same z-slab decomposition, but each layer's fused requant epilogue also
+ * stores its first / last owned output plane straight into the lower / upper
+ * neighbour's halo plane (peer memory opened with CUDA IPC, NVLink through
+ * NVSwitch), and a device progress flag replaces each send/recv pair: after
+ * layer i, one thread of a one-CTA kernel stores stamp 64*epoch + i + 2 with
+ * st.release.sys into both neighbours' flags and then waits (ld.acquire.sys)
+ * for the same stamp from both neighbours before layer i + 1 runs (stamp
+ * 64*epoch + 0 = "done with the previous forward", so halos are never
+ * overwritten while still read; + 1 = input planes delivered).  A wait that sees no progress for 60 s traps
+ * (a CUDA error on the caller's stream, never a silent hang).  Results are
+ * bit-identical to tn_fcn_forward.  Setup calls allocate; the forward does not.
+ *   tn_halo_create   plans rank's slab [z0, z1) and cudaMallocs its workspace
+ *                    + flags (tn_halo_workspace_bytes);
+ *   tn_halo_export   writes the 64-byte cudaIpcMemHandle of that workspace;
+ *   tn_halo_connect  opens the neighbours' handles (NULL at the volume ends);
+ *                    the lower neighbour owns [lower_z0, z0), the upper one
+ *                    [z1, upper_z1); all ranks must use the same net and global;
+ *   tn_fcn_forward_slab_p2p  one forward of the slab (x_slab / logits_slab as
+ *                    in tn_fcn_forward_slab), every rank once per forward;
+ *   tn_fcn_forward_slabs_local_p2p  all slabs on this device, layer-major, with
+ *                    the same epilogue stores and flags (single-GPU check of the
+ *                    schedule; workspace = tn_fcn_slabs_local_workspace_bytes). */
+typedef struct tn_halo tn_halo;
+tn_status tn_halo_create(const tn_fcn* net, tn_dims global, int32_t z0, int32_t z1, tn_halo** out);
+size_t    tn_halo_workspace_bytes(const tn_halo* h);
+tn_status tn_halo_export(const tn_halo* h, void* handle_out /*host, 64 bytes*/);
+tn_status tn_halo_connect(tn_halo* h, const tn_fcn* net, tn_dims global,
+                          const void* lower_handle /*host 64 B or NULL*/, int32_t lower_z0,
+                          const void* upper_handle /*host 64 B or NULL*/, int32_t upper_z1);
+tn_status tn_fcn_forward_slab_p2p(const tn_fcn* net, tn_halo* h, const float* x_slab, float* logits_slab,
+                                  int64_t* d_bad, tn_stream stream);
+tn_status tn_fcn_forward_slabs_local_p2p(const tn_fcn* net, const float* x, tn_dims global, int32_t nslabs,
+                                         float* logits, void* ws, size_t ws_bytes, int64_t* d_bad,
+                                         tn_stream stream);
+void      tn_halo_destroy(tn_halo* h);
+
 /* ---- Model preparation (host, not on the hot path) ---------
  * tn_ternarize_weights: Eq. 4 per output filter f of a float
  * filter bank w[k][n] (host, row-major; n = C_in * 27): Delta = 0.7/n sum|W_i|,

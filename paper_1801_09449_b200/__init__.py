@@ -103,6 +103,13 @@ SIGNATURES = {
     "tn_fcn_forward_slab": (ctypes.c_int, [_P, _P, _P, _D, _I32, _I32, _P, _P, _SZ, _P, _P]),
     "tn_fcn_slabs_local_workspace_bytes": (_SZ, [_P, _D, _I32]),
     "tn_fcn_forward_slabs_local": (ctypes.c_int, [_P, _P, _D, _I32, _P, _P, _SZ, _P, _P]),
+    "tn_halo_create": (ctypes.c_int, [_P, _D, _I32, _I32, ctypes.POINTER(_P)]),
+    "tn_halo_workspace_bytes": (_SZ, [_P]),
+    "tn_halo_export": (ctypes.c_int, [_P, _P]),
+    "tn_halo_connect": (ctypes.c_int, [_P, _P, _D, _P, _I32, _P, _I32]),
+    "tn_fcn_forward_slab_p2p": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "tn_fcn_forward_slabs_local_p2p": (ctypes.c_int, [_P, _P, _D, _I32, _P, _P, _SZ, _P, _P]),
+    "tn_halo_destroy": (None, [_P]),
 }
 
 
@@ -460,6 +467,22 @@ class TernaryFCN:
                                               ws.numel(), _ptr(d_bad), _stream(stream)), "tn_fcn_forward_slabs_local")
         return logits
 
+    def forward_slabs_local_p2p(self, x, nslabs, logits=None, ws=None, d_bad=None, stream=None):
+        """All z-slabs on this device with the NEXT-1 schedule: epilogue stores into the
+        neighbouring slabs' halo planes and device progress flags (no copies, no NCCL)."""
+        xd = dims_of(x)
+        if ws is None:
+            nb = int(lib.tn_fcn_slabs_local_workspace_bytes(self.handle, xd, int(nslabs)))
+            if nb == 0:
+                raise TNError(TN_ESHAPE, "tn_fcn_slabs_local_workspace_bytes", lib.tn_last_error().decode())
+            ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        if logits is None:
+            logits = torch.empty((xd.n, self.nclass, xd.d, xd.h, xd.w), dtype=torch.float32, device=x.device)
+        _check(lib.tn_fcn_forward_slabs_local_p2p(self.handle, _ptr(x), xd, int(nslabs), _ptr(logits), _ptr(ws),
+                                                  ws.numel(), _ptr(d_bad), _stream(stream)),
+               "tn_fcn_forward_slabs_local_p2p")
+        return logits
+
     def forward_slab(self, comm, x_slab, global_shape, z0, z1, logits=None, ws=None, d_bad=None, stream=None):
         """This rank's slab [z0, z1) of a volume decomposed over the ranks of comm (NCCL halos)."""
         gd = dims(*global_shape)
@@ -482,6 +505,49 @@ class TernaryFCN:
         nwords = od.n * od.d * od.h * od.w * 2 * cw(od.c)
         view = ws[off:off + 4 * nwords].view(torch.int32).view(od.n, od.d, od.h, od.w, 2, cw(od.c))
         return view, od
+
+
+class HaloP2P:
+    """NEXT-1: this rank's slab [z0, z1) of a volume split in z over the ranks of a
+    torch.distributed group (ranks in z order, equal slabs), with halos stored by the
+    conv epilogues straight into the neighbours' memory (CUDA IPC over NVLink) and
+    device progress flags instead of NCCL.  The IPC handles travel through the group."""
+
+    def __init__(self, net, global_shape, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        gd = dims(*global_shape)
+        D = gd.d
+        if D % world:
+            raise TNError(TN_ESHAPE, "HaloP2P", "depth must divide over the ranks")
+        dz = D // world
+        self.net, self.gd = net, gd
+        self.z0, self.z1 = rank * dz, (rank + 1) * dz
+        h = ctypes.c_void_p()
+        _check(lib.tn_halo_create(net.handle, gd, self.z0, self.z1, ctypes.byref(h)), "tn_halo_create")
+        self.handle = h
+        mine = (ctypes.c_uint8 * 64)()
+        _check(lib.tn_halo_export(h, mine), "tn_halo_export")
+        handles = [bytes(mine)]
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(mine), group=group)
+        lo = (ctypes.c_uint8 * 64)(*handles[rank - 1]) if rank > 0 else None
+        up = (ctypes.c_uint8 * 64)(*handles[rank + 1]) if rank + 1 < world else None
+        _check(lib.tn_halo_connect(h, net.handle, gd, lo, self.z0 - dz, up, self.z1 + dz), "tn_halo_connect")
+
+    def forward(self, x_slab, logits=None, d_bad=None, stream=None):
+        if logits is None:
+            logits = torch.empty((1, self.net.nclass, self.z1 - self.z0, self.gd.h, self.gd.w),
+                                 dtype=torch.float32, device=x_slab.device)
+        _check(lib.tn_fcn_forward_slab_p2p(self.net.handle, self.handle, _ptr(x_slab), _ptr(logits), _ptr(d_bad),
+                                           _stream(stream)), "tn_fcn_forward_slab_p2p")
+        return logits
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and lib is not None:
+            lib.tn_halo_destroy(h)
+            self.handle = None
 
 
 class Comm:

@@ -194,6 +194,7 @@ tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int
         !(g_conv_kernel == TN_KERNEL_AUTO && conv_tz_supported(cd, true)) && split_tc_possible(cd)) {
         ConvDesc a = cd, b = cd;
         a.nseg = 1; a.yp = nullptr; a.y = scratch; a.logits = nullptr; a.lo = a.hi = nullptr;
+        a.halo_lo = a.halo_hi = nullptr;
         tn_status s1 = cuda_status(launch_conv_tc(a, st), where);
         if (s1 != TN_OK) return s1;
         b.nseg = 1; b.seg[0] = cd.seg[1]; b.y_in = scratch;

@@ -247,6 +247,11 @@ conv_popc_kernel(const ConvDesc cd, const Tiling tl, int Kpad) {
             } else {
                 for (int q = 0; q < 2 * cd.cwo; ++q) dst[q] = src[q];
             }
+            if (cd.halo_lo != nullptr || cd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes (N = 1)
+                const int64_t hw = static_cast<int64_t>(cd.Ho) * cd.Wo;
+                const int zo = static_cast<int>((vox[i] / hw) % cd.Do);
+                halo_store_words(cd.halo_lo, cd.halo_hi, zo, cd.Do, vox[i] % hw, src, 2 * cd.cwo);
+            }
         }
     }
 }
@@ -338,6 +343,10 @@ conv_first_kernel(const FirstDesc fd, const Tiling tl) {
         }
         const int64_t v = ((static_cast<int64_t>(n) * fd.Do + zo) * fd.Ho + yo) * fd.Wo + xo;
         *reinterpret_cast<uint2*>(fd.yp + v * 2) = make_uint2(os, om);
+        if (fd.halo_lo != nullptr || fd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes (N = 1)
+            const uint32_t wds[2] = {os, om};
+            halo_store_words(fd.halo_lo, fd.halo_hi, zo, fd.Do, static_cast<int64_t>(yo) * fd.Wo + xo, wds, 2);
+        }
     }
 }
 

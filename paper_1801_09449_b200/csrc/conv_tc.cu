@@ -699,6 +699,18 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                             dst[word] = sbits;
                             dst[CWO + word] = mbits;
                         }
+                        if (cd.halo_lo != nullptr || cd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes
+                            const int64_t voff = static_cast<int64_t>(y) * cd.Wo + x;
+                            uint32_t* hl = cd.halo_lo ? cd.halo_lo + voff * 2 * CWO + (CWO == 1 ? 0 : word) : nullptr;
+                            uint32_t* hh = cd.halo_hi ? cd.halo_hi + voff * 2 * CWO + (CWO == 1 ? 0 : word) : nullptr;
+                            const uint32_t wds[2] = {sbits, mbits};
+                            if (CWO == 1) {
+                                halo_store_words(hl, hh, zo, cd.Do, 0, wds, 2);
+                            } else {   // this warp's word of each bitplane
+                                halo_store_words(hl, hh, zo, cd.Do, 0, wds, 1);
+                                halo_store_words(hl ? hl + CWO : nullptr, hh ? hh + CWO : nullptr, zo, cd.Do, 0, wds + 1, 1);
+                            }
+                        }
                     }
                 }
                 tc_fence_before();

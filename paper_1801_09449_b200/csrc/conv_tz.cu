@@ -1000,6 +1000,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         } else {
                             *reinterpret_cast<uint4*>(dst) = make_uint4(sbits[0], sbits[1], mbits[0], mbits[1]);
                         }
+                        if (cd.halo_lo != nullptr || cd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes
+                            const uint32_t wds[4] = {sbits[0], CWO == 1 ? mbits[0] : sbits[CWO - 1], mbits[0], mbits[CWO - 1]};
+                            halo_store_words(cd.halo_lo, cd.halo_hi, z, cd.Do, voff, wds, 2 * CWO);
+                        }
                     }
                     }   // tiles of the unit
                     tmem_wait_st();
@@ -1112,8 +1116,10 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         pl.reg0[i] = pl.nreg;
         pl.nreg += f4 ? std::max(1, cd.seg[i].c / 32) : 0;
     }
-    if (cd.Do != out_extent(cd.Dci, pl.s, 1, 1) || cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) ||
-        cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
+    // z-slabs: the launch covers global output planes [zo_beg, zo_beg + Do) of the layer
+    // (segment buffers start at global plane zbeg); y and x are always whole
+    if (cd.zo_beg < 0 || cd.zo_beg + cd.Do > out_extent(cd.Dci, pl.s, 1, 1) ||
+        cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) || cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
     const bool split = pl.s == 1 && cd.K == 64;
@@ -1363,6 +1369,8 @@ static ConvDesc first_desc(const FirstDesc& fd) {
     cd.d_bad = fd.d_bad;
     cd.bad_base = fd.bad_base;
     cd.bad_nstride = fd.bad_nstride;
+    cd.halo_lo = fd.halo_lo;
+    cd.halo_hi = fd.halo_hi;
     return cd;
 }
 

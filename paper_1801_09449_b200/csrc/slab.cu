@@ -103,7 +103,7 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
 // layer's halo planes (if sp.L[i].halo) before any consumer runs.
 // logits/lstride: when i is the last layer, the A8 prediction is fused into it.
 tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i, int64_t* d_bad, cudaStream_t s,
-                         float* logits, int64_t lstride) {
+                         float* logits, int64_t lstride, uint32_t* halo_lo = nullptr, uint32_t* halo_hi = nullptr) {
     {
         const tn_layer& ly = net->layers[i];
         const tn_slab_layer& o = sp.L[i];
@@ -120,6 +120,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             fd.lo = ly.lo; fd.hi = ly.hi; fd.yp = outp; fd.d_bad = d_bad;
             fd.bad_base = static_cast<int64_t>(sp.z0 - 1) * sp.g.h * sp.g.w;
             fd.bad_nstride = static_cast<int64_t>(sp.g.d) * sp.g.h * sp.g.w;
+            fd.halo_lo = halo_lo; fd.halo_hi = halo_hi;
             cudaError_t e = launch_conv_first(fd, s);
             if (e != cudaSuccess) { set_error("slab layer %d: %s", i, cudaGetErrorString(e)); return TN_ECUDA; }
         } else {
@@ -145,6 +146,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             cd.Do = o.z1 - o.z0; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = o.z0;
             cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
             cd.cwo = (ly.c_out + 31) / 32;
+            cd.halo_lo = halo_lo; cd.halo_hi = halo_hi;
             if (i + 1 == static_cast<int>(net->layers.size())) {
                 cd.logits = logits; cd.lstride = lstride;
                 cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
@@ -179,7 +181,123 @@ tn_status exchange_halo(tn_comm* c, char* buf, int64_t plane_bytes, int planes, 
     return nccl_status(ncclGroupEnd(), "halo exchange");
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-1: halos without NCCL.  Each layer's requant epilogue stores its first /
+// last owned output plane straight into the lower / upper neighbour's halo
+// plane (ConvDesc::halo_lo / halo_hi: peer memory mapped over NVLink with CUDA
+// IPC, or another slab's buffer when all slabs share one device), and a device
+// flag replaces the send/recv pair.  Every slab owns two 64-bit progress flags
+// (after its workspace): flags[0] is written by the lower neighbour, flags[1] by
+// the upper one.  A neighbour's progress in forward e is stamped e * 64 + j:
+//   j = 0       "finished forward e-1": its halo planes may be overwritten;
+//   j = 1       its boundary input planes are in my x halo;
+//   j = i + 2   layer i's boundary planes are in my halo planes of layer i.
+// Layer i reads layers < i and the input, so it runs after stamp e*64 + i + 1
+// from both neighbours: one one-thread kernel per stage publishes my stamp and
+// waits for the neighbours' (the single-device emulation splits the two).  A stamp is stored with st.release.sys after the
+// producing kernel in stream order and read with ld.acquire.sys, so the
+// producer's peer stores are visible before the consumer's next kernel runs.
+// A wait that sees no progress for 60 s traps (a loud CUDA error, never a hang).
+constexpr size_t kFlagBytes = 256;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One thread: publish stamp `sig` to the neighbours' flags (if sig != 0), then wait
+// until my own flags from the present neighbours reach `need` (if need != 0).
+__global__ void halo_sync_kernel(unsigned long long* to_lower, unsigned long long* to_upper, unsigned long long sig,
+                                 const unsigned long long* flags, int wait_lo, int wait_hi, unsigned long long need) {
+    if (threadIdx.x != 0) return;
+    if (sig != 0) {
+        __threadfence_system();
+        if (to_lower != nullptr) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_lower), "l"(sig) : "memory");
+        if (to_upper != nullptr) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_upper), "l"(sig) : "memory");
+    }
+    if (need == 0) return;
+    const unsigned long long t0 = global_ns();
+    for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? wait_lo : wait_hi)) continue;
+        while (ld_acquire_sys(flags + side) < need) {
+            __nanosleep(100);
+            if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
+        }
+    }
+}
+
+// One slab as seen by the P2P schedule: its plan, its workspace and flags.
+struct SlabView {
+    const SlabPlan* p = nullptr;
+    char* base = nullptr;
+};
+
+unsigned long long* flags_of(const SlabView& v) {
+    return v.base ? reinterpret_cast<unsigned long long*>(v.base + v.p->total) : nullptr;
+}
+
+// Signal `sig` to the present neighbours (0: none) and wait for `need` from them (0: none).
+tn_status p2p_sync(const SlabView& me, const SlabView& lower, const SlabView& upper, unsigned long long sig,
+                   unsigned long long need, cudaStream_t s) {
+    const bool hl = lower.base != nullptr, hh = upper.base != nullptr;
+    if ((!hl && !hh) || (sig == 0 && need == 0)) return TN_OK;
+    halo_sync_kernel<<<1, 32, 0, s>>>(hl ? flags_of(lower) + 1 : nullptr, hh ? flags_of(upper) + 0 : nullptr, sig,
+                                      flags_of(me), hl ? 1 : 0, hh ? 1 : 0, need);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error("halo flags: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+    return TN_OK;
+}
+
+// Phase "input": own float planes into my extended x buffer; my first plane into
+// the lower neighbour's upper x halo, my last into the upper neighbour's lower one.
+tn_status p2p_input(const SlabView& me, const SlabView& lower, const SlabView& upper, const float* x_slab,
+                    cudaStream_t s) {
+    const SlabPlan& sp = *me.p;
+    const size_t xp = sp.x_plane;
+    const int dz = sp.z1 - sp.z0;
+    const char* src = reinterpret_cast<const char*>(x_slab);
+    cudaError_t e = cudaMemcpyAsync(me.base + sp.x_off + xp, src, xp * dz, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && lower.base)
+        e = cudaMemcpyAsync(lower.base + lower.p->x_off + xp * (lower.p->z1 - lower.p->z0 + 1), src, xp,
+                            cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && upper.base)
+        e = cudaMemcpyAsync(upper.base + upper.p->x_off, src + xp * (dz - 1), xp, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) { set_error("input planes: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+    return TN_OK;
+}
+
+// Phase "layer i": the conv with its boundary planes stored into the neighbours.
+tn_status p2p_layer(const tn_fcn* net, const SlabView& me, const SlabView& lower, const SlabView& upper, int i,
+                    int64_t* d_bad, cudaStream_t s, float* logits, int64_t lstride) {
+    const tn_slab_layer& o = me.p->L[i];
+    uint32_t* hlo = nullptr;
+    uint32_t* hhi = nullptr;
+    if (o.halo && lower.base) {
+        const tn_slab_layer& lo = lower.p->L[i];
+        hlo = reinterpret_cast<uint32_t*>(lower.base + lo.offset + lo.plane_bytes * (lo.z1 - lo.z0 + 1));
+    }
+    if (o.halo && upper.base) hhi = reinterpret_cast<uint32_t*>(upper.base + upper.p->L[i].offset);
+    return run_slab_layer(net, *me.p, me.base, i, d_bad, s, logits, lstride, hlo, hhi);
+}
+
 }  // namespace
+
+// A rank's slab for the P2P path: workspace and flags allocated here (setup, not the hot
+// path) so that one IPC handle maps both; neighbours' workspaces opened from handles.
+struct tn_halo {
+    SlabPlan me;
+    char* ws = nullptr;
+    SlabPlan nb[2];
+    char* nb_ws[2] = {nullptr, nullptr};
+    unsigned long long epoch = 0;
+};
 
 extern "C" {
 
@@ -274,7 +392,7 @@ size_t tn_fcn_slabs_local_workspace_bytes(const tn_fcn* net, tn_dims global, int
     for (int r = 0; r < nslabs; ++r) {
         const size_t b = tn_fcn_slab_workspace_bytes(net, global, r * dz, (r + 1) * dz);
         if (b == 0) return 0;
-        tot += align_up(b);
+        tot += align_up(b + kFlagBytes);
     }
     return tot;
 }
@@ -295,7 +413,7 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
         tn_status st = make_slab_plan(net, global, r * dz, (r + 1) * dz, P[r]);
         if (st != TN_OK) return st;
         B[r] = p;
-        p += align_up(P[r].total);
+        p += align_up(P[r].total + kFlagBytes);
     }
     auto copy = [&](char* dst, const char* src, size_t n) -> tn_status {
         cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s);
@@ -346,6 +464,140 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
         }
     }
     return TN_OK;
+}
+
+tn_status tn_fcn_forward_slabs_local_p2p(const tn_fcn* net, const float* x, tn_dims global, int32_t nslabs,
+                                         float* logits, void* ws, size_t ws_bytes, int64_t* d_bad, tn_stream stream) {
+    if (net == nullptr || x == nullptr || logits == nullptr || ws == nullptr) { set_error("NULL argument"); return TN_EINVAL; }
+    if (nslabs < 1 || global.d % nslabs) { set_error("nslabs must divide the depth"); return TN_ESHAPE; }
+    const size_t need = tn_fcn_slabs_local_workspace_bytes(net, global, nslabs);
+    if (need == 0) return TN_ESHAPE;
+    if (ws_bytes < need) { set_error("workspace too small: need %zu", need); return TN_EINVAL; }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int dz = global.d / nslabs;
+    std::vector<SlabPlan> P(nslabs);
+    std::vector<SlabView> V(nslabs + 2);          // V[r + 1] = slab r; V[0], V[nslabs + 1] = none
+    char* p = static_cast<char*>(ws);
+    for (int r = 0; r < nslabs; ++r) {
+        tn_status st = make_slab_plan(net, global, r * dz, (r + 1) * dz, P[r]);
+        if (st != TN_OK) return st;
+        V[r + 1].p = &P[r];
+        V[r + 1].base = p;
+        p += align_up(P[r].total + kFlagBytes);
+    }
+    // stateless: the flags restart at epoch 1 every call (all slabs share this stream)
+    for (int r = 0; r < nslabs; ++r) {
+        cudaError_t e = cudaMemsetAsync(flags_of(V[r + 1]), 0, 2 * sizeof(unsigned long long), s);
+        if (e != cudaSuccess) { set_error("flag reset: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+    }
+    const unsigned long long E = 64;
+    const int nl = static_cast<int>(net->layers.size());
+    tn_status st = TN_OK;
+    // the same phases as tn_fcn_forward_slab_p2p, interleaved layer-major across the slabs
+    // (one stream: every slab signals a stage before any slab waits for it)
+    for (int r = 1; r <= nslabs && st == TN_OK; ++r) st = p2p_sync(V[r], V[r - 1], V[r + 1], E + 0, 0, s);
+    for (int r = 1; r <= nslabs && st == TN_OK; ++r) {
+        st = p2p_sync(V[r], V[r - 1], V[r + 1], 0, E + 0, s);
+        if (st == TN_OK)
+            st = p2p_input(V[r], V[r - 1], V[r + 1], x + static_cast<int64_t>(r - 1) * dz * global.h * global.w, s);
+        if (st == TN_OK) st = p2p_sync(V[r], V[r - 1], V[r + 1], E + 1, 0, s);
+    }
+    const int64_t cstride = static_cast<int64_t>(global.d) * global.h * global.w;
+    for (int i = 0; i < nl && st == TN_OK; ++i) {
+        for (int r = 1; r <= nslabs && st == TN_OK; ++r) {
+            st = p2p_sync(V[r], V[r - 1], V[r + 1], 0, E + i + 1, s);
+            float* lg = logits + static_cast<int64_t>(P[r - 1].L.back().z0) * global.h * global.w;
+            if (st == TN_OK) st = p2p_layer(net, V[r], V[r - 1], V[r + 1], i, d_bad, s, lg, cstride);
+            if (st == TN_OK && P[r - 1].L[i].halo) st = p2p_sync(V[r], V[r - 1], V[r + 1], E + i + 2, 0, s);
+        }
+    }
+    return st;
+}
+
+tn_status tn_halo_create(const tn_fcn* net, tn_dims global, int32_t z0, int32_t z1, tn_halo** out) {
+    if (net == nullptr || out == nullptr) { set_error("net/out is NULL"); return TN_EINVAL; }
+    *out = nullptr;
+    tn_halo* h = new (std::nothrow) tn_halo();
+    if (h == nullptr) { set_error("out of host memory"); return TN_EINVAL; }
+    tn_status st = make_slab_plan(net, global, z0, z1, h->me);
+    if (st != TN_OK) { delete h; return st; }
+    cudaError_t e = cudaMalloc(&h->ws, h->me.total + kFlagBytes);
+    if (e == cudaSuccess) e = cudaMemset(h->ws + h->me.total, 0, kFlagBytes);
+    if (e != cudaSuccess) {
+        set_error("halo workspace: %s", cudaGetErrorString(e));
+        if (h->ws) cudaFree(h->ws);
+        delete h;
+        return TN_ECUDA;
+    }
+    *out = h;
+    return TN_OK;
+}
+
+tn_status tn_halo_export(const tn_halo* h, void* handle_out) {
+    if (h == nullptr || handle_out == nullptr) { set_error("halo/handle is NULL"); return TN_EINVAL; }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaIpcMemHandle_t m;
+    cudaError_t e = cudaIpcGetMemHandle(&m, h->ws);
+    if (e != cudaSuccess) { set_error("cudaIpcGetMemHandle: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+    memcpy(handle_out, &m, sizeof(m));
+    return TN_OK;
+}
+
+tn_status tn_halo_connect(tn_halo* h, const tn_fcn* net, tn_dims global, const void* lower_handle, int32_t lower_z0,
+                          const void* upper_handle, int32_t upper_z1) {
+    if (h == nullptr || net == nullptr) { set_error("halo/net is NULL"); return TN_EINVAL; }
+    if (h->nb_ws[0] || h->nb_ws[1]) { set_error("already connected"); return TN_EINVAL; }
+    const void* hd[2] = {lower_handle, upper_handle};
+    const int zr[2][2] = {{lower_z0, h->me.z0}, {h->me.z1, upper_z1}};
+    for (int side = 0; side < 2; ++side) {
+        if (hd[side] == nullptr) continue;
+        tn_status st = make_slab_plan(net, global, zr[side][0], zr[side][1], h->nb[side]);
+        if (st != TN_OK) return st;
+        cudaIpcMemHandle_t m;
+        memcpy(&m, hd[side], sizeof(m));
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, m, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) { set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+        h->nb_ws[side] = static_cast<char*>(ptr);
+    }
+    return TN_OK;
+}
+
+size_t tn_halo_workspace_bytes(const tn_halo* h) { return h ? h->me.total + kFlagBytes : 0; }
+
+tn_status tn_fcn_forward_slab_p2p(const tn_fcn* net, tn_halo* h, const float* x_slab, float* logits_slab,
+                                  int64_t* d_bad, tn_stream stream) {
+    if (net == nullptr || h == nullptr) { set_error("net/halo is NULL"); return TN_EINVAL; }
+    if (x_slab == nullptr || logits_slab == nullptr) { set_error("x/logits NULL"); return TN_EINVAL; }
+    if ((reinterpret_cast<uintptr_t>(x_slab) | reinterpret_cast<uintptr_t>(logits_slab)) & 15u) {
+        set_error("pointers must be 16-byte aligned");
+        return TN_EALIGN;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    SlabView me, lo, up;
+    me.p = &h->me; me.base = h->ws;
+    if (h->nb_ws[0]) { lo.p = &h->nb[0]; lo.base = h->nb_ws[0]; }
+    if (h->nb_ws[1]) { up.p = &h->nb[1]; up.base = h->nb_ws[1]; }
+    const unsigned long long E = 64ull * ++h->epoch;
+    // one flag kernel per stage: publish my progress, then wait for the neighbours' same stage
+    tn_status st = p2p_sync(me, lo, up, E + 0, E + 0, s);
+    if (st == TN_OK) st = p2p_input(me, lo, up, x_slab, s);
+    if (st == TN_OK) st = p2p_sync(me, lo, up, E + 1, E + 1, s);
+    const int64_t lstride = static_cast<int64_t>(h->me.z1 - h->me.z0) * h->me.g.h * h->me.g.w;
+    const int nl = static_cast<int>(net->layers.size());
+    for (int i = 0; i < nl && st == TN_OK; ++i) {
+        st = p2p_layer(net, me, lo, up, i, d_bad, s, logits_slab, lstride);
+        if (st == TN_OK && h->me.L[i].halo) st = p2p_sync(me, lo, up, E + i + 2, E + i + 2, s);
+    }
+    return st;
+}
+
+void tn_halo_destroy(tn_halo* h) {
+    if (h == nullptr) return;
+    for (int side = 0; side < 2; ++side)
+        if (h->nb_ws[side]) cudaIpcCloseMemHandle(h->nb_ws[side]);
+    if (h->ws) cudaFree(h->ws);
+    delete h;
 }
 
 }  // extern "C"

@@ -60,6 +60,11 @@ struct ConvDesc {
     float t_lo, t_hi;
     int64_t* d_bad;
     int64_t bad_base, bad_nstride;
+    // NEXT-1 (z-slabs, N = 1): when set, the requant epilogue also stores output plane 0
+    // into halo_lo and plane Do-1 into halo_hi ([Ho][Wo][2][cwo] each) -- the neighbouring
+    // slabs' halo planes, in peer memory over NVLink (or another slab's buffer on one device).
+    uint32_t* halo_lo;
+    uint32_t* halo_hi;
 };
 
 struct FirstDesc {
@@ -76,7 +81,19 @@ struct FirstDesc {
     int64_t* d_bad;
     int64_t bad_base;             // flat index of buffer element 0 in the global tensor
     int64_t bad_nstride;          // global per-n stride (D_g*H*W)
+    uint32_t* halo_lo;            // NEXT-1 boundary-plane stores (see ConvDesc)
+    uint32_t* halo_hi;
 };
+
+// NEXT-1: store one voxel's packed words ([2][cwo]) to the neighbours' halo planes
+// when its output plane is a slab boundary.  voff = (y * Wo + x) within the plane.
+__device__ __forceinline__ void halo_store_words(uint32_t* halo_lo, uint32_t* halo_hi, int zo, int Do,
+                                                 int64_t voff, const uint32_t* words, int nw) {
+    if (zo == 0 && halo_lo != nullptr)
+        for (int q = 0; q < nw; ++q) halo_lo[voff * nw + q] = words[q];
+    if (zo == Do - 1 && halo_hi != nullptr)
+        for (int q = 0; q < nw; ++q) halo_hi[voff * nw + q] = words[q];
+}
 
 // Kernel launchers (return cudaGetLastError()).
 cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d_bad, cudaStream_t s);

@@ -133,3 +133,36 @@ def test_kernel_selection_host_logic(tn):
         tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
     assert tn.lib.tn_set_grid_cap(-1) == tn.TN_EINVAL
     assert tn.lib.tn_set_grid_cap(0) == tn.TN_OK
+
+
+def test_halo_p2p_host_validation(tn):
+    """NEXT-1 setup calls validate before any allocation (no GPU needed)."""
+    net = _dummy_fcn(tn)
+    h = ctypes.c_void_p()
+    # a slab that is not a multiple of the FCN's total downsampling (8)
+    assert tn.lib.tn_halo_create(net, tn.dims(1, 1, 32, 16, 16), 0, 12, ctypes.byref(h)) == tn.TN_ESHAPE
+    assert tn.lib.tn_halo_create(None, tn.dims(1, 1, 32, 16, 16), 0, 8, ctypes.byref(h)) == tn.TN_EINVAL
+    assert tn.lib.tn_halo_export(None, None) == tn.TN_EINVAL
+    assert tn.lib.tn_fcn_forward_slab_p2p(net, None, None, None, None, None) == tn.TN_EINVAL
+    assert tn.lib.tn_halo_workspace_bytes(None) == 0
+    tn.lib.tn_halo_destroy(None)
+    # the single-device NEXT-1 schedule shares the emulation's workspace (+ 256 B of flags per slab)
+    gd = tn.dims(1, 1, 32, 16, 16)
+    per = sum(tn.lib.tn_fcn_slab_workspace_bytes(net, gd, 8 * r, 8 * r + 8) for r in range(4))
+    assert tn.lib.tn_fcn_slabs_local_workspace_bytes(net, gd, 4) >= per + 4 * 256
+    tn.lib.tn_fcn_destroy(net)
+
+
+def _dummy_fcn(tn):
+    table = tn.fcn_table()
+    layers = (tn.tn_layer * len(table))()
+    for i, (kind, co, s, segs) in enumerate(table):
+        L = layers[i]
+        L.kind, L.c_out, L.stride, L.dil, L.nseg = kind, co, s, 1, len(segs)
+        for j, (src, up) in enumerate(segs):
+            L.src[j], L.upsample[j], L.wp[j] = src, up, 0x1000
+        L.lo = L.hi = 0x1000
+    h = ctypes.c_void_p()
+    P = ctypes.c_void_p(0x1000)
+    assert tn.lib.tn_fcn_create(layers, len(table), -200.0, 200.0, P, P, 2, ctypes.byref(h)) == tn.TN_OK
+    return h

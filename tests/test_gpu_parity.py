@@ -464,6 +464,47 @@ def test_fcn_slab_nccl_single_rank(tn):
         net.forward_slab(comm, xd, shape, 0, 12)
 
 
+# --------------------------------------------------------------------------- NEXT-1: epilogue-fused halos
+@pytest.mark.parametrize("shape,nslabs", [((1, 1, 32, 48, 48), 2), ((1, 1, 64, 24, 40), 8),
+                                          ((1, 1, 16, 40, 56), 2)])
+def test_fcn_slabs_local_p2p_bit_identical(tn, fcn_kernel, shape, nslabs):
+    """NEXT-1 schedule on one device: every conv epilogue (TZ, TC, popc, first layer) stores
+    its boundary planes straight into the neighbouring slabs' halo planes and progress
+    flags replace the copies; == the whole-volume forward bit for bit, also when the same
+    workspace is reused (flags restart per call)."""
+    if fcn_kernel == "tc":
+        pytest.skip("the dx-merged TC kernel plans whole volumes only (Do = out_extent(Dci)); "
+                    "slab convs run on TZ / popc")
+    x = synth.ct_volume(shape, seed=13)
+    p = synth.fcn_params()
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    xd = dev(x)
+    whole = net(xd).cpu().numpy()
+    nb = int(tn.lib.tn_fcn_slabs_local_workspace_bytes(net.handle, tn.dims(*shape), nslabs))
+    ws = torch.full((nb,), 0x5A, dtype=torch.uint8, device="cuda")   # garbage halos must be overwritten
+    flag = tn.bad_flag()
+    for _ in range(2):
+        got = net.forward_slabs_local_p2p(xd, nslabs, ws=ws, d_bad=flag).cpu().numpy()
+        np.testing.assert_array_equal(got, whole)
+    assert bad_value(flag) == tn.INT64_MAX
+
+
+def test_fcn_halo_p2p_single_rank(tn):
+    """The rank-side NEXT-1 entry points (tn_halo_create / export / connect /
+    tn_fcn_forward_slab_p2p) with no neighbours: repeated forwards advance the epoch."""
+    shape = (1, 1, 16, 32, 32)
+    x = synth.ct_volume(shape, seed=14)
+    p = synth.fcn_params()
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    xd = dev(x)
+    whole = net(xd).cpu().numpy()
+    h = tn.HaloP2P(net, shape, 0, 1)
+    assert int(tn.lib.tn_halo_workspace_bytes(h.handle)) > 0
+    for _ in range(3):
+        np.testing.assert_array_equal(h.forward(xd).cpu().numpy(), whole)
+    del h
+
+
 # --------------------------------------------------------------------------- NEXT-3: a float model prepared
 def test_fcn_from_float_model_prepared_on_host(tn):
     """A float U-Net (random float filters + batch-norm statistics) prepared with the
