@@ -246,26 +246,40 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed between steps outside the events
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # (no event between pack and conv here: the conv is launched with programmatic
+    # dependent launch and its prologue overlaps the pack's tail)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.zero_()
-            a, b, c = ev[i]
+            a, c = ev[i]
             a.record(stream)
             tn.tn_pack_i8(x_d, xp)
-            b.record(stream)
             tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
             c.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(c) for a, _, c in ev]
-    conv_ms = [b.elapsed_time(c) for _, b, c in ev]
-    pack_ms = [a.elapsed_time(b) for a, b, _ in ev]
+    step_ms = [a.elapsed_time(c) for a, c in ev]
+    # kernel timing pass for the roofline: the same steps with an event between pack and
+    # conv (the conv's own launch duration on its stream; this serialises the two)
+    ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        a, b, c = ev3[i]
+        a.record(stream)
+        tn.tn_pack_i8(x_d, xp)
+        b.record(stream)
+        tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+        c.record(stream)
+    torch.cuda.synchronize()
+    conv_ms = [b.elapsed_time(c) for _, b, c in ev3]
+    pack_ms = [a.elapsed_time(b) for a, b, _ in ev3]
+    split_step_ms = [a.elapsed_time(c) for a, _, c in ev3]
     tot_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)
@@ -334,7 +348,9 @@ def main():
                                   " (assumed POPC rate)")}
     roof["kernel"] = "tn_conv3d_requant"
     roof["avg_ms"] = conv_avg_s * 1e3
-    roof["share_of_step"] = float(np.sum(conv_ms) / np.sum(step_ms))
+    roof["share_of_step"] = float(np.sum(conv_ms) / np.sum(split_step_ms))
+    roof["timing"] = "conv launch duration from a second pass of the same steps with an event between pack and conv"
+
 
     # ---- FCN voxels/s: configs[3], 8 volumes sharded across ranks
     fcn = None

@@ -31,6 +31,13 @@
  *  - Requantisation (reading R5): t = +1 if acc >= hi[k]; else -1 if
  *    acc <= lo[k]; else 0.
  *  - 16-byte alignment is required for every tensor pointer (128-bit I/O).
+ *  - Programmatic dependent launch: the tensor-core convs start their prologue
+ *    (filter bank, thresholds, prediction weights) while the previous kernel on
+ *    the stream is still finishing, and wait for it (griddepcontrol.wait) only
+ *    before reading activations.  So filter banks, thresholds and prediction
+ *    weights must not be written by the kernel launched IMMEDIATELY before a conv
+ *    (a copy, or any earlier kernel, is fine).  tn_pack_weights ends with an
+ *    empty kernel so that packing and then convolving right away is safe.
  *
  * Errors: host-detectable errors return before any work is queued, with text in
  * tn_last_error().  Device-detected domain errors (a code outside {-1,0,1}, a

@@ -278,6 +278,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             ofs += 4 * n4;
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+#if TN_EXP_PROF
+        if (threadIdx.x == 0) g_tztrace[16 * blockIdx.x + 15] = clock64() - k_begin;
+#endif
         if (threadIdx.x < K) {
             if (F4) {   // f32 accumulators: the same integers as floats (exact, +0.0 for 0)
                 s_nhi[threadIdx.x] = __float_as_int(fused ? static_cast<float>(-hi_r) : 0.0f);

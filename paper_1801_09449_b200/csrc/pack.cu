@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include <climits>
+#include <cstdlib>
 
 namespace tn {
 namespace {
@@ -237,12 +238,15 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
 // C1: 24 us for 64 MiB in + 16 MiB out (3.5 TB/s) against 31 us for the
 // register-only 4-voxel variant below.
 constexpr int kPackTile = 512;
-template <int CW>
+template <int CW, int kPackTile, bool CHECK>
 __global__ void __launch_bounds__(256)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
     extern __shared__ __align__(128) uint8_t sx[];          // [2][C][kPackTile]
     __shared__ __align__(8) uint64_t bar[2];
+    // let a PDL-launched consumer (the conv) start its prologue as SMs free up; it still
+    // waits (griddepcontrol.wait) for this whole grid before reading the packed tensor
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int tile_bytes = C * kPackTile;
     auto issue = [&](int64_t tile, int b) {
         const int64_t t0 = tile * kPackTile;
@@ -297,25 +301,27 @@ pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t nt
             uint32_t accS[4], accM[4];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-                uint32_t as = 0u, am = 0u;
+                // bit jj of each byte: lsb (nonzero) and bit 7 (negative) of channel 8g + jj;
+                // the fields are disjoint, so sign = mask & ~negative at the end
+                uint32_t an = 0u, am = 0u;
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     const int c = 32 * j + 8 * g + jj;
                     const uint32_t w = c < C ? reinterpret_cast<const uint32_t*>(st + c * kPackTile)[i4] : 0u;
-                    const uint32_t lsb = w & 0x01010101u;
-                    const uint32_t t7 = (w >> 7) & 0x01010101u;
-                    const uint32_t pos = lsb & ~t7;
-                    bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
-                    am += lsb << jj;
-                    as += pos << jj;
+                    if (CHECK) {
+                        const uint32_t lsb = w & 0x01010101u, t7 = (w >> 7) & 0x01010101u;
+                        bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
+                    }
+                    am |= (w << jj) & (0x01010101u << jj);
+                    an |= (w >> (7 - jj)) & (0x01010101u << jj);
                 }
-                accS[g] = as;
+                accS[g] = am & ~an;
                 accM[g] = am;
             }
             transpose4x4(accS[0], accS[1], accS[2], accS[3], os[0][j], os[1][j], os[2][j], os[3][j]);
             transpose4x4(accM[0], accM[1], accM[2], accM[3], om[0][j], om[1][j], om[2][j], om[3][j]);
         }
-        if (bad != 0u) {
+        if (CHECK && bad != 0u) {
             const int64_t n = t0 / DHW, v0 = t0 - n * DHW;
             int64_t first = LLONG_MAX;
             for (int c = 0; c < C; ++c)
@@ -501,18 +507,52 @@ cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
         }
+        static int tile = 0;
         if (!configured) {
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            const char* e = getenv("TN_PACK_TILE");
+            tile = e ? atoi(e) : 256;
             configured = true;
         }
-        // one tile per CTA, one buffer (measured: 3 co-resident 64 KB CTAs per SM hide the
-        // load latency better than a persistent double-buffered CTA: 26.6 vs 33.6 us on C1)
-        const int64_t ntiles = total / kPackTile;
-        const size_t smem = static_cast<size_t>(xd.c) * kPackTile;
-        const unsigned blocks = static_cast<unsigned>(ntiles);
-        if (cw == 1) pack_i8_bulk_kernel<1><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
-        else pack_i8_bulk_kernel<2><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
+        const int64_t ntiles = total / tile;
+        static int per_sm = -1;
+        if (per_sm < 0) { const char* e = getenv("TN_PACK_PERSIST"); per_sm = e ? atoi(e) : 0; }
+        size_t smem = static_cast<size_t>(xd.c) * tile;
+        unsigned blocks = static_cast<unsigned>(ntiles);
+        if (per_sm > 0 && ntiles > static_cast<int64_t>(per_sm) * num_sms) {
+            blocks = static_cast<unsigned>(per_sm * num_sms);   // persistent, double-buffered
+            smem *= 2;
+        }
+#define TN_PT(PTV)                                                                                           \
+        if (tile == PTV) {                                                                                  \
+            if (d_bad != nullptr) {                                                                          \
+                if (cw == 1) pack_i8_bulk_kernel<1, PTV, true><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad); \
+                else pack_i8_bulk_kernel<2, PTV, true><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);         \
+            } else {                                                                                        \
+                if (cw == 1) pack_i8_bulk_kernel<1, PTV, false><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad); \
+                else pack_i8_bulk_kernel<2, PTV, false><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);         \
+            }                                                                                               \
+        }
+        TN_PT(512)
+        TN_PT(256)
+        TN_PT(128)
+        TN_PT(1024)
+#undef TN_PT
         return cudaGetLastError();
     }
     if (total > 0 && DHW % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
@@ -534,11 +574,18 @@ cudaError_t launch_pack_f32(const float* x, tn_dims xd, float t_lo, float t_hi, 
     return pack_dispatch<float>(x, xd, Classify<float>{t_lo, t_hi}, xp, d_bad, s);
 }
 
+__global__ void stream_fence_kernel() {}
+
 cudaError_t launch_pack_weights(const int8_t* w, int k, int c, uint32_t* wp, int64_t* d_bad,
                                 cudaStream_t s) {
     const int cw = (c + 31) / 32;
     const int nt = k * 27 * cw;
     pack_weights_kernel<<<(nt + 127) / 128, 128, 0, s>>>(w, k, c, cw, wp, d_bad);
+    // The conv kernels stage their filter bank before griddepcontrol.wait (programmatic
+    // dependent launch), so the packed weights must not come from the kernel launched
+    // immediately before a conv: an empty kernel after the packing keeps that true even
+    // when the caller convolves right away.
+    stream_fence_kernel<<<1, 32, 0, s>>>();
     return cudaGetLastError();
 }
 

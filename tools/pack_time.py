@@ -6,6 +6,8 @@ import numpy as np, torch
 import synth
 import paper_1801_09449_b200 as tn
 x, w, lo, hi = synth.conv_config("C1")
+if len(sys.argv) > 1:   # optional shape override: N C D H W
+    x = synth.ternary_codes(tuple(map(int, sys.argv[1:6])), 0.5, seed=10)
 xd = torch.from_numpy(x).cuda()
 xp = tn.tn_pack_i8(xd)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -25,4 +27,5 @@ def run(g):
     return e0.elapsed_time(e1) * 1e3 / 10
 ga, gb = graph(True), graph(False)
 us = run(ga) - run(gb)
-print(f"pack C1: {us:.1f} us  {(64 + 16) * 2**20 / us / 1e3:.0f} GB/s (flush-subtracted)")
+nb = x.size + x.size // x.shape[1] * 8 * ((x.shape[1] + 31) // 32)
+print(f"pack {x.shape}: {us:.1f} us  {nb / us / 1e3:.0f} GB/s (flush-subtracted)")

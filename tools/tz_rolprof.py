@@ -42,7 +42,7 @@ os.makedirs("gpurun_out", exist_ok=True)
 np.save(f"gpurun_out/tzprof_{mode}_{'_'.join(map(str, args))}.npy", A)
 m = A.mean(0)
 gs, ge = A[:, 13], A[:, 14]
-print(f"  kernel cycles mean {m[12]:.0f} max {A[:,12].max():.0f}; setup mean {m[11]:.0f}; "
+print(f"  kernel cycles mean {m[12]:.0f} max {A[:,12].max():.0f}; setup mean {m[11]:.0f} (weights staged at {m[15]:.0f}); "
       f"globaltimer span {(ge.max() - gs.min()) / 1e3:.1f} us, CTA start spread {(gs.max() - gs.min()) / 1e3:.1f} us, "
       f"end spread {(ge.max() - ge.min()) / 1e3:.1f} us")
 print(f"{mode} {args}: planes/CTA {m[5]:.1f}")
