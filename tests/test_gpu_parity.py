@@ -354,6 +354,43 @@ def test_fcn_c2_full_size_matches_oracle(tn):
     _fcn_compare(tn, x, synth.fcn_params(cfg["seed_params"]))
 
 
+# Backward dependency interval of one output voxel of the R9 FCN (1-D, by axis): it reads
+# inputs from 37..44 voxels below to 30..37 above, depending on its position mod 8.
+_FCN_DEP_BELOW, _FCN_DEP_ABOVE = 44, 37
+
+
+@pytest.mark.parametrize("cfg_name,origin", [("C4", (64, 192, 320)), ("C4", (0, 0, 384)), ("C3", (0, 64, 128))])
+def test_fcn_full_size_cropped_oracle(tn, cfg_name, origin):
+    """configs[4] (1x1x256x512x512) and configs[3] (128x256x256) at full size on the GPU against
+    the oracle on a 128^3 crop aligned to the FCN's /8 grid.  Outputs at least 44 voxels above
+    the crop's lower faces and 37 below its upper faces depend only on inputs inside the crop
+    (the R9 dependency interval), so they must equal the whole-volume logits (R13 tolerance);
+    faces on the volume boundary pad with zeros in both, so the corner crop checks padding at
+    full size too.  For C4 the 8-slab NEXT-1 schedule must reproduce the whole volume exactly."""
+    cfg = synth.CONFIGS[cfg_name]
+    shape = cfg["vol_shape"]
+    p = synth.fcn_params(cfg["seed_params"])
+    x = synth.ct_volume(shape, seed=cfg["seeds"][0])
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    xd = dev(x)
+    got = net(xd)
+    n = 128
+    sl = tuple(slice(o, o + n) for o in origin)
+    ref, _, _ = oracle.fcn_forward(np.ascontiguousarray(x[(slice(None), slice(None)) + sl]), p["t_lo"], p["t_hi"],
+                                   p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"])
+    # comparable region per axis: the margin is only needed on faces inside the volume
+    lo_ = [0 if o == 0 else _FCN_DEP_BELOW for o in origin]
+    hi_ = [n if o + n == ext else n - _FCN_DEP_ABOVE for o, ext in zip(origin, shape[2:])]
+    r = ref[:, :, lo_[0]:hi_[0], lo_[1]:hi_[1], lo_[2]:hi_[2]]
+    g = got[:, :, origin[0] + lo_[0]:origin[0] + hi_[0], origin[1] + lo_[1]:origin[1] + hi_[1],
+            origin[2] + lo_[2]:origin[2] + hi_[2]].cpu().numpy()
+    assert r.size >= 2 * 40 ** 3
+    tol = np.maximum(np.abs(r), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(g - r) <= tol)
+    if cfg_name == "C4":
+        np.testing.assert_array_equal(net.forward_slabs_local_p2p(xd, 8).cpu().numpy(), got.cpu().numpy())
+
+
 # --------------------------------------------------------------------------- C1 at full size
 def test_c1_full_size_sampled(tn):
     """configs[1] (1x64x64x128x128, K=64, fused requant) in the bench's launch
