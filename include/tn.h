@@ -174,7 +174,9 @@ void      tn_fcn_destroy(tn_fcn* net);
 
 /* Internal-activation access for debugging and per-layer parity: after a
  * tn_fcn_forward on the same ws, returns the device pointer and dims of layer
- * i's packed output inside ws (NULL if out of range).                        */
+ * i's packed output inside ws (NULL if out of range).  The LAST layer's codes
+ * are only written when the prediction is not fused into its epilogue (the
+ * CUDA-core fallback); the tensor-core kernels produce its logits only.       */
 const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* ws, int32_t i,
                                     tn_dims* out_dims /*host*/);
 

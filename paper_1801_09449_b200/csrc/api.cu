@@ -240,6 +240,7 @@ tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
         if (kf == TN_KERNEL_TZ || kf == TN_KERNEL_TC) return cuda_status(launch_kernel(kf, cd, st), where);
         ConvDesc c2 = cd;
         c2.logits = nullptr;
+        c2.no_yp = 0;   // the predict kernel reads the packed output
         tn_status s2 = run_conv(c2, st, where);
         if (s2 != TN_OK) return s2;
         const tn_dims td{cd.N, cd.K, cd.Do, cd.Ho, cd.Wo};

@@ -691,7 +691,7 @@ conv_tc_kernel(const ConvDesc cd, const TcPlan pl) {
                             cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = acc;
                         }
                     }
-                    if (fused && vpos) {
+                    if (fused && vpos && !(cd.logits != nullptr && cd.no_yp)) {
                         uint32_t* dst = cd.yp + vox * 2 * CWO;
                         if constexpr (CWO == 1) {
                             *reinterpret_cast<uint2*>(dst) = make_uint2(sbits, mbits);

@@ -45,6 +45,8 @@
 //   warp 18     loader: one elected lane issues 1-D bulk copies (cp.async.bulk)
 //               of the contiguous packed rows a strip needs, per plane and segment
 #include "tn_internal.cuh"
+
+#include <cstdlib>
 #include "tc_ptx.cuh"
 
 #include <algorithm>
@@ -997,6 +999,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 }
                             }
                         }
+                        if (PRED && cd.no_yp) continue;   // last FCN layer: only the logits are consumed
                         uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
                         if constexpr (CWO == 1) {
                             *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
@@ -1222,6 +1225,11 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     // smaller strips when the layer would otherwise give fewer units than SMs (the
     // R3 layers: 16 planes of 9 tiles), so every SM gets work
     int tstart = std::min(tmax, pl.NT);
+    {
+        static int env_tmax = -1;   // experiment knob: TN_TZ_TMAX caps the strip width
+        if (env_tmax < 0) { const char* e = getenv("TN_TZ_TMAX"); env_tmax = e ? atoi(e) : 0; }
+        if (env_tmax > 0) tstart = std::min(tstart, env_tmax);
+    }
     {
         const int nsm = tz_num_sms();
         while (tstart > 1 && static_cast<int64_t>(cd.N) * ((pl.NT + tstart - 1) / tstart) * cd.Do < nsm) --tstart;

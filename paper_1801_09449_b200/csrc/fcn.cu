@@ -220,6 +220,7 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
             cd.logits = logits;
             cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
             cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
+            cd.no_yp = 1;   // fused prediction: the last layer's packed codes are not stored
         }
         st = run_conv_scratch(cd, s, "tn_fcn_forward", reinterpret_cast<int32_t*>(base + soff));
         if (st != TN_OK) return st;

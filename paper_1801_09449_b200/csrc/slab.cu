@@ -150,6 +150,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             if (i + 1 == static_cast<int>(net->layers.size())) {
                 cd.logits = logits; cd.lstride = lstride;
                 cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
+                cd.no_yp = 1;
             }
             tn_status st = run_conv_scratch(cd, s, "slab conv", reinterpret_cast<int32_t*>(ws + sp.scratch_off));
             if (st != TN_OK) return st;

@@ -53,6 +53,7 @@ struct ConvDesc {
     const float* pw;
     const float* pb;
     int nclass;
+    int no_yp;                    // with fused logits: skip the packed output (only the logits are used)
     // First layer (A7) on the tensor-core TZ kernel: seg[0] describes the float
     // input (c = 1, xp unused); Eq. 6 band (t_lo, t_hi); non-finite inputs are
     // reported through d_bad (flat index n * bad_nstride + bad_base + (zb*H+y)*W+x).
