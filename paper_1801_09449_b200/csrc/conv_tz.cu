@@ -88,7 +88,41 @@ __device__ long long g_tztrace[148 * 16];
 #define TZ_EXP_NOACCWAIT 0
 #endif
 #ifndef TZ_WAIT
+#ifndef TZ_DEBUG_WAIT
+#define TZ_DEBUG_WAIT 0
+#endif
+#if TZ_DEBUG_WAIT
+// debug build: a wait that sees no progress for 2 s records (block, thread, line, parity,
+// barrier offset) into pinned host memory (readable while the kernel hangs) and keeps waiting
+__device__ unsigned int* g_tz_dbg = nullptr;
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int line) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    bool reported = false;
+    while (true) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+        if (ok) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!reported && t - t0 > 2000000000ull && g_tz_dbg != nullptr) {
+            reported = true;
+            const unsigned slot = atomicAdd(g_tz_dbg, 1u);
+            if (slot < 4000) {
+                volatile unsigned int* r = g_tz_dbg + 16 + 8 * slot;
+                r[0] = blockIdx.x; r[1] = threadIdx.x; r[2] = line; r[3] = parity; r[4] = a;
+                __threadfence_system();
+            }
+        }
+    }
+}
+#define TZ_WAIT(b, p) mbar_wait_dbg(b, p, __LINE__)
+extern "C" int tn_exp_set_tz_dbg(void* p) { return static_cast<int>(cudaMemcpyToSymbol(g_tz_dbg, &p, sizeof(p))); }
+#else
 #define TZ_WAIT mbar_wait
+#endif
 #endif
 
 namespace tn {
@@ -804,7 +838,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         const uint32_t cbar = smem_u32(acc_full + done_bar[0] + v0);
                         constexpr uint32_t kBarStep = 8 * kZMmaWarps;
                         int k = 0;
-                        for (int v = v0; v * TZ_TU < Tv; v += kZMmaWarps, ++k) {
+                        for (int v = v0; v < NU; v += kZMmaWarps, ++k) {   // (units past Tv: empty commit)
                             if (!TZ_EXP_NOACCWAIT) mbar_wait_addr(wbar + k * kBarStep, wpar);
                             tc_fence_after();
                             const int t1 = min((v + 1) * TZ_TU, Tv);
@@ -818,7 +852,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             tc_commit_addr(cbar + k * kBarStep);
                         }
                     } else
-                    for (int v = warp - kZMmaWarp; v * TZ_TU < Tv; v += kZMmaWarps) {
+                    // every synchronisation unit of the strip takes part, also those past the
+                    // last tile of a ragged strip (no MMAs, an empty commit): the per-unit
+                    // barriers then advance one phase per output plane in every strip, which the
+                    // parities assume when a CTA's range continues into a full strip (n > 1)
+                    for (int v = warp - kZMmaWarp; v < NU; v += kZMmaWarps) {
                         ZSTAMP(y1);
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
@@ -901,7 +939,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
-                for (int v = g; v * TZ_TU < Tv; v += kZEpiGroups) {
+                for (int v = g; v < NU; v += kZEpiGroups) {   // all units (see the MMA issuer)
                     ZSTAMP(p0);
                     TZ_WAIT(acc_full + sgm * NU + v, par);
                     ZACC(p_w, p0);

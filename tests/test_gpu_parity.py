@@ -242,6 +242,37 @@ def test_conv3d_binary_eq8(tn, kernel, case):
     np.testing.assert_array_equal(u32(yp), ref)
 
 
+@pytest.mark.parametrize("case", [((5, 16, 64, 128, 128), 16), ((8, 64, 16, 32, 32), 64), ((5, 32, 16, 64, 64), 32),
+                                  ((3, 16, 24, 40, 130), 16)],
+                         ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}")
+def test_conv3d_batched_ranges_cross_samples(tn, kernel, case):
+    """n > 1 with 148 persistent CTAs whose unit ranges run from the ragged last strip of one
+    sample into the first strip of the next (regression: the per-unit barriers of a ragged
+    strip must still advance, or the kernel deadlocks): the batched result equals the
+    per-sample launches bit for bit, and sampled outputs equal the oracle."""
+    shape, k = case
+    x, w = _case(shape, k, seed=shape[0] * 13 + k)
+    base = synth.threshold_base(shape[1], 0.5)
+    lo, hi = synth.jittered_thresholds(k, base, seed=k + 1)
+    xp, wp = tn.tn_pack_i8(dev(x)), tn.tn_pack_weights(dev(w))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, tn.dims(*shape), wp, k, tn.geom(), dev(lo), dev(hi))
+    one = (1,) + shape[1:]
+    for i in range(shape[0]):
+        yi = tn.tn_conv3d_requant(tn.tn_pack_i8(dev(x[i:i + 1])), tn.dims(*one), wp, k, tn.geom(), dev(lo), dev(hi))
+        np.testing.assert_array_equal(u32(yp)[i:i + 1], u32(yi), err_msg=f"sample {i}")
+    g = synth.rng(5)
+    m = 200
+    at = np.stack([g.integers(0, shape[0], m), g.integers(0, k, m), g.integers(0, shape[2], m),
+                   g.integers(0, shape[3], m), g.integers(0, shape[4], m)], 1).astype(np.int32)
+    acc = oracle.conv3d_at(x, w, at)
+    n_, k_, z_, y_, x_ = at.T
+    ref = np.where(acc >= hi[k_], 1, np.where(acc <= lo[k_], -1, 0))
+    ypn = u32(yp)
+    sb = (ypn[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
+    mb = (ypn[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
+    np.testing.assert_array_equal(np.where(mb == 1, np.where(sb == 1, 1, -1), 0), ref)
+
+
 def test_requant_sentinels_and_order(tn):
     i32 = np.iinfo(np.int32)
     y = np.arange(-40, 40, dtype=np.int32).reshape(1, 1, 1, 80, 1).repeat(40, axis=4)
