@@ -488,19 +488,25 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
                         device=dev)
     mine = [i for i in range(len(cfg["seeds"])) if i % world == rank]
     shape = cfg["vol_shape"]
-    vols = [torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][i])).to(dev) for i in mine]
-    ws = net.workspace(shape, dev)
-    logits = torch.empty((1, 2) + shape[2:], dtype=torch.float32, device=dev)
-    for v in vols[:1]:
-        net(v, logits=logits, ws=ws)
+    # this rank's volumes go through ONE batched forward (n = 8 / world): every layer is a
+    # single launch over all of them, so partition tails and kernel prologues are paid once
+    xb = torch.cat([torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][i])) for i in mine], 0).to(dev)
+    bshape = (len(mine),) + tuple(shape[1:])
+    ws = net.workspace(bshape, dev)
+    logits = torch.empty((len(mine), 2) + shape[2:], dtype=torch.float32, device=dev)
+    net(xb, logits=logits, ws=ws)
+    one = net(xb[:1].contiguous())          # the batched forward equals a single-volume one
     torch.cuda.synchronize()
+    if not torch.equal(one, logits[:1]):
+        print(json.dumps({"error": "batched FCN differs from the single-volume forward"}), flush=True)
+        sys.exit(1)
+    del one
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.fcn_steps):
-        for v in vols:
-            net(v, logits=logits, ws=ws)
+        net(xb, logits=logits, ws=ws)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -511,9 +517,10 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
     vox = int(np.prod(shape[2:]))
     total_vox = args.fcn_steps * len(cfg["seeds"]) * vox
     return {"metric": "FCN voxels/s", "value": total_vox / (ms / 1e3), "unit": "voxels/s",
-            "config": "C3: 8 CT-like volumes 1x1x128x256x256, one volume per rank at a time (BASELINE configs[3])",
+            "config": "C3: 8 CT-like volumes 1x1x128x256x256 sharded over the ranks (8 / N each), one batched "
+                      "forward per rank (BASELINE configs[3])",
             "ms_per_batch": ms / args.fcn_steps, "effective_gmacs": total_vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
-            "steps": args.fcn_steps, "gpu_launches_per_volume": 15, "scaling": "strong (fixed batch of 8)"}
+            "steps": args.fcn_steps, "gpu_launches_per_forward": 15, "scaling": "strong (fixed batch of 8)"}
 
 
 def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
