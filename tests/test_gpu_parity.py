@@ -374,7 +374,7 @@ def _fcn_compare(tn, x, p, per_layer=True):
     return got
 
 
-@pytest.mark.parametrize("shape", [(1, 1, 16, 16, 16), (1, 1, 32, 48, 48), (2, 1, 8, 24, 40)])
+@pytest.mark.parametrize("shape", [(1, 1, 16, 16, 16), (1, 1, 32, 48, 48), (2, 1, 8, 24, 40), (3, 1, 32, 64, 64)])
 def test_fcn_matches_oracle_small(tn, fcn_kernel, shape):
     x = synth.ct_volume(shape, seed=shape[3])
     _fcn_compare(tn, x, synth.fcn_params())
