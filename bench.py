@@ -144,6 +144,10 @@ def oracle_c1_sample(x, w, lo, hi, planes: int):
     return planes * 128 * 128 * 64 * 64 * 27
 
 
+C1_WORKLOAD = ("C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 s1 p1 + fused integer-threshold requant, "
+               "P(0)=0.5 act / 0.6 weights (BASELINE configs[1])")
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -166,7 +170,7 @@ def run_reference(args, world, rank):
         "value": value, "unit": "GMAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 + requant (BASELINE configs[1])",
+        "config": {"workload": C1_WORKLOAD,
                    "sample": f"output planes [0,{planes}) of 64 per step"},
         "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": f"oracle conv3d+requant, {planes} of 64 output planes of C1 per step"},
@@ -388,8 +392,7 @@ def main():
             "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 s1 p1 + fused "
-                                   "integer-threshold requant, P(0)=0.5 act / 0.6 weights (BASELINE configs[1])",
+            "config": {"workload": C1_WORKLOAD,
                        "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
                        "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
                        "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)",
