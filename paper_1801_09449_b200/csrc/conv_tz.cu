@@ -1264,11 +1264,6 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     // R3 layers: 16 planes of 9 tiles), so every SM gets work
     int tstart = std::min(tmax, pl.NT);
     {
-        static int env_tmax = -1;   // experiment knob: TN_TZ_TMAX caps the strip width
-        if (env_tmax < 0) { const char* e = getenv("TN_TZ_TMAX"); env_tmax = e ? atoi(e) : 0; }
-        if (env_tmax > 0) tstart = std::min(tstart, env_tmax);
-    }
-    {
         const int nsm = tz_num_sms();
         while (tstart > 1 && static_cast<int64_t>(cd.N) * ((pl.NT + tstart - 1) / tstart) * cd.Do < nsm) --tstart;
     }

@@ -228,17 +228,18 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
     for (int i = 0; i < VPT; ++i) store_voxel<CW>(xp + (g0 + i) * 2 * CW, os[i], om[i]);
 }
 
-// Bulk-staged variant: a CTA walks tiles of kPackTile (512) consecutive voxels
-// (launched one tile per CTA: 32 KB per CTA, six co-resident per SM).  One thread issues one 1-D bulk copy (cp.async.bulk, 1 KB)
-// per channel row of the NEXT tile into the other shared-memory buffer while the
-// 256 threads pack the current one, so DRAM sees C long contiguous reads per
-// tile and the loads overlap the bit work.  Byte-lane SWAR on 4 voxels per
-// thread from shared memory (consecutive threads read consecutive words of a
-// channel row: conflict-free).  Needs DHW % 512 == 0, C <= 64, 16-byte input.
-// C1: 24 us for 64 MiB in + 16 MiB out (3.5 TB/s) against 31 us for the
-// register-only 4-voxel variant below.
-constexpr int kPackTile = 512;
-template <int CW, int kPackTile, bool CHECK>
+// Bulk-staged variant: one tile of kPackTile (256) consecutive voxels per CTA (16 KB
+// of shared memory for C = 64, 13 CTAs co-resident per SM).  Warp 0's lanes issue one
+// 1-D bulk copy (cp.async.bulk, 256 B) per channel row, so DRAM sees C contiguous
+// reads per tile; then byte-lane SWAR over 4 voxels per thread from shared memory
+// (consecutive threads read consecutive words of a channel row: conflict-free),
+// accumulating each byte's nonzero bit and negative bit (sign = mask & ~negative at
+// the end).  Validation work only when d_bad is given.  Triggers the dependent conv's
+// programmatic launch at its start.  Needs DHW % 256 == 0, C <= 64, 16-byte input.
+// C1: 19.8 us for 64 MiB in + 16 MiB out (4.2 TB/s; was 24 us with 512-voxel tiles
+// and per-channel validation, 31 us for the register-only variant below).
+constexpr int kPackTile = 256;
+template <int CW, bool CHECK>
 __global__ void __launch_bounds__(256)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
@@ -500,59 +501,18 @@ cudaError_t launch_pack_i8(const int8_t* x, tn_dims xd, uint32_t* xp, int64_t* d
     const int64_t total = DHW * xd.n;
     const int cw = (xd.c + 31) / 32;
     if (total > 0 && DHW % kPackTile == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (cw == 1 || cw == 2)) {
-        static int num_sms = 0;
-        static bool configured = false;
-        if (num_sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        // one 256-voxel tile per CTA (measured on C1: 256 > 512 > 1024 > 128 voxels; a
+        // persistent double-buffered grid is slower at every CTAs-per-SM count, 26.3-121 us)
+        const int64_t ntiles = total / kPackTile;
+        const size_t smem = static_cast<size_t>(xd.c) * kPackTile;
+        const unsigned blocks = static_cast<unsigned>(ntiles);
+        if (d_bad != nullptr) {
+            if (cw == 1) pack_i8_bulk_kernel<1, true><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
+            else pack_i8_bulk_kernel<2, true><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
+        } else {
+            if (cw == 1) pack_i8_bulk_kernel<1, false><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
+            else pack_i8_bulk_kernel<2, false><<<blocks, kPackTile / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);
         }
-        static int tile = 0;
-        if (!configured) {
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<1, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            cudaFuncSetAttribute(pack_i8_bulk_kernel<2, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            const char* e = getenv("TN_PACK_TILE");
-            tile = e ? atoi(e) : 256;
-            configured = true;
-        }
-        const int64_t ntiles = total / tile;
-        static int per_sm = -1;
-        if (per_sm < 0) { const char* e = getenv("TN_PACK_PERSIST"); per_sm = e ? atoi(e) : 0; }
-        size_t smem = static_cast<size_t>(xd.c) * tile;
-        unsigned blocks = static_cast<unsigned>(ntiles);
-        if (per_sm > 0 && ntiles > static_cast<int64_t>(per_sm) * num_sms) {
-            blocks = static_cast<unsigned>(per_sm * num_sms);   // persistent, double-buffered
-            smem *= 2;
-        }
-#define TN_PT(PTV)                                                                                           \
-        if (tile == PTV) {                                                                                  \
-            if (d_bad != nullptr) {                                                                          \
-                if (cw == 1) pack_i8_bulk_kernel<1, PTV, true><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad); \
-                else pack_i8_bulk_kernel<2, PTV, true><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);         \
-            } else {                                                                                        \
-                if (cw == 1) pack_i8_bulk_kernel<1, PTV, false><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad); \
-                else pack_i8_bulk_kernel<2, PTV, false><<<blocks, PTV / 4, smem, s>>>(x, xd.c, DHW, ntiles, xp, d_bad);         \
-            }                                                                                               \
-        }
-        TN_PT(512)
-        TN_PT(256)
-        TN_PT(128)
-        TN_PT(1024)
-#undef TN_PT
         return cudaGetLastError();
     }
     if (total > 0 && DHW % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
