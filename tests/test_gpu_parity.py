@@ -273,6 +273,45 @@ def test_conv3d_batched_ranges_cross_samples(tn, kernel, case):
     np.testing.assert_array_equal(np.where(mb == 1, np.where(sb == 1, 1, -1), 0), ref)
 
 
+def test_conv3d_empty_inputs(tn, kernel):
+    """Empty tensors (n = 0, or an empty spatial extent) are a successful no-op under every
+    kernel selector; nothing is launched and the output stays untouched."""
+    for shape in [(0, 16, 4, 4, 4), (1, 16, 0, 8, 8), (2, 64, 3, 0, 6)]:
+        k = 16
+        w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.6, seed=3)
+        wp = tn.tn_pack_weights(dev(w))
+        xp = torch.zeros(16, dtype=torch.int32, device="cuda")          # any valid aligned pointer
+        lo = dev(np.full(k, -3, np.int32))
+        hi = dev(np.full(k, 3, np.int32))
+        sentinel = torch.full((64,), 7, dtype=torch.int32, device="cuda")
+        assert tn.lib.tn_conv3d_requant(tn._ptr(xp), tn.dims(*shape), tn._ptr(wp), k, tn.geom(), tn._ptr(lo),
+                                        tn._ptr(hi), tn._ptr(sentinel), tn._stream()) == tn.TN_OK
+        assert tn.lib.tn_conv3d(tn._ptr(xp), tn.dims(*shape), tn._ptr(wp), k, tn.geom(), tn._ptr(sentinel),
+                                tn._stream()) == tn.TN_OK
+        torch.cuda.synchronize()
+        assert bool((sentinel == 7).all())
+
+
+@pytest.mark.parametrize("case", [((1, 16, 3, 4, 1100), 16, 1), ((1, 32, 4, 3, 1030), 32, 2), ((1, 16, 5, 6, 7), 1, 1),
+                                  ((1, 16, 4, 130, 2), 16, 1), ((1, 64, 3, 2, 1024), 64, 1)],
+                         ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}_s{c[2]}")
+def test_conv3d_extreme_widths_and_tiny_k(tn, kernel, case):
+    """Rows wider than the tap-offset kernel's raster limit (Po <= 1024: W = 1030 / 1100 fall
+    back to the dx-merged or popcount kernel under AUTO), a 1024-wide row at the limit, K = 1,
+    and a 2-voxel-wide strip: bit-exact against the oracle."""
+    shape, k, s = case
+    x, w = _case(shape, k, seed=sum(shape) + k)
+    base = synth.threshold_base(shape[1], 0.5)
+    lo, hi = synth.jittered_thresholds(k, base, seed=k + 7)
+    acc = oracle.conv3d(x, w, s)
+    ref, _ = oracle.pack(oracle.requant(acc, lo, hi))
+    xp, wp = tn.tn_pack_i8(dev(x)), tn.tn_pack_weights(dev(w))
+    y = run_or_skip(kernel, tn.tn_conv3d, xp, tn.dims(*shape), wp, k, tn.geom(s))
+    np.testing.assert_array_equal(y.cpu().numpy(), acc.transpose(0, 2, 3, 4, 1))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, tn.dims(*shape), wp, k, tn.geom(s), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+
+
 def test_requant_sentinels_and_order(tn):
     i32 = np.iinfo(np.int32)
     y = np.arange(-40, 40, dtype=np.int32).reshape(1, 1, 1, 80, 1).repeat(40, axis=4)
