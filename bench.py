@@ -523,7 +523,7 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
             "config": "C3: 8 CT-like volumes 1x1x128x256x256 sharded over the ranks (8 / N each), one batched "
                       "forward per rank (BASELINE configs[3])",
             "ms_per_batch": ms / args.fcn_steps, "effective_gmacs": total_vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
-            "steps": args.fcn_steps, "gpu_launches_per_forward": 15, "scaling": "strong (fixed batch of 8)"}
+            "steps": args.fcn_steps, "gpu_launches_per_forward": 14, "scaling": "strong (fixed batch of 8)"}
 
 
 def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
