@@ -49,8 +49,26 @@ __device__ __forceinline__ uint32_t spread8_nib(uint32_t t) {
     return t;
 }
 // 16 ternary lanes (bits sh..sh+15 of a sign / mask word pair) -> 16 FP4 nibbles
+#ifndef TN_F4_PRMT
+#define TN_F4_PRMT 1
+#endif
+// 8 lanes -> a PRMT selector whose nibble k is the lane pair (2k+1, 2k) of x (bits 0..7)
+__device__ __forceinline__ uint32_t pair_selector(uint32_t x) {
+    x &= 0xFFu;
+    x = (x | (x << 4)) & 0x0F0Fu;
+    return (x | (x << 2)) & 0x3333u;
+}
 __device__ __forceinline__ uint2 expand16_f4(uint32_t s, uint32_t m, int sh) {
     const uint32_t mm = m >> sh, nn = (m & ~s) >> sh;
+    if (TN_F4_PRMT) {
+        // byte k of the result = FP4 lanes 2k (low nibble) and 2k+1: each lane pair picks one
+        // of four bytes with PRMT -- mask: {00, 02, 20, 22}, negative: {00, 08, 80, 88}
+        const uint32_t lo = __byte_perm(0x22200200u, 0u, pair_selector(mm)) |
+                            __byte_perm(0x88800800u, 0u, pair_selector(nn));
+        const uint32_t hi = __byte_perm(0x22200200u, 0u, pair_selector(mm >> 8)) |
+                            __byte_perm(0x88800800u, 0u, pair_selector(nn >> 8));
+        return make_uint2(lo, hi);
+    }
     const uint32_t lo = (spread8_nib(mm) << 1) | (spread8_nib(nn) << 3);
     const uint32_t hi = (spread8_nib(mm >> 8) << 1) | (spread8_nib(nn >> 8) << 3);
     return make_uint2(lo, hi);
