@@ -151,6 +151,9 @@ C1_WORKLOAD = ("C1: 1x64x64x128x128 ternary conv3d 64->64 3x3x3 s1 p1 + fused in
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 runs the oracle alone, on every core
+    if world > 1 or os.environ.get("OMP_NUM_THREADS") == "1":
+        os.environ["OMP_NUM_THREADS"] = str(cpu_cores())
     import oracle
     x, w, lo, hi = synth.conv_config("C1")
     planes = 2
