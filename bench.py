@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-fcn", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-binary", action="store_true")
+    ap.add_argument("--no-c0", action="store_true")
     ap.add_argument("--no-slab-schedules", action="store_true")
     ap.add_argument("--c4-halo", choices=("nccl", "p2p"), default="nccl",
                     help="configs[4] halo exchange at N > 1: NCCL send/recv, or NEXT-1 epilogue stores + flags")
@@ -364,6 +365,9 @@ def main():
     if not args.no_fcn:
         fcn = bench_fcn(args, tn, torch, dist, world, rank, dev, stream)
 
+    # ---- configs[0]: the small int32-output layer, launch-latency bound -> CUDA-graph replays
+    c0 = bench_c0(args, tn, torch, dev) if not args.no_c0 else None
+
     # ---- NEXT-4 binary network (Eq. 8): C1 shape with {-1,+1} codes and a sign requant
     binary = None
     if not args.no_binary:
@@ -415,11 +419,48 @@ def main():
             "fcn": fcn,
             "fcn_slab": c4,
             "binary": binary,
+            "c0": c0,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_c0(args, tn, torch, dev):
+    """configs[0] (1x16x32x32x32, 16 -> 16, int32 channel-last output): 226 M MAC per launch is a
+    few microseconds of work, so it is timed as CUDA-graph replays of 100 back-to-back launches
+    (SURVEY 8(d)); parity-checked against the oracle first (all outputs)."""
+    import oracle
+    x, w, _, _ = synth.conv_config("C0")
+    xd = tn.dims(*x.shape)
+    xp = tn.tn_pack_i8(torch.from_numpy(x).to(dev))
+    wp = tn.tn_pack_weights(torch.from_numpy(w).to(dev))
+    y = tn.tn_conv3d(xp, xd, wp, 16, tn.geom())
+    torch.cuda.synchronize()
+    if not np.array_equal(y.cpu().numpy(), oracle.conv3d(x, w).transpose(0, 2, 3, 4, 1)):
+        print(json.dumps({"error": "C0 parity check failed; refusing to report"}), flush=True)
+        sys.exit(1)
+    st = torch.cuda.Stream(device=dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for _ in range(100):
+            tn.tn_conv3d(xp, xd, wp, 16, tn.geom(), y=y, stream=st)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    us = a.elapsed_time(b) * 1e3 / 500
+    macs = 32 * 32 * 32 * 16 * 16 * 27
+    return {"metric": "ternary conv3d effective GMAC/s (C0, int32 output)", "unit": "GMAC/s",
+            "value": macs / (us / 1e6) / 1e9, "us_per_launch": us,
+            "config": "C0: 1x16x32x32x32 16->16 3x3x3 s1 p1, int32 channel-last output (BASELINE configs[0]); "
+                      "CUDA-graph replays of 100 launches, L2-resident (2.3 MB working set)",
+            "parity": "passed (all outputs vs oracle)"}
 
 
 def bench_binary(args, tn, torch, dist, world, rank, dev, stream, flush):
