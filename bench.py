@@ -367,6 +367,7 @@ def main():
 
     # ---- configs[0]: the small int32-output layer, launch-latency bound -> CUDA-graph replays
     c0 = bench_c0(args, tn, torch, dev) if not args.no_c0 else None
+    c2 = bench_c2(args, tn, torch, dev, stream) if not args.no_fcn else None
 
     # ---- NEXT-4 binary network (Eq. 8): C1 shape with {-1,+1} codes and a sign requant
     binary = None
@@ -420,11 +421,38 @@ def main():
             "fcn_slab": c4,
             "binary": binary,
             "c0": c0,
+            "fcn_c2": c2,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_c2(args, tn, torch, dev, stream):
+    """configs[2]: one 1x1x96x144x144 CT-like volume through the FCN (device time per volume)."""
+    cfg = synth.CONFIGS["C2"]
+    shape = cfg["vol_shape"]
+    p = synth.fcn_params(cfg["seed_params"])
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"], device=dev)
+    x = torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][0])).to(dev)
+    ws = net.workspace(shape, dev)
+    logits = torch.empty((1, 2) + shape[2:], dtype=torch.float32, device=dev)
+    for _ in range(2):
+        net(x, logits=logits, ws=ws)
+    torch.cuda.synchronize()
+    steps = max(3, args.fcn_steps)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        net(x, logits=logits, ws=ws)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    vox = int(np.prod(shape[2:]))
+    return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s", "ms_per_volume": ms,
+            "config": "C2: one CT-like volume 1x1x96x144x144 (BASELINE configs[2]); parity at this size in "
+                      "test_fcn_c2_full_size_matches_oracle", "steps": steps}
 
 
 def bench_c0(args, tn, torch, dev):
