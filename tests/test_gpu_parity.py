@@ -413,6 +413,26 @@ def _fcn_compare(tn, x, p, per_layer=True):
     return got
 
 
+@pytest.mark.parametrize("nclass", [1, 3, 8])
+def test_fcn_prediction_class_counts(tn, fcn_kernel, nclass):
+    """A8 with 1, 3 and 8 classes (the fused epilogue's generic table path; the 2-class case is
+    in every other FCN test): logits equal the oracle's prediction of the oracle's layer-14 codes."""
+    shape = (2, 1, 16, 24, 40)
+    x = synth.ct_volume(shape, seed=nclass)
+    p = synth.fcn_params()
+    g = synth.rng(70 + nclass)
+    pw = (0.25 * g.standard_normal((nclass, 16))).astype(np.float32)
+    pb = (0.1 * g.standard_normal(nclass)).astype(np.float32)
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], pw, pb, p["t_lo"], p["t_hi"])
+    got = net(dev(x)).cpu().numpy()
+    _, acts, _ = oracle.fcn_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"],
+                                    p["pred_b"], want_acts=True)
+    ref = oracle.predict(acts[13], pw, pb)
+    assert got.shape == ref.shape
+    tol = np.maximum(np.abs(ref), _logit_tol(pw, pb) / 1e-5) * 1e-5
+    assert np.all(np.abs(got - ref) <= tol)
+
+
 @pytest.mark.parametrize("shape", [(1, 1, 16, 16, 16), (1, 1, 32, 48, 48), (2, 1, 8, 24, 40), (3, 1, 32, 64, 64)])
 def test_fcn_matches_oracle_small(tn, fcn_kernel, shape):
     x = synth.ct_volume(shape, seed=shape[3])
