@@ -593,6 +593,29 @@ def test_fcn_slab_nccl_single_rank(tn):
         net.forward_slab(comm, xd, shape, 0, 12)
 
 
+def test_fcn_nonfinite_input_reported(tn):
+    """A non-finite CT value reaches d_bad as its flat NCDHW index (SPEC.md:39 pattern) through the
+    batched FCN forward and through both slab schedules (global z offsets in bad_base)."""
+    p = synth.fcn_params()
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    shape = (2, 1, 16, 24, 40)
+    x = synth.ct_volume(shape, seed=4)
+    x[1, 0, 7, 3, 5] = np.nan
+    x[1, 0, 9, 0, 0] = np.inf
+    flag = tn.bad_flag()
+    net(dev(x), d_bad=flag)
+    _, obad = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    assert bad_value(flag) == obad == ((1 * 16 + 7) * 24 + 3) * 40 + 5
+    shape = (1, 1, 32, 24, 40)
+    x = synth.ct_volume(shape, seed=5)
+    x[0, 0, 21, 2, 9] = -np.inf
+    _, obad = oracle.tern_f32(x, synth.CT_T_LO, synth.CT_T_HI)
+    for fn in (net.forward_slabs_local, net.forward_slabs_local_p2p):
+        flag = tn.bad_flag()
+        fn(dev(x), 2, d_bad=flag)
+        assert bad_value(flag) == obad == (21 * 24 + 2) * 40 + 9
+
+
 # --------------------------------------------------------------------------- NEXT-1: epilogue-fused halos
 @pytest.mark.parametrize("shape,nslabs", [((1, 1, 32, 48, 48), 2), ((1, 1, 64, 24, 40), 8),
                                           ((1, 1, 16, 40, 56), 2)])
