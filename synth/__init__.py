@@ -96,6 +96,23 @@ def conv_config(name: str):
     return x, w, lo, hi
 
 
+def binary_config():
+    """NEXT-4 binary workload on C1's shape: {-1,+1} activations (seed 13) and weights (seed 14),
+    sign thresholds hi in {-2, 0, 2} (seed 15) with lo = hi - 1 (acc is always even)."""
+    x = ternary_codes((1, 64, 64, 128, 128), 0.0, seed=13)
+    w = ternary_codes((64, 64, 3, 3, 3), 0.0, seed=14)
+    hi = (2 * rng(15).integers(-1, 2, size=64)).astype(np.int32)
+    return x, w, hi - 1, hi
+
+
+def sample_positions(shape, k, m, seed):
+    """m random output coordinates (n, k, z, y, x) of a stride-1 conv over shape (for sampled parity)."""
+    g = rng(seed)
+    n, _, d, h, w = shape
+    return np.stack([g.integers(0, n, m), g.integers(0, k, m), g.integers(0, d, m),
+                     g.integers(0, h, m), g.integers(0, w, m)], 1).astype(np.int32)
+
+
 def fcn_params(seed: int = 21):
     """Ternary weights, integer thresholds and prediction weights for the FCN.
 

@@ -412,3 +412,20 @@ def test_conv3d_binary_windows_eq8():
     t = oracle.requant(y, hi - 1, hi)
     assert np.all(t != 0)
     np.testing.assert_array_equal(t, np.where(y >= hi[None, :, None, None, None], 1, -1))
+
+
+# --------------------------------------------------------------------------- bench golden samples
+def test_bench_golden_samples_are_the_oracles():
+    """tests/golden/bench_samples.npz (bench.py's parity gates) holds exactly what the oracle
+    computes at those sampled outputs (rewritten only by tools/make_bench_golden.py)."""
+    g = np.load(os.path.join(GOLDEN, "bench_samples.npz"))
+    x0, w0, _, _ = synth.conv_config("C0")
+    np.testing.assert_array_equal(g["c0_at"], synth.sample_positions(x0.shape, 16, 512, seed=777))
+    np.testing.assert_array_equal(oracle.conv3d_at(x0, w0, g["c0_at"]), g["c0_ref"])
+    for (x, w, lo, hi), at, ref in ((synth.conv_config("C1"), g["c1_at"], g["c1_ref"]),
+                                    (synth.binary_config(), g["bin_at"], g["bin_ref"])):
+        acc = oracle.conv3d_at(x, w, at)
+        k = at[:, 1]
+        want = np.where(acc >= hi[k], 1, np.where(acc <= lo[k], -1, 0))
+        np.testing.assert_array_equal(want, ref)
+    assert np.all(g["bin_ref"] != 0) and set(np.unique(g["c1_ref"])) == {-1, 0, 1}
