@@ -421,7 +421,6 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     }
     const uint32_t tmem_base = *s_tmem;
     pdl_launch_dependents();
-    pdl_wait();   // activations of the previous layer are complete and visible from here on
 
     if (warp < kZEpiWarps) {
         // ---- initialise this warp's TMEM blocks (its quadrant, its tiles, all RO blocks)
@@ -446,6 +445,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         tmem_wait_st();
         tc_fence_before();
     }
+    pdl_wait();   // activations of the previous layer are complete and visible from here on
     __syncthreads();
     tc_fence_after();
 
