@@ -231,7 +231,7 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
 // Bulk-staged variant: one tile of kPackTile (256) consecutive voxels per CTA (16 KB
 // of shared memory for C = 64, 13 CTAs co-resident per SM).  Warp 0's lanes issue one
 // 1-D bulk copy (cp.async.bulk, 256 B) per channel row, so DRAM sees C contiguous
-// reads per tile; then byte-lane SWAR over 4 voxels per thread from shared memory
+// reads per tile, each 32-channel word on its own mbarrier; then byte-lane SWAR over 4 voxels per thread from shared memory
 // (consecutive threads read consecutive words of a channel row: conflict-free),
 // accumulating each byte's nonzero bit and negative bit (sign = mask & ~negative at
 // the end).  Validation work only when d_bad is given.  Triggers the dependent conv's
@@ -240,102 +240,85 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
 // and per-channel validation, 31 us for the register-only variant below).
 constexpr int kPackTile = 256;
 template <int CW, bool CHECK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kPackTile / 4)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
-    extern __shared__ __align__(128) uint8_t sx[];          // [2][C][kPackTile]
-    __shared__ __align__(8) uint64_t bar[2];
+    extern __shared__ __align__(128) uint8_t sx[];          // [C][kPackTile]
+    __shared__ __align__(8) uint64_t bar[2];                // one per 32-channel word
     // let a PDL-launched consumer (the conv) start its prologue as SMs free up; it still
     // waits (griddepcontrol.wait) for this whole grid before reading the packed tensor
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int tile_bytes = C * kPackTile;
-    auto issue = [&](int64_t tile, int b) {
-        const int64_t t0 = tile * kPackTile;
-        const int64_t n = t0 / DHW;
-        const int8_t* xb = x + n * C * DHW + (t0 - n * DHW);
-        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(tile_bytes) : "memory");
-        for (int c = 0; c < C; ++c)
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             static_cast<uint32_t>(__cvta_generic_to_shared(sx + b * tile_bytes + c * kPackTile))),
-                         "l"(xb + c * DHW), "r"(kPackTile), "r"(sb)
-                         : "memory");
-    };
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b])))
-                         : "memory");
+    const int64_t tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    if (threadIdx.x < CW) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x])))
+                     : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x < 32 && blockIdx.x < ntiles) {
-        // first tile: the 32 lanes of warp 0 issue the channel-row copies in parallel
-        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kPackTile;
+    const int64_t t0 = tile * kPackTile;
+    if (threadIdx.x < 32) {
+        // the 32 lanes of warp 0 issue the channel-row copies; word j's rows complete on bar[j],
+        // so the bit work on word 0 overlaps the arrival of word 1
         const int64_t n = t0 / DHW;
         const int8_t* xb = x + n * C * DHW + (t0 - n * DHW);
-        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[0]));
-        if (threadIdx.x == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(tile_bytes) : "memory");
+        if (threadIdx.x < CW) {
+            const int cj = min(32, C - 32 * static_cast<int>(threadIdx.x));
+            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x]));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(cj * kPackTile) : "memory");
+        }
         __syncwarp();
-        for (int c = threadIdx.x; c < C; c += 32)
+        for (int c = threadIdx.x; c < C; c += 32) {
+            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[c >> 5]));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              static_cast<uint32_t>(__cvta_generic_to_shared(sx + c * kPackTile))),
                          "l"(xb + c * DHW), "r"(kPackTile), "r"(sb)
                          : "memory");
+        }
     }
-    const int i4 = threadIdx.x;                 // this thread's 4 voxels of a tile
-    uint32_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int b = it & 1;
-        // prefetch the next tile into the other buffer (its previous contents were
-        // consumed before the __syncthreads that ended the last iteration)
-        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, b ^ 1);
-        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
-        asm volatile("{\n\t.reg .pred p;\nTN_PW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-                     "@!p bra TN_PW_%=;\n\t}" ::"r"(sb), "r"((it >> 1) & 1) : "memory");
-        const uint8_t* st = sx + b * tile_bytes;
-        const int64_t t0 = tile * kPackTile;
-        uint32_t os[4][CW], om[4][CW];
-        uint32_t bad = 0;
+    const int i4 = threadIdx.x;                 // this thread's 4 voxels of the tile
+    uint32_t os[4][CW], om[4][CW];
+    uint32_t bad = 0;
 #pragma unroll
-        for (int j = 0; j < CW; ++j) {
-            uint32_t accS[4], accM[4];
+    for (int j = 0; j < CW; ++j) {
+        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[j]));
+        asm volatile("{\n\t.reg .pred p;\nTN_PW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+                     "@!p bra TN_PW_%=;\n\t}" ::"r"(sb) : "memory");
+        uint32_t accS[4], accM[4];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                // bit jj of each byte: lsb (nonzero) and bit 7 (negative) of channel 8g + jj;
-                // the fields are disjoint, so sign = mask & ~negative at the end
-                uint32_t an = 0u, am = 0u;
+        for (int g = 0; g < 4; ++g) {
+            // bit jj of each byte: lsb (nonzero) and bit 7 (negative) of channel 8g + jj;
+            // the fields are disjoint, so sign = mask & ~negative at the end
+            uint32_t an = 0u, am = 0u;
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int c = 32 * j + 8 * g + jj;
-                    const uint32_t w = c < C ? reinterpret_cast<const uint32_t*>(st + c * kPackTile)[i4] : 0u;
-                    if (CHECK) {
-                        const uint32_t lsb = w & 0x01010101u, t7 = (w >> 7) & 0x01010101u;
-                        bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
-                    }
-                    am |= (w << jj) & (0x01010101u << jj);
-                    an |= (w >> (7 - jj)) & (0x01010101u << jj);
+            for (int jj = 0; jj < 8; ++jj) {
+                const int c = 32 * j + 8 * g + jj;
+                const uint32_t w = c < C ? reinterpret_cast<const uint32_t*>(sx + c * kPackTile)[i4] : 0u;
+                if (CHECK) {
+                    const uint32_t lsb = w & 0x01010101u, t7 = (w >> 7) & 0x01010101u;
+                    bad |= ((w & 0xFEFEFEFEu) ^ (t7 * 0xFEu)) | (t7 & ~lsb);
                 }
-                accS[g] = am & ~an;
-                accM[g] = am;
+                am |= (w << jj) & (0x01010101u << jj);
+                an |= (w >> (7 - jj)) & (0x01010101u << jj);
             }
-            transpose4x4(accS[0], accS[1], accS[2], accS[3], os[0][j], os[1][j], os[2][j], os[3][j]);
-            transpose4x4(accM[0], accM[1], accM[2], accM[3], om[0][j], om[1][j], om[2][j], om[3][j]);
+            accS[g] = am & ~an;
+            accM[g] = am;
         }
-        if (CHECK && bad != 0u) {
-            const int64_t n = t0 / DHW, v0 = t0 - n * DHW;
-            int64_t first = LLONG_MAX;
-            for (int c = 0; c < C; ++c)
-                for (int i = 0; i < 4; ++i) {
-                    const int8_t v = static_cast<int8_t>(st[c * kPackTile + 4 * i4 + i]);
-                    if (v < -1 || v > 1) first = min(first, (n * C + c) * DHW + v0 + 4 * i4 + i);
-                }
-            report_bad(d_bad, first);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) store_voxel<CW>(xp + (t0 + 4 * i4 + i) * 2 * CW, os[i], om[i]);
-        __syncthreads();   // buffer b is free for the prefetch two iterations on
+        transpose4x4(accS[0], accS[1], accS[2], accS[3], os[0][j], os[1][j], os[2][j], os[3][j]);
+        transpose4x4(accM[0], accM[1], accM[2], accM[3], om[0][j], om[1][j], om[2][j], om[3][j]);
     }
+    if (CHECK && bad != 0u) {
+        const int64_t n = t0 / DHW, v0 = t0 - n * DHW;
+        int64_t first = LLONG_MAX;
+        for (int c = 0; c < C; ++c)
+            for (int i = 0; i < 4; ++i) {
+                const int8_t v = static_cast<int8_t>(sx[c * kPackTile + 4 * i4 + i]);
+                if (v < -1 || v > 1) first = min(first, (n * C + c) * DHW + v0 + 4 * i4 + i);
+            }
+        report_bad(d_bad, first);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) store_voxel<CW>(xp + (t0 + 4 * i4 + i) * 2 * CW, os[i], om[i]);
 }
 
 template <typename T>
