@@ -244,13 +244,13 @@ __global__ void __launch_bounds__(kPackTile / 4)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
     extern __shared__ __align__(128) uint8_t sx[];          // [C][kPackTile]
-    __shared__ __align__(8) uint64_t bar[2];                // one per 32-channel word
+    __shared__ __align__(8) uint64_t bar[8];                // one per 8-channel group
     // let a PDL-launched consumer (the conv) start its prologue as SMs free up; it still
     // waits (griddepcontrol.wait) for this whole grid before reading the packed tensor
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t tile = blockIdx.x;
     if (tile >= ntiles) return;
-    if (threadIdx.x < CW) {
+    if (threadIdx.x < 4 * CW) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x])))
                      : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -262,14 +262,14 @@ pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t nt
         // so the bit work on word 0 overlaps the arrival of word 1
         const int64_t n = t0 / DHW;
         const int8_t* xb = x + n * C * DHW + (t0 - n * DHW);
-        if (threadIdx.x < CW) {
-            const int cj = min(32, C - 32 * static_cast<int>(threadIdx.x));
+        if (threadIdx.x < 4 * CW) {   // group of 8 channels (empty groups past C: zero bytes)
+            const int cj = max(0, min(8, C - 8 * static_cast<int>(threadIdx.x)));
             const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x]));
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(cj * kPackTile) : "memory");
         }
         __syncwarp();
         for (int c = threadIdx.x; c < C; c += 32) {
-            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[c >> 5]));
+            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[c >> 3]));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              static_cast<uint32_t>(__cvta_generic_to_shared(sx + c * kPackTile))),
                          "l"(xb + c * DHW), "r"(kPackTile), "r"(sb)
@@ -281,12 +281,12 @@ pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t nt
     uint32_t bad = 0;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
-        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[j]));
-        asm volatile("{\n\t.reg .pred p;\nTN_PW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-                     "@!p bra TN_PW_%=;\n\t}" ::"r"(sb) : "memory");
         uint32_t accS[4], accM[4];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
+            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[4 * j + g]));
+            asm volatile("{\n\t.reg .pred p;\nTN_PW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+                         "@!p bra TN_PW_%=;\n\t}" ::"r"(sb) : "memory");
             // bit jj of each byte: lsb (nonzero) and bit 7 (negative) of channel 8g + jj;
             // the fields are disjoint, so sign = mask & ~negative at the end
             uint32_t an = 0u, am = 0u;
