@@ -228,52 +228,46 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
     for (int i = 0; i < VPT; ++i) store_voxel<CW>(xp + (g0 + i) * 2 * CW, os[i], om[i]);
 }
 
-// Bulk-staged variant: one tile of kPackTile (256) consecutive voxels per CTA (16 KB
-// of shared memory for C = 64, 13 CTAs co-resident per SM).  Warp 0's lanes issue one
-// 1-D bulk copy (cp.async.bulk, 256 B) per channel row, so DRAM sees C contiguous
-// reads per tile, each 32-channel word on its own mbarrier; then byte-lane SWAR over 4 voxels per thread from shared memory
-// (consecutive threads read consecutive words of a channel row: conflict-free),
-// accumulating each byte's nonzero bit and negative bit (sign = mask & ~negative at
-// the end).  Validation work only when d_bad is given.  Triggers the dependent conv's
-// programmatic launch at its start.  Needs DHW % 256 == 0, C <= 64, 16-byte input.
-// C1: 19.8 us for 64 MiB in + 16 MiB out (4.2 TB/s; was 24 us with 512-voxel tiles
-// and per-channel validation, 31 us for the register-only variant below).
+// Shared-memory-staged variant: one tile of kPackTile (256) consecutive voxels per CTA
+// (16 KB of shared memory for C = 64, 13 CTAs co-resident per SM).  The threads copy the
+// tile's C channel rows (contiguous 256-byte runs in DRAM) with 16-byte cp.async in eight
+// commit groups of 8 channels, then byte-lane SWAR over 4 voxels per thread from shared
+// memory (consecutive threads read consecutive words of a channel row: conflict-free),
+// accumulating each byte's nonzero bit and negative bit (sign = mask & ~negative at the
+// end); the bit work on a group overlaps the arrival of the later groups.  Validation
+// work only when d_bad is given.  Triggers the dependent conv's programmatic launch at
+// its start.  Needs DHW % 256 == 0, C <= 64, 16-byte input.
+// C1: 18.0 us for 64 MiB in + 16 MiB out (4.7 TB/s; 1-D bulk copies per channel row:
+// 18.7 us; 512-voxel tiles with per-channel validation: 24 us; register-only variant
+// below: 31 us).
 constexpr int kPackTile = 256;
 template <int CW, bool CHECK>
 __global__ void __launch_bounds__(kPackTile / 4)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
                     uint32_t* __restrict__ xp, int64_t* d_bad) {
     extern __shared__ __align__(128) uint8_t sx[];          // [C][kPackTile]
-    __shared__ __align__(8) uint64_t bar[8];                // one per 8-channel group
     // let a PDL-launched consumer (the conv) start its prologue as SMs free up; it still
     // waits (griddepcontrol.wait) for this whole grid before reading the packed tensor
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t tile = blockIdx.x;
     if (tile >= ntiles) return;
-    if (threadIdx.x < 4 * CW) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x])))
-                     : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     const int64_t t0 = tile * kPackTile;
-    if (threadIdx.x < 32) {
-        // the 32 lanes of warp 0 issue the channel-row copies; word j's rows complete on bar[j],
-        // so the bit work on word 0 overlaps the arrival of word 1
+    {
+        // every thread copies 16-byte pieces of the channel rows with cp.async, one commit
+        // group per 8 channels, so the bit work on a group overlaps the later groups' arrival
         const int64_t n = t0 / DHW;
         const int8_t* xb = x + n * C * DHW + (t0 - n * DHW);
-        if (threadIdx.x < 4 * CW) {   // group of 8 channels (empty groups past C: zero bytes)
-            const int cj = max(0, min(8, C - 8 * static_cast<int>(threadIdx.x)));
-            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[threadIdx.x]));
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(cj * kPackTile) : "memory");
-        }
-        __syncwarp();
-        for (int c = threadIdx.x; c < C; c += 32) {
-            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[c >> 3]));
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             static_cast<uint32_t>(__cvta_generic_to_shared(sx + c * kPackTile))),
-                         "l"(xb + c * DHW), "r"(kPackTile), "r"(sb)
-                         : "memory");
+        constexpr int kPieces = kPackTile / 16;      // per channel row
+#pragma unroll
+        for (int gq = 0; gq < 4 * CW; ++gq) {
+            const int c0 = 8 * gq, c1 = min(C, c0 + 8);
+            for (int e = threadIdx.x; e < (c1 - c0) * kPieces; e += kPackTile / 4) {
+                const int c = c0 + e / kPieces, pc = e % kPieces;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                                 __cvta_generic_to_shared(sx + c * kPackTile + 16 * pc))),
+                             "l"(xb + c * DHW + 16 * pc) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
     }
     const int i4 = threadIdx.x;                 // this thread's 4 voxels of the tile
@@ -284,9 +278,17 @@ pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t nt
         uint32_t accS[4], accM[4];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-            const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[4 * j + g]));
-            asm volatile("{\n\t.reg .pred p;\nTN_PW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-                         "@!p bra TN_PW_%=;\n\t}" ::"r"(sb) : "memory");
+            // wait for this thread's copies of group 4j+g, then for everyone's
+            const int left = 4 * CW - 1 - (4 * j + g);
+            if (left >= 7) asm volatile("cp.async.wait_group 7;" ::: "memory");
+            else if (left == 6) asm volatile("cp.async.wait_group 6;" ::: "memory");
+            else if (left == 5) asm volatile("cp.async.wait_group 5;" ::: "memory");
+            else if (left == 4) asm volatile("cp.async.wait_group 4;" ::: "memory");
+            else if (left == 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+            else if (left == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else if (left == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
             // bit jj of each byte: lsb (nonzero) and bit 7 (negative) of channel 8g + jj;
             // the fields are disjoint, so sign = mask & ~negative at the end
             uint32_t an = 0u, am = 0u;
