@@ -240,7 +240,10 @@ pack_i8_swar_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t to
 // C1: 18.0 us for 64 MiB in + 16 MiB out (4.7 TB/s; 1-D bulk copies per channel row:
 // 18.7 us; 512-voxel tiles with per-channel validation: 24 us; register-only variant
 // below: 31 us).
-constexpr int kPackTile = 256;
+#ifndef TN_PACK_TILE
+#define TN_PACK_TILE 256
+#endif
+constexpr int kPackTile = TN_PACK_TILE;
 template <int CW, bool CHECK>
 __global__ void __launch_bounds__(kPackTile / 4)
 pack_i8_bulk_kernel(const int8_t* __restrict__ x, int C, int64_t DHW, int64_t ntiles,
