@@ -398,6 +398,21 @@ def main():
         cpu = {"value": mm / dt / 1e9, "unit": "GMAC/s", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": f"oracle conv3d+requant over output planes [0,{planes}) of C1's 64 ({dt:.1f} s)",
                "host_cores_visible": cpu_cores()}
+        # the other configs' oracle timings, same cores: C0 whole, one C2 volume
+        x0, w0, _, _ = synth.conv_config("C0")
+        t0 = time.perf_counter()
+        oracle.conv3d(x0, w0)
+        dt0 = time.perf_counter() - t0
+        c2 = synth.CONFIGS["C2"]
+        p2 = synth.fcn_params(c2["seed_params"])
+        v2 = synth.ct_volume(c2["vol_shape"], seed=c2["seeds"][0])
+        t0 = time.perf_counter()
+        oracle.fcn_forward(v2, p2["t_lo"], p2["t_hi"], p2["weights"], p2["lo"], p2["hi"], p2["pred_w"], p2["pred_b"])
+        dt2 = time.perf_counter() - t0
+        cpu["other_configs"] = {
+            "C0": {"value": 32 * 32 * 32 * 16 * 16 * 27 / dt0 / 1e9, "unit": "GMAC/s", "seconds": dt0},
+            "C2": {"value": int(np.prod(c2["vol_shape"])) / dt2, "unit": "voxels/s", "seconds": dt2,
+                   "sample": "one whole 96x144x144 volume through the oracle FCN"}}
 
     if rank == 0:
         line = {
