@@ -1,6 +1,7 @@
-// Microtest (round-2 groundwork): tcgen05.mma kind::f8f6f4 with E2M1 operands in 8-bit
-// containers and f16 or f32 accumulators, on ternary values {-1,0,+1}.  Which bits of the
-// container hold the E2M1 code, whether f16 accumulation of small integers is exact, how
+// Microtest (round-2 groundwork): tcgen05.mma kind::f8f6f4 with E2M1 operands
+// and f16 or f32 accumulators, on ternary values {-1,0,+1}.  Which smem placement of the
+// E2M1 codes the MMA reads (found: 16 codes packed in the first 8 bytes of each 16-byte
+// row), whether f16 accumulation of small integers is exact (yes), how
 // f16 results sit in TMEM, and cycles per 128xNx32 MMA.
 // usage: f8f6f4_test  (prints one line per (placement, D format, N))
 #include <cstdio>
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(128, 1) kern(const uint8_t* A, const uint8_t* 
 static uint8_t fp4(int v) { return v == 1 ? 0x2 : (v == -1 ? 0xA : 0x0); }
 
 int main() {
-    for (int shift : {0, 1, 2, 3, 4}) {   // E2M1 code at bit `shift` of the byte
+    for (int shift : {0, 4, 8}) {   // 0 / 4: E2M1 code at bit `shift` of a byte; 8: 16 codes packed in the first 8 bytes of each 16-byte row
         for (int dfmt : {1, 0}) {         // f32, f16 accumulators
             for (int n : {48, 96}) {
                 std::vector<int> a(128 * 32), b(n * 32);
@@ -94,10 +95,14 @@ int main() {
                 for (auto& v : a) v = rand() % 3 - 1;
                 for (auto& v : b) v = rand() % 3 - 1;
                 std::vector<uint8_t> A(4096, 0), B(2 * n * 16, 0);
+                auto put = [&](std::vector<uint8_t>& M, size_t row0, int k, int v) {
+                    if (shift == 8) M[row0 + (k % 16) / 2] |= fp4(v) << (4 * (k & 1));
+                    else M[row0 + (k % 16)] = fp4(v) << shift;
+                };
                 for (int r = 0; r < 128; ++r)
-                    for (int k = 0; k < 32; ++k) A[(k / 16) * 2048 + r * 16 + (k % 16)] = fp4(a[r * 32 + k]) << shift;
+                    for (int k = 0; k < 32; ++k) put(A, (k / 16) * 2048 + r * 16, k, a[r * 32 + k]);
                 for (int r = 0; r < n; ++r)
-                    for (int k = 0; k < 32; ++k) B[(k / 16) * n * 16 + r * 16 + (k % 16)] = fp4(b[r * 32 + k]) << shift;
+                    for (int k = 0; k < 32; ++k) put(B, (size_t)(k / 16) * n * 16 + r * 16, k, b[r * 32 + k]);
                 uint8_t *dA, *dB; uint32_t* dD; long long* dc;
                 cudaMalloc(&dA, A.size()); cudaMalloc(&dB, B.size()); cudaMalloc(&dD, 128 * n * 4); cudaMalloc(&dc, 148 * 8);
                 cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
