@@ -2,7 +2,8 @@
 // and f16 or f32 accumulators, on ternary values {-1,0,+1}.  Which smem placement of the
 // E2M1 codes the MMA reads (found: 16 codes packed in the first 8 bytes of each 16-byte
 // row), whether f16 accumulation of small integers is exact (yes), how
-// f16 results sit in TMEM, and cycles per 128xNx32 MMA.
+// f16 results sit in TMEM (low half of a column; .pack::16b loads pair them), and cycles
+// per 128xNx32 MMA.
 // usage: f8f6f4_test  (prints one line per (placement, D format, N))
 #include <cstdio>
 #include <cstdint>
@@ -75,6 +76,14 @@ __global__ void __launch_bounds__(128, 1) kern(const uint8_t* A, const uint8_t* 
         if (blockIdx.x == 0)
             for (int i = 0; i < 16; ++i) D[threadIdx.x * n + c + i] = v[i];
     }
+    if (dfmt == 0 && blockIdx.x == 0) {   // the first 16 f16 columns, two per register (.pack::16b)
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(d + ((uint32_t)(32 * w) << 16)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int i = 0; i < 8; ++i) D[128 * n + threadIdx.x * 8 + i] = v[i];
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -87,7 +96,7 @@ __global__ void __launch_bounds__(128, 1) kern(const uint8_t* A, const uint8_t* 
 static uint8_t fp4(int v) { return v == 1 ? 0x2 : (v == -1 ? 0xA : 0x0); }
 
 int main() {
-    for (int shift : {0, 4, 8}) {   // 0 / 4: E2M1 code at bit `shift` of a byte; 8: 16 codes packed in the first 8 bytes of each 16-byte row
+    for (int shift : {8}) {   // 0 / 4: E2M1 code at bit `shift` of a byte; 8: 16 codes packed in the first 8 bytes of each 16-byte row
         for (int dfmt : {1, 0}) {         // f32, f16 accumulators
             for (int n : {48, 96}) {
                 std::vector<int> a(128 * 32), b(n * 32);
@@ -104,7 +113,7 @@ int main() {
                 for (int r = 0; r < n; ++r)
                     for (int k = 0; k < 32; ++k) put(B, (size_t)(k / 16) * n * 16 + r * 16, k, b[r * 32 + k]);
                 uint8_t *dA, *dB; uint32_t* dD; long long* dc;
-                cudaMalloc(&dA, A.size()); cudaMalloc(&dB, B.size()); cudaMalloc(&dD, 128 * n * 4); cudaMalloc(&dc, 148 * 8);
+                cudaMalloc(&dA, A.size()); cudaMalloc(&dB, B.size()); cudaMalloc(&dD, 128 * n * 4 + 128 * 8 * 4); cudaMalloc(&dc, 148 * 8);
                 cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
                 cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
                 cudaMemset(dD, 0, 128 * n * 4);
@@ -112,7 +121,7 @@ int main() {
                 kern<<<1, 128, 64 * 1024>>>(dA, dB, dD, n, dfmt, 1, dc);
                 cudaError_t e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) { printf("shift %d dfmt %d N=%d error %s\n", shift, dfmt, n, cudaGetErrorString(e)); return 1; }
-                std::vector<uint32_t> D(128 * n);
+                std::vector<uint32_t> D(128 * n + 128 * 8);
                 cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
                 int bad32 = 0, badlo = 0, badpk = 0;
                 for (int m = 0; m < 128; ++m)
@@ -127,6 +136,19 @@ int main() {
                         __half hp = __ushort_as_half((unsigned short)((D[m * n + j / 2] >> (16 * (j & 1))) & 0xFFFF));
                         if ((float)ref != __half2float(hp)) ++badpk;
                     }
+                int badp16 = -1;
+                if (dfmt == 0) {   // .pack::16b: register i of row m holds columns 2i (low) and 2i+1 (high)
+                    badp16 = 0;
+                    for (int m = 0; m < 128; ++m)
+                        for (int j = 0; j < 16; ++j) {
+                            int ref = 0;
+                            for (int k = 0; k < 32; ++k) ref += a[m * 32 + k] * b[j * 32 + k];
+                            const uint32_t r32 = D[128 * n + m * 8 + j / 2];
+                            __half h = __ushort_as_half((unsigned short)((r32 >> (16 * (j & 1))) & 0xFFFF));
+                            if ((float)ref != __half2float(h)) ++badp16;
+                        }
+                    printf("    .pack::16b load of 16 f16 columns: mismatches %d of %d\n", badp16, 128 * 16);
+                }
                 const int R = 4096;
                 kern<<<148, 128, 64 * 1024>>>(dA, dB, dD, n, dfmt, R, dc);
                 e = cudaDeviceSynchronize();
