@@ -148,6 +148,11 @@ def oracle_c1_sample(x, w, lo, hi, planes: int):
 GOLDEN = os.path.join(ROOT, "tests", "golden", "bench_samples.npz")
 
 
+def bench_peaks():
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(pk)) if os.path.exists(pk) else {}
+
+
 def golden():
     """Expected sampled outputs for the parity gates, written by tools/make_bench_golden.py (which
     calls only the oracle): the GPU arm does not execute oracle/ outside its cpu_baseline leg."""
@@ -202,8 +207,22 @@ def run_reference(args, world, rank):
 
 
 # ----------------------------------------------------------------------------- our arm
+def self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run with N
+    ranks (one per GPU, rendezvous on 127.0.0.1), so that --gpus is never silently ignored."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -212,6 +231,9 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE {world}; refusing to report"}), flush=True)
+        sys.exit(2)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -338,7 +360,7 @@ def main():
     # ---- roofline of the dominant kernel (the conv)
     conv_avg_s = float(np.mean(conv_ms)) / 1e3
     kernel = tn.tn_conv_kernel_for([xd], 64, g)
-    uses_tc = kernel in (tn.TN_KERNEL_TC, tn.TN_KERNEL_TZ)
+    uses_tc = kernel == tn.TN_KERNEL_TZ
     clocks = clk.summary()
     if uses_tc:
         bf16 = peaks.get("bf16_tflops", 1590.0)
@@ -403,17 +425,18 @@ def main():
         t0 = time.perf_counter()
         oracle.conv3d(x0, w0)
         dt0 = time.perf_counter() - t0
-        c2 = synth.CONFIGS["C2"]
-        p2 = synth.fcn_params(c2["seed_params"])
-        v2 = synth.ct_volume(c2["vol_shape"], seed=c2["seeds"][0])
+        cfg2 = synth.CONFIGS["C2"]
+        p2 = synth.fcn_params(cfg2["seed_params"])
+        v2 = synth.ct_volume(cfg2["vol_shape"], seed=cfg2["seeds"][0])
         t0 = time.perf_counter()
         oracle.fcn_forward(v2, p2["t_lo"], p2["t_hi"], p2["weights"], p2["lo"], p2["hi"], p2["pred_w"], p2["pred_b"])
         dt2 = time.perf_counter() - t0
         cpu["other_configs"] = {
             "C0": {"value": 32 * 32 * 32 * 16 * 16 * 27 / dt0 / 1e9, "unit": "GMAC/s", "seconds": dt0},
-            "C2": {"value": int(np.prod(c2["vol_shape"])) / dt2, "unit": "voxels/s", "seconds": dt2,
+            "C2": {"value": int(np.prod(cfg2["vol_shape"])) / dt2, "unit": "voxels/s", "seconds": dt2,
                    "sample": "one whole 96x144x144 volume through the oracle FCN"}}
 
+    assert c2 is None or "ms_per_volume" in c2, "fcn_c2 must be the configs[2] timing"
     if rank == 0:
         line = {
             "metric": "ternary conv3d effective GMAC/s (C1, fused requant)",
@@ -424,10 +447,11 @@ def main():
                        "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
                        "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
                        "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)",
-                                       2: "tcgen05 kind::i8 implicit GEMM, dx taps merged along N (conv_tc)",
                                        3: "tcgen05 kind::i8 implicit GEMM, taps as UMMA descriptor offsets, "
                                           "kernel planes merged along N (conv_tz)"}.get(kernel, "?"),
-                       "l2": "256 MiB buffer zeroed between timed steps, outside the events",
+                       "l2": "256 MiB buffer zeroed between timed steps, outside the events; the 16.8 MB "
+                             "packed output a step leaves dirty in L2 is written back during that zeroing, "
+                             "i.e. outside the events (about 2.6 us at the measured HBM rate)",
                        "parallelism": f"replicas x{world}", "parity": parity},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -449,6 +473,106 @@ def main():
         dist.destroy_process_group()
 
 
+
+# ----------------------------------------------------------------------------- FCN gates + roofline
+FP4_PER_BF16 = 4.0     # nominal dense fp4 (9 PFLOP/s) / bf16 (2.25 PFLOP/s), B200_PROFILING.md
+
+
+def logits_gate(torch, logits, name, p, z0=0, z1=None, dist=None, world=1):
+    """Compare this rank's logits with the oracle's values stored at sampled positions of
+    configs[2]/[3]/[4] (tests/golden/bench_samples.npz, written by tools/make_bench_golden.py
+    from oracle/ only) within reading R13; positions outside [z0, z1) belong to other ranks.
+    Exits (refusing to report) on any mismatch on any rank."""
+    gold = golden()
+    at, ref = gold[f"fcn_{name}_at"], gold[f"fcn_{name}_ref"]
+    z1 = logits.shape[2] + z0 if z1 is None else z1
+    sel = (at[:, 2] >= z0) & (at[:, 2] < z1)
+    ok, checked = True, int(sel.sum())
+    if checked:
+        a = at[sel].astype(np.int64)
+        a[:, 2] -= z0
+        idx = tuple(torch.from_numpy(a[:, j]).to(logits.device) for j in range(5))
+        got = logits[idx].cpu().numpy().astype(np.float64)
+        r = ref[sel].astype(np.float64)
+        j = a[:, 1]
+        scale = np.abs(p["pred_b"]).astype(np.float64)[j] + np.abs(p["pred_w"]).astype(np.float64).sum(1)[j]
+        ok = bool(np.all(np.abs(got - r) <= 1e-5 * np.maximum(np.abs(r), scale)))
+    if world > 1:
+        t = torch.tensor([int(ok), checked], device=logits.device)
+        f = torch.tensor([int(ok)], device=logits.device)
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ok, checked = bool(f.item()), int(t[1].item())
+    if not ok:
+        print(json.dumps({"error": f"FCN {name} logits differ from the oracle; refusing to report"}), flush=True)
+        sys.exit(1)
+    return f"passed ({checked} sampled logits vs the oracle's values, reading R13 tolerance)"
+
+
+def fcn_layer_work(table, shape, nclass):
+    """Per layer of one forward over `shape` (n,1,D,H,W): algorithmic ternary MACs
+    (27 * C_in * C_out per output voxel) and algorithmic HBM bytes (each input segment's packed
+    buffer read once at its own resolution -- the float volume for the first layer -- plus the
+    packed output written once; the last layer writes fp32 logits instead)."""
+    n, _, D, H, W = shape
+    cwb = lambda c: 8 * ((c + 31) // 32)
+    outs, res = [], []
+    for i, (kind, co, s, segs) in enumerate(table):
+        if segs[0][0] < 0:
+            d, h, w, cin, b_in = D, H, W, 1, n * D * H * W * 4
+        else:
+            f = 2 if segs[0][1] else 1
+            d, h, w = (outs[segs[0][0]][a] * f for a in (1, 2, 3))
+            cin = sum(outs[sj][0] for sj, _ in segs)
+            b_in = sum(n * outs[sj][1] * outs[sj][2] * outs[sj][3] * cwb(outs[sj][0]) for sj, _ in segs)
+        do, ho, wo = ((v - 1) // s + 1 for v in (d, h, w))
+        outs.append((co, do, ho, wo))
+        last = i == len(table) - 1
+        b_out = n * do * ho * wo * (4 * nclass if last else cwb(co))
+        res.append({"layer": i + 1, "macs": n * do * ho * wo * co * 27 * cin, "bytes": b_in + b_out})
+    return res
+
+
+def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3):
+    """Per-layer binding roofline of one FCN forward: each layer's bound is the larger of its
+    algorithmic MACs at the fp4 dense tensor peak (4 x measured bf16, the guide's nominal
+    ratio; every layer's ternary products are exact in E2M1) and its algorithmic bytes at the
+    measured HBM bandwidth.  Layers are timed one by one (tn_fcn_forward_range, CUDA events on
+    the launching stream); frac = sum of the bounds / the whole forward's device time."""
+    L = len(net.table)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(L + 1)]
+    ms = np.zeros(L)
+    for _ in range(reps):
+        ev[0].record(stream)
+        for i in range(L):
+            net.forward_range(x, i, i + 1 if i < L - 1 else -1, logits=logits, ws=ws)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        ms += [ev[i].elapsed_time(ev[i + 1]) for i in range(L)]
+    ms /= reps
+    hbm = peaks.get("hbm_gbs", 6548.2) * 1e9
+    mac_peak = FP4_PER_BF16 * peaks.get("bf16_tflops", 1662.6) * 1e12 / 2.0
+    per, bound_ms = [], 0.0
+    for wk, t in zip(fcn_layer_work(net.table, tuple(x.shape), net.nclass), ms):
+        tt, th = wk["macs"] / mac_peak * 1e3, wk["bytes"] / hbm * 1e3
+        b = max(tt, th)
+        bound_ms += b
+        per.append({"layer": wk["layer"], "ms": float(t), "bound_ms": b, "bound": "tensor" if tt >= th else "hbm",
+                    "frac": b / float(t), "gmac": wk["macs"] / 1e9, "mb": wk["bytes"] / 1e6})
+    dom = max(per, key=lambda r: r["ms"])
+    dom_t = dom["bound"] == "tensor"
+    achieved = dom["gmac"] * 1e9 / (dom["ms"] / 1e3) / 1e12 if dom_t else dom["mb"] * 1e6 / (dom["ms"] / 1e3) / 1e9
+    return {"bound": "per-layer max(fp4 tensor, hbm)", "bound_ms": bound_ms, "achieved_ms": forward_ms,
+            "frac": bound_ms / forward_ms, "layers_sum_ms": float(ms.sum()),
+            "dominant": {"layer": dom["layer"], "bound": dom["bound"], "achieved": achieved,
+                         "peak": mac_peak / 1e12 if dom_t else hbm / 1e9,
+                         "unit": "TMAC/s (fp4 dense)" if dom_t else "GB/s", "frac": dom["frac"], "traffic": None},
+            "per_layer": per,
+            "peak_source": "fp4 = 4 x MEASURED_PEAKS.bf16_tflops / 2 MAC; HBM = MEASURED_PEAKS.hbm_gbs",
+            "timing": "layers timed one at a time (tn_fcn_forward_range, events between launches); "
+                      "frac uses the whole forward's time"}
+
+
 def bench_c2(args, tn, torch, dev, stream):
     """configs[2]: one 1x1x96x144x144 CT-like volume through the FCN (device time per volume)."""
     cfg = synth.CONFIGS["C2"]
@@ -458,8 +582,10 @@ def bench_c2(args, tn, torch, dev, stream):
     x = torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][0])).to(dev)
     ws = net.workspace(shape, dev)
     logits = torch.empty((1, 2) + shape[2:], dtype=torch.float32, device=dev)
-    for _ in range(2):
-        net(x, logits=logits, ws=ws)
+    net(x, logits=logits, ws=ws)
+    torch.cuda.synchronize()
+    parity = logits_gate(torch, logits, "c2", p)
+    net(x, logits=logits, ws=ws)
     torch.cuda.synchronize()
     steps = max(3, args.fcn_steps)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -470,9 +596,11 @@ def bench_c2(args, tn, torch, dev, stream):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     vox = int(np.prod(shape[2:]))
+    roof = fcn_roofline(torch, net, x, logits, ws, stream, ms, bench_peaks())
     return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s", "ms_per_volume": ms,
-            "config": "C2: one CT-like volume 1x1x96x144x144 (BASELINE configs[2]); parity at this size in "
-                      "test_fcn_c2_full_size_matches_oracle", "steps": steps}
+            "config": "C2: one CT-like volume 1x1x96x144x144 (BASELINE configs[2]); every layer bit-exact at "
+                      "this size in test_fcn_c2_full_size_matches_oracle", "steps": steps, "parity": parity,
+            "roofline": roof}
 
 
 def bench_c0(args, tn, torch, dev):
@@ -575,12 +703,9 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
     ws = net.workspace(bshape, dev)
     logits = torch.empty((len(mine), 2) + shape[2:], dtype=torch.float32, device=dev)
     net(xb, logits=logits, ws=ws)
-    one = net(xb[:1].contiguous())          # the batched forward equals a single-volume one
     torch.cuda.synchronize()
-    if not torch.equal(one, logits[:1]):
-        print(json.dumps({"error": "batched FCN differs from the single-volume forward"}), flush=True)
-        sys.exit(1)
-    del one
+    # volume 0 (seed 100) is always this rank-0 batch's first volume
+    parity = logits_gate(torch, logits[:1] if rank == 0 else logits[:0], "c3", p, dist=dist, world=world)
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -596,7 +721,9 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
         ms = float(t.item())
     vox = int(np.prod(shape[2:]))
     total_vox = args.fcn_steps * len(cfg["seeds"]) * vox
-    return {"metric": "FCN voxels/s", "value": total_vox / (ms / 1e3), "unit": "voxels/s",
+    roof = fcn_roofline(torch, net, xb, logits, ws, stream, ms / args.fcn_steps, bench_peaks())
+    return {"metric": "FCN voxels/s", "value": total_vox / (ms / 1e3), "unit": "voxels/s", "parity": parity,
+            "roofline": roof,
             "config": "C3: 8 CT-like volumes 1x1x128x256x256 sharded over the ranks (8 / N each), one batched "
                       "forward per rank (BASELINE configs[3])",
             "ms_per_batch": ms / args.fcn_steps, "effective_gmacs": total_vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
@@ -633,6 +760,7 @@ def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
         mode = "whole volume on one GPU"
     run()
     torch.cuda.synchronize()
+    parity = logits_gate(torch, logits, "c4", p, z0=z0, z1=z1, dist=dist, world=world)
     steps = max(2, args.fcn_steps)
     if world > 1:
         dist.barrier()
@@ -673,8 +801,13 @@ def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
             sched[name + "_ms_per_volume"] = a.elapsed_time(b) / steps
         sched["note"] = "bit-identical to the whole-volume logits (checked before timing)"
         del wsl
-    return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s",
-            "slab_schedules_1gpu": sched,
+    roof = None
+    if world == 1:
+        wsr = net.workspace(shape, dev)
+        roof = fcn_roofline(torch, net, x, logits, wsr, stream, ms, bench_peaks())
+        del wsr
+    return {"metric": "FCN voxels/s", "value": vox / (ms / 1e3), "unit": "voxels/s", "parity": parity,
+            "roofline": roof, "slab_schedules_1gpu": sched,
             "config": f"C4: one CT-like volume 1x1x{D}x{H}x{W} (BASELINE configs[4]); {mode}",
             "ms_per_volume": ms, "effective_gmacs": vox * FCN_MACS_PER_VOXEL / (ms / 1e3) / 1e9,
             "steps": steps, "scaling": "strong (fixed volume)"}

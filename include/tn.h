@@ -171,6 +171,13 @@ size_t    tn_fcn_workspace_bytes(const tn_fcn* net, tn_dims xd);
 tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
                          size_t ws_bytes, int64_t* d_bad, tn_stream stream);
 void      tn_fcn_destroy(tn_fcn* net);
+/* The layers [first, last) of tn_fcn_forward only (last = -1: to the end; the
+ * prediction runs with the last layer), reading earlier layers' outputs from ws.
+ * Calling it for consecutive ranges on one stream is tn_fcn_forward; used to time
+ * layers individually.  TN_EINVAL if the range is outside the table.          */
+tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
+                               size_t ws_bytes, int64_t* d_bad, int32_t first, int32_t last,
+                               tn_stream stream);
 
 /* Internal-activation access for debugging and per-layer parity: after a
  * tn_fcn_forward on the same ws, returns the device pointer and dims of layer
@@ -284,16 +291,17 @@ tn_status tn_fold_thresholds(const float* alpha, const float* gamma, const float
                              int8_t* negate);
 
 /* Kernel selection for the ternary conv (all exact; parity tests run each).
- *   TN_KERNEL_POPC  CUDA-core XOR/AND/POPC form of Eq. 9 (any geometry)
- *   TN_KERNEL_TC    tcgen05 kind::i8, dx taps merged along N (stride 1, C <= 64)
- *   TN_KERNEL_TZ    tcgen05, taps as descriptor offsets and the three kernel
- *                   planes merged along N (stride 1/2, C <= 64, small 27*C*K
- *                   filter bank; W even); ternary operands as FP4 E2M1
- *                   (kind::mxf4, unit block scales: exact) where they fit, else
- *                   int8 (kind::i8)
+ *   TN_KERNEL_POPC  CUDA-core XOR/AND/POPC form of Eq. 9 (any geometry): the
+ *                   paper's own method, and the fallback for shapes outside TZ
+ *   TN_KERNEL_TZ    the tcgen05 kernel: taps as descriptor offsets and the three
+ *                   kernel planes merged along N (stride 1/2, pad 1, C <= 64 per
+ *                   launch in 16-channel chunks, K in {16, 32, 64}, small 27*C*K
+ *                   filter bank); ternary operands as FP4 E2M1 (kind::mxf4,
+ *                   unit block scales: exact) where they fit, else int8 (kind::i8)
  *   TN_KERNEL_TZ8   like AUTO, with the TZ kernel restricted to int8 operands
- * TN_KERNEL_AUTO picks TZ, else TC, else POPC per shape.  Host, process-wide. */
-enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TC = 2, TN_KERNEL_TZ = 3, TN_KERNEL_TZ8 = 4 };
+ * TN_KERNEL_AUTO picks TZ, else POPC per shape.  Host, process-wide.  (Value 2,
+ * a retired second tensor-core kernel, is rejected with TN_EINVAL.)           */
+enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TZ = 3, TN_KERNEL_TZ8 = 4 };
 tn_status tn_set_conv_kernel(int32_t which);
 int32_t   tn_get_conv_kernel(void);
 /* Upper bound on the CTAs of the persistent tensor-core conv grids (0 = one per
@@ -301,7 +309,7 @@ int32_t   tn_get_conv_kernel(void);
  * small cap to give each CTA long runs of output planes.  Host, process-wide;
  * TN_EINVAL if max_ctas < 0.                                                  */
 tn_status tn_set_grid_cap(int32_t max_ctas);
-/* Which kernel (TN_KERNEL_POPC, _TC or _TZ) a tn_conv3d_seg call with these
+/* Which kernel (TN_KERNEL_POPC or _TZ) a tn_conv3d_seg call with these
  * arguments would run under the current selection; -1 if the call is invalid
  * (or a forced tensor-core kernel does not cover the shape).  Host only.      */
 int32_t   tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);

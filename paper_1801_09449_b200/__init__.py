@@ -23,7 +23,7 @@ INT64_MAX = (1 << 63) - 1
 
 TN_OK, TN_EINVAL, TN_ESHAPE, TN_EALIGN, TN_EUNSUPPORTED, TN_EDOMAIN, TN_ECUDA, TN_ENCCL = range(8)
 TN_LAYER_FIRST, TN_LAYER_CONV = 1, 2
-TN_KERNEL_AUTO, TN_KERNEL_POPC, TN_KERNEL_TC, TN_KERNEL_TZ, TN_KERNEL_TZ8 = 0, 1, 2, 3, 4
+TN_KERNEL_AUTO, TN_KERNEL_POPC, TN_KERNEL_TZ, TN_KERNEL_TZ8 = 0, 1, 3, 4
 _STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ESHAPE", 3: "TN_EALIGN", 4: "TN_EUNSUPPORTED",
            5: "TN_EDOMAIN", 6: "TN_ECUDA", 7: "TN_ENCCL"}
 
@@ -87,6 +87,7 @@ SIGNATURES = {
     "tn_fcn_workspace_bytes": (_SZ, [_P, _D]),
     "tn_fcn_forward": (ctypes.c_int, [_P, _P, _D, _P, _P, _SZ, _P, _P]),
     "tn_fcn_destroy": (None, [_P]),
+    "tn_fcn_forward_range": (ctypes.c_int, [_P, _P, _D, _P, _P, _SZ, _P, _I32, _I32, _P]),
     "tn_fcn_layer_output": (_P, [_P, _D, _P, _I32, ctypes.POINTER(_D)]),
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
     "tn_get_conv_kernel": (_I32, []),
@@ -443,6 +444,17 @@ class TernaryFCN:
         return logits
 
     __call__ = forward
+
+    def forward_range(self, x, first, last, logits=None, ws=None, d_bad=None, stream=None):
+        """Layers [first, last) of forward() only (last = -1: to the end, with the prediction)."""
+        xd = dims_of(x)
+        if ws is None:
+            ws = self.workspace(x.shape, x.device)
+        if logits is None:
+            logits = torch.empty((xd.n, self.nclass, xd.d, xd.h, xd.w), dtype=torch.float32, device=x.device)
+        _check(lib.tn_fcn_forward_range(self.handle, _ptr(x), xd, _ptr(logits), _ptr(ws), ws.numel(), _ptr(d_bad),
+                                        int(first), int(last), _stream(stream)), "tn_fcn_forward_range")
+        return logits
 
     def slab_plan(self, global_shape, z0, z1):
         """Per-layer slab geometry from the library's planner (host only)."""

@@ -1,7 +1,7 @@
 // api.cu -- the C ABI of libtn.so (include/tn.h): host-side validation, error
 // text, descriptor construction and kernel selection.  No compute happens here;
 // every step of the path runs in the kernels of pack.cu / conv_popc.cu /
-// conv_tc.cu / conv_tz.cu.
+// conv_tz.cu.
 #include "tn_internal.cuh"
 
 #include <cstdarg>
@@ -176,46 +176,16 @@ tn_status tn_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int3
 
 namespace tn {
 
-// Shared by tn_conv3d / tn_conv3d_requant / tn_conv3d_seg and the FCN driver.
-// Two-segment conv whose concatenated channels exceed the tensor-core kernel's
-// resident filter bank (e.g. the FCN's 64+64 -> 64 decoder block): pass 1 =
-// segment 0 into int32 partial sums (scratch), pass 2 = segment 1 plus the
-// partials through the epilogue.  Returns false if the split does not apply.
-static bool split_tc_possible(const ConvDesc& cd) {
-    if (cd.nseg != 2 || cd.y_in != nullptr || conv_tc_supported(cd)) return false;
-    ConvDesc a = cd, b = cd;
-    a.nseg = 1; a.yp = nullptr; a.y = reinterpret_cast<int32_t*>(16); a.logits = nullptr;
-    b.nseg = 1; b.seg[0] = cd.seg[1]; b.y_in = reinterpret_cast<const int32_t*>(16);
-    return conv_tc_supported(a) && conv_tc_supported(b);
-}
-
-tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch) {
-    if (scratch != nullptr && (g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TC) &&
-        !(g_conv_kernel == TN_KERNEL_AUTO && conv_tz_supported(cd, true)) && split_tc_possible(cd)) {
-        ConvDesc a = cd, b = cd;
-        a.nseg = 1; a.yp = nullptr; a.y = scratch; a.logits = nullptr; a.lo = a.hi = nullptr;
-        a.halo_lo = a.halo_hi = nullptr;
-        tn_status s1 = cuda_status(launch_conv_tc(a, st), where);
-        if (s1 != TN_OK) return s1;
-        b.nseg = 1; b.seg[0] = cd.seg[1]; b.y_in = scratch;
-        return run_conv(b, st, where);
-    }
-    return run_conv(cd, st, where);
-}
-
 // Kernel choice for one conv launch under the process-wide selector:
-// TN_KERNEL_TZ (tap-offset z-merged tensor-core kernel, small C*K), then
-// TN_KERNEL_TC (dx-merged tensor-core kernel), then the CUDA-core popc kernel;
+// TN_KERNEL_TZ (the tcgen05 tap-offset z-merged kernel) where it covers the
+// shape, else the CUDA-core popc kernel (Eq. 9 as XOR/AND/POPC: any geometry);
 // a forced selector only takes its own kernel.  -1 if nothing covers the shape.
 static int pick_kernel(const ConvDesc& cd, int mode) {
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ || mode == TN_KERNEL_TZ8) &&
         conv_tz_supported(cd, mode != TN_KERNEL_TZ8))
         return TN_KERNEL_TZ;
     // TZ8 = AUTO with int8 TZ operands (falls back like AUTO)
-    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TC || mode == TN_KERNEL_TZ8) && conv_tc_supported(cd))
-        return TN_KERNEL_TC;
-    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC || mode == TN_KERNEL_TZ8) && cd.y_in == nullptr &&
-        cd.logits == nullptr)
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC || mode == TN_KERNEL_TZ8) && cd.logits == nullptr)
         return TN_KERNEL_POPC;
     return -1;
 }
@@ -223,7 +193,6 @@ static int pick_kernel(const ConvDesc& cd, int mode) {
 static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st) {
     switch (kernel) {
         case TN_KERNEL_TZ: return launch_conv_tz(cd, st, g_conv_kernel != TN_KERNEL_TZ8);
-        case TN_KERNEL_TC: return launch_conv_tc(cd, st);
         case TN_KERNEL_POPC: return launch_conv_popc(cd, st);
     }
     return cudaErrorNotSupported;
@@ -232,12 +201,10 @@ static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
     if (cd.N == 0 || cd.Do == 0 || cd.Ho == 0 || cd.Wo == 0) return TN_OK;
     const int mode = g_conv_kernel;
-    if (cd.y_in != nullptr && pick_kernel(cd, mode) != TN_KERNEL_TC)
-        return fail(TN_EUNSUPPORTED, "%s: partial-sum input needs the tcgen05 (TC) kernel", where);
     if (cd.logits != nullptr) {
-        // fused prediction in a tensor-core epilogue; otherwise conv + predict kernel
+        // fused prediction in the tensor-core epilogue; otherwise conv + predict kernel
         const int kf = pick_kernel(cd, mode);
-        if (kf == TN_KERNEL_TZ || kf == TN_KERNEL_TC) return cuda_status(launch_kernel(kf, cd, st), where);
+        if (kf == TN_KERNEL_TZ) return cuda_status(launch_kernel(kf, cd, st), where);
         ConvDesc c2 = cd;
         c2.logits = nullptr;
         c2.no_yp = 0;   // the predict kernel reads the packed output
@@ -376,7 +343,7 @@ tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float
 }
 
 tn_status tn_set_conv_kernel(int32_t which) {
-    if (which < TN_KERNEL_AUTO || which > TN_KERNEL_TZ8)
+    if (which != TN_KERNEL_AUTO && which != TN_KERNEL_POPC && which != TN_KERNEL_TZ && which != TN_KERNEL_TZ8)
         return fail(TN_EINVAL, "unknown kernel selector %d", which);
     g_conv_kernel = which;
     return TN_OK;

@@ -2,7 +2,7 @@
 // into the UMMA descriptors ("tap-offset") and the three kernel planes dz merged
 // along N ("z-merged").  Written for the layers with few channels (C, K <= 64,
 // 27*C*K small enough for the filter bank to sit in shared memory three times
-// over), where the dx-merged kernel (conv_tc.cu) is limited by issue slots.
+// over) -- every tensor-core shape of the library.
 //
 // The arithmetic is the same integer as Eq. 9: int8 products
 // of ternary values {-1,0,+1} accumulated exactly in int32, over the 3x3x3
@@ -487,8 +487,27 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             src[sg] = reinterpret_cast<const uint32_t*>(
                                 cd.xf + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W);
                         } else {
-                            bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 8u * sd.cw : 0u;
-                            src[sg] = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw;
+                            // rows of 8*cw bytes: with cw = 1 and an odd W the range may start or end
+                            // 8 bytes off a 16-byte boundary.  Copy the aligned superset (the
+                            // expanders skip the 8-byte head); if its last 16 bytes would cross the
+                            // end of the buffer, those 8 valid bytes take a plain load instead.
+                            const uint32_t* sp0 =
+                                sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw;
+                            const uint32_t head = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(sp0)) & 15u;
+                            src[sg] = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(sp0) - head);
+                            bytes[sg] = 0u;
+                            if (ok) {
+                                const uint32_t nb = static_cast<uint32_t>(nr[sg]) * sd.W * 8u * sd.cw;
+                                uint32_t al = (head + nb + 15u) & ~15u;
+                                const char* buf_end = reinterpret_cast<const char*>(sd.xp) +
+                                                      static_cast<int64_t>(cd.N) * sd.D * sd.H * sd.W * 8 * sd.cw;
+                                if (reinterpret_cast<const char*>(src[sg]) + al > buf_end) {
+                                    al -= 16u;
+                                    *reinterpret_cast<uint2*>(s_stage + st * pl.stage_bytes + pl.seg_off[sg] + al) =
+                                        *reinterpret_cast<const uint2*>(buf_end - 8);
+                                }
+                                bytes[sg] = al;
+                            }
                         }
                         total += bytes[sg];
                     }
@@ -535,11 +554,14 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 ++e_planes;
 #endif
                 bool zok[kMaxSeg];
+                uint32_t head[kMaxSeg];    // the loader's 16-byte alignment head of each segment's rows
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) {
                     const SegDesc& sd = cd.seg[sg];
                     const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
                     zok[sg] = zs >= 0 && zs < sd.D;
+                    head[sg] = FIRST ? 0u : static_cast<uint32_t>(reinterpret_cast<uintptr_t>(
+                        sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw)) & 15u;
                 }
                 const uint8_t* stg = s_stage + st * pl.stage_bytes;
                 uint8_t* slot = s_a + as * pl.slot_bytes;
@@ -608,7 +630,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 // (packed 16 channels and FP4 16 channels are both 8 bytes).
                 const bool up_conv = NSEG == 2 && cd.seg[0].c == 16;
                 if (up_conv) {
-                    uint2* p0 = reinterpret_cast<uint2*>(const_cast<uint8_t*>(stg) + pl.seg_off[0]);
+                    uint2* p0 = reinterpret_cast<uint2*>(const_cast<uint8_t*>(stg) + pl.seg_off[0] + head[0]);
                     const int nv = nr[0] * cd.seg[0].W;
                     for (int e = et; e < nv; e += kZExpThreads) {
                         const uint2 w = p0[e];
@@ -637,7 +659,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const bool up = sg == 0 && kUp0;
                             const int ys = up ? (yi >> 1) : yi, xs = up ? (xi >> 1) : xi;
                             const bool ok = v && zok[sg];
-                            const uint8_t* sp = stg + pl.seg_off[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
+                            const uint8_t* sp = stg + pl.seg_off[sg] + head[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
                             uint8_t* rb = slot + (ph * pl.nreg + pl.reg0[sg]) * pl.REG + 16 + r * 16;
                             if (sd.c == 16) {
                                 uint2 w = make_uint2(0u, 0u);
@@ -689,7 +711,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const bool up = sg == 0 && kUp0;
                             const int ys = up ? (yi >> 1) : yi, xs = up ? (xi >> 1) : xi;
                             const bool ok = v && zok[sg];
-                            const uint8_t* sp = stg + pl.seg_off[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
+                            const uint8_t* sp = stg + pl.seg_off[sg] + head[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
                             const int choff = sg ? pl.cch[0] : 0;
                             if (sd.cw == 1) {
                                 uint2 w = make_uint2(0u, 0u);
@@ -1125,7 +1147,7 @@ static int tz_num_sms() {
 
 static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 = false) {
     constexpr size_t kSmemMax = 227 * 1024;
-    if (cd.nseg < 1 || cd.nseg > 2 || cd.y_in != nullptr) return false;
+    if (cd.nseg < 1 || cd.nseg > 2) return false;
     for (int a = 0; a < 3; ++a)
         if (cd.s[a] != cd.s[0] || cd.p[a] != 1 || cd.dl[a] != 1) return false;
     pl.s = cd.s[0];
@@ -1140,7 +1162,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.cch[1] = 0;
     for (int i = 0; i < cd.nseg && !first; ++i) {
         const SegDesc& sd = cd.seg[i];
-        if (sd.c <= 0 || sd.c % 16 != 0 || (sd.c + 31) / 32 != sd.cw || sd.W % 2 != 0) return false;
+        if (sd.c <= 0 || sd.c % 16 != 0 || (sd.c + 31) / 32 != sd.cw) return false;
         if ((reinterpret_cast<uintptr_t>(sd.xp) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
         pl.cch[i] = sd.c / 16;
         ct += pl.cch[i];
@@ -1289,7 +1311,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                 maxr = std::max(maxr, yhi - ylo + 1);
             }
             pl.seg_off[sg] = off;
-            off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw), 128);
+            off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw) + (first ? 0 : 16), 128);   // + alignment head
             if (first) {   // ternary code planes: maxr + 2 rows of W + 8 bytes (4 zero columns each side)
                 pl.code_pitch = sd.W + 8;
                 pl.code_bytes = round_up((maxr + 2) * pl.code_pitch, 128);
@@ -1355,9 +1377,9 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     if (pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                       \
         kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, true>                      \
                     : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, true>;
-    TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(4, 1, 1)
+    TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(3, 1, 1) TZ_PICK(4, 1, 1)
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
-    TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(4, 1, 2)
+    TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(3, 1, 2) TZ_PICK(4, 1, 2)
     TZ_PICK4(1, 1, 1) TZ_PICK4(2, 1, 1) TZ_PICK4(4, 1, 1)
     TZ_PICK4(2, 2, 1) TZ_PICK4(4, 2, 1) if (K == 64) { TZ_PICK4(8, 2, 1) }
     TZ_PICK4(1, 1, 2) TZ_PICK4(2, 1, 2) TZ_PICK4(4, 1, 2)
@@ -1378,12 +1400,15 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
 
 static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
     int ct = 0;
-    for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
-    if (pl.f4 && cd.nseg == 2 && ct == 3) return false;
+    for (int i = 0; i < cd.nseg; ++i) {
+        ct += pl.cch[i];
+        // FP4 rows hold 16 channels (two positions) or whole 32-channel groups
+        if (pl.f4 && cd.seg[i].c != 16 && cd.seg[i].c % 32 != 0) return false;
+    }
+    if (pl.f4 && ct == 3) return false;
     if (ct == 8) return pl.f4 && cd.K == 64 && pl.s == 1 && cd.nseg == 2;
-    if (pl.s == 2) return cd.nseg == 1 && (ct == 1 || ct == 2 || ct == 4);
-    if (cd.nseg == 1) return ct == 1 || ct == 2 || ct == 4;
-    return ct >= 2;
+    if (cd.nseg == 1) return ct >= 1 && ct <= 4;
+    return pl.s == 1 && ct >= 2;
 }
 
 static ConvDesc first_desc(const FirstDesc& fd) {

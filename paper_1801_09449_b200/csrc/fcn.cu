@@ -33,7 +33,7 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
                size_t* scratch_off) {
     const int L = static_cast<int>(net->layers.size());
     P.assign(L, LayerPlan{});
-    size_t off = 0, scratch = 0;
+    size_t off = 0;
     for (int i = 0; i < L; ++i) {
         const tn_layer& ly = net->layers[i];
         int d, h, w;
@@ -63,11 +63,9 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
         P[i].off = off;
         P[i].bytes = tn_packed_bytes(o);
         off = align_up(off + P[i].bytes);
-        if (ly.nseg == 2 && net->cin[0][i] + net->cin[1][i] > 64)   // split over two tensor-core passes
-            scratch = std::max(scratch, static_cast<size_t>(o.n) * o.d * o.h * o.w * o.c * 4);
     }
     *scratch_off = off;
-    *total = align_up(off + scratch);
+    *total = align_up(off);
     return TN_OK;
 }
 
@@ -154,7 +152,18 @@ const uint32_t* tn_fcn_layer_output(const tn_fcn* net, tn_dims xd, const void* w
 
 tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
                          size_t ws_bytes, int64_t* d_bad, tn_stream stream) {
+    return tn_fcn_forward_range(net, x, xd, logits, ws, ws_bytes, d_bad, 0, -1, stream);
+}
+
+tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
+                               size_t ws_bytes, int64_t* d_bad, int32_t first, int32_t last, tn_stream stream) {
     if (net == nullptr) { set_error("net is NULL"); return TN_EINVAL; }
+    const int nl = static_cast<int>(net->layers.size());
+    if (last < 0) last = nl;
+    if (first < 0 || first > last || last > nl) {
+        set_error("layer range [%d, %d) outside [0, %d)", first, last, nl);
+        return TN_EINVAL;
+    }
     if (xd.c != 1) { set_error("FCN input must have c == 1 (got %d)", xd.c); return TN_ESHAPE; }
     if (xd.n < 1 || xd.d < 1 || xd.h < 1 || xd.w < 1) { set_error("FCN input must be non-empty"); return TN_ESHAPE; }
     std::vector<LayerPlan> P;
@@ -175,7 +184,7 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     char* base = static_cast<char*>(ws);
     const int L = static_cast<int>(net->layers.size());
-    for (int i = 0; i < L; ++i) {
+    for (int i = first; i < last; ++i) {
         const tn_layer& ly = net->layers[i];
         uint32_t* outp = reinterpret_cast<uint32_t*>(base + P[i].off);
         const tn_dims& o = P[i].out;
@@ -222,10 +231,10 @@ tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* l
             cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
             cd.no_yp = 1;   // fused prediction: the last layer's packed codes are not stored
         }
-        st = run_conv_scratch(cd, s, "tn_fcn_forward", reinterpret_cast<int32_t*>(base + soff));
+        st = run_conv(cd, s, "tn_fcn_forward");
         if (st != TN_OK) return st;
     }
-    if (net->layers[L - 1].kind == TN_LAYER_FIRST || TN_EXP_NOFUSEPRED) {
+    if (last == L && (net->layers[L - 1].kind == TN_LAYER_FIRST || TN_EXP_NOFUSEPRED)) {
         const LayerPlan& last = P[L - 1];
         cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(base + last.off), last.out,
                                        net->pred_w, net->pred_b, net->nclass, logits, s);

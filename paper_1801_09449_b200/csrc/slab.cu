@@ -42,7 +42,6 @@ struct SlabPlan {
     int z0, z1;
     size_t x_off, x_bytes, x_plane;          // extended float input [z0-1, z1+1)
     std::vector<tn_slab_layer> L;
-    size_t scratch_off;      // int32 partial sums for split two-segment blocks
     size_t total;
 };
 
@@ -78,7 +77,7 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
     sp.x_plane = static_cast<size_t>(g.h) * g.w * sizeof(float);
     sp.x_off = 0;
     sp.x_bytes = sp.x_plane * (z1 - z0 + 2);
-    size_t off = align_up(sp.x_bytes), scratch = 0;
+    size_t off = align_up(sp.x_bytes);
     sp.L.assign(nl, tn_slab_layer{});
     for (int i = 0; i < nl; ++i) {
         tn_slab_layer& s = sp.L[i];
@@ -91,11 +90,8 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
         s.plane_bytes = static_cast<int64_t>(s.h) * s.w * 2 * ((s.c + 31) / 32) * 4;
         s.offset = static_cast<int64_t>(off);
         off = align_up(off + static_cast<size_t>(s.plane_bytes) * (s.z1 - s.z0 + 2));
-        if (net->layers[i].nseg == 2 && net->cin[0][i] + net->cin[1][i] > 64)
-            scratch = std::max(scratch, static_cast<size_t>(s.z1 - s.z0) * s.h * s.w * s.c * 4);
     }
-    sp.scratch_off = off;
-    sp.total = align_up(off + scratch);
+    sp.total = align_up(off);
     return TN_OK;
 }
 
@@ -152,7 +148,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
                 cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
                 cd.no_yp = 1;
             }
-            tn_status st = run_conv_scratch(cd, s, "slab conv", reinterpret_cast<int32_t*>(ws + sp.scratch_off));
+            tn_status st = run_conv(cd, s, "slab conv");
             if (st != TN_OK) return st;
         }
     }

@@ -40,8 +40,6 @@ struct ConvDesc {
     // outputs: exactly one of y / yp
     int32_t* y;                   // int32 channel-last [N][Do][Ho][Wo][K]
     uint32_t* yp;                 // packed [N][Do][Ho][Wo][2][cwo]
-    const int32_t* y_in;          // optional int32 partial sums [N][Do][Ho][Wo][K] added before the
-                                  // epilogue (tensor-core kernel; split-channel convs)
     const int32_t* lo;
     const int32_t* hi;
     int cwo;
@@ -114,12 +112,9 @@ cudaError_t launch_bad_init(int64_t* d_bad, cudaStream_t s);
 cudaError_t launch_conv_popc(const ConvDesc& cd, cudaStream_t s);
 cudaError_t launch_conv_first(const FirstDesc& fd, cudaStream_t s);
 
-// tcgen05 implicit-GEMM path; returns cudaErrorNotSupported if the shape is
-// outside what the kernel handles (caller then uses the popc kernel).
-bool        conv_tc_supported(const ConvDesc& cd);
-cudaError_t launch_conv_tc(const ConvDesc& cd, cudaStream_t s);
 // tcgen05 tap-offset, z-merged implicit GEMM (conv_tz.cu): C, K <= 64 with a
-// small filter bank; same contract.
+// small filter bank; returns cudaErrorNotSupported if the shape is outside what
+// the kernel handles (the caller then uses the popc kernel).
 // allow_f4: may use FP4 E2M1 operands (kind::mxf4; exact, twice the int8 rate).
 bool        conv_tz_supported(const ConvDesc& cd, bool allow_f4 = true);
 bool        conv_tz_uses_f4(const ConvDesc& cd, bool allow_f4 = true);
@@ -148,10 +143,8 @@ struct tn_fcn {
 
 namespace tn {
 
-// Conv dispatch (api.cu): kernel selection; the _scratch variant may split a
-// two-segment conv into two tensor-core passes through int32 partial sums.
+// Conv dispatch (api.cu): kernel selection and launch.
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where);
-tn_status run_conv_scratch(ConvDesc& cd, cudaStream_t st, const char* where, int32_t* scratch);
 
 // Host-side error text.
 void set_error(const char* fmt, ...);

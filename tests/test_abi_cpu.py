@@ -89,7 +89,6 @@ def test_fcn_create_validation_and_workspace(tn):
     # packed bytes/voxel: 8 for c <= 32, 16 for c = 64.  R0: #1 #2 #13 #14; R1: #3 #4 #11 #12;
     # R2: #5 (32) #6 (64) #9 (64) #10 (32); R3: #7 #8 (64)
     expect = 8 * R0 * 4 + 8 * (R0 // 8) * 4 + 48 * (R0 // 64) + 32 * (R0 // 512)
-    expect += (R0 // 64) * 64 * 4   # int32 partial sums of the split 64+64 -> 64 block (#9)
     assert abs(ws - expect) < 256 * 16
     tn.lib.tn_fcn_destroy(h)
     # a forward reference is rejected
@@ -105,10 +104,11 @@ def test_fcn_macs_per_voxel_matches_survey(tn):
 
 def test_kernel_selection_host_logic(tn):
     """The per-shape kernel choice is host logic (no GPU): every configs[3] FCN layer and C1 run
-    on the tap-offset tensor-core kernel (TZ); shapes outside it fall back to TC or popc."""
+    on the tap-offset tensor-core kernel (TZ); shapes outside it fall back to popc.  There is one
+    tensor-core kernel: the retired dx-merged selector (2) is rejected."""
     d = tn.dims
     R0, R1, R2, R3 = (128, 256, 256), (64, 128, 128), (32, 64, 64), (16, 32, 32)
-    tz, tc, popc = tn.TN_KERNEL_TZ, tn.TN_KERNEL_TC, tn.TN_KERNEL_POPC
+    tz, popc = tn.TN_KERNEL_TZ, tn.TN_KERNEL_POPC
     cases = [  # (segment dims, upsample flags, k, geom, expected)
         ([d(1, 64, 64, 128, 128)], None, 64, tn.geom(), tz),              # C1
         ([d(1, 16, *R0)], None, 16, tn.geom(), tz),                        # #2 / #14
@@ -118,19 +118,22 @@ def test_kernel_selection_host_logic(tn):
         ([d(1, 64, *R2)], None, 64, tn.geom(2), tz),                       # #7 (FP4 operands)
         ([d(1, 64, *R3), d(1, 64, *R2)], [1, 0], 64, tn.geom(), tz),       # #9 (FP4, one pass)
         ([d(1, 16, *R1), d(1, 16, *R0)], [1, 0], 16, tn.geom(), tz),       # #13
-        ([d(1, 16, 9, 17, 35)], None, 16, tn.geom(), tc),                  # odd W: no 1-D bulk rows
+        ([d(1, 16, 9, 17, 35)], None, 16, tn.geom(), tz),                  # odd W: aligned bulk rows
+        ([d(1, 48, 9, 17, 35)], None, 32, tn.geom(), tz),                  # three 16-channel chunks
+        ([d(1, 64, *R2)], None, 64, tn.geom(2), tz),                       # #7
         ([d(1, 16, 11, 12, 13)], None, 16, tn.geom(1, 2, 2), popc),        # dilation 2
         ([d(1, 33, 6, 7, 8)], None, 5, tn.geom(), popc),                   # ragged C, K = 5
     ]
     for segs, up, k, g, want in cases:
         assert tn.tn_conv_kernel_for(segs, k, g, up) == want, (segs[0].c, k, want)
     # forced selectors answer for their own kernel only
-    tn.tn_set_conv_kernel(tn.TN_KERNEL_TC)
+    tn.tn_set_conv_kernel(tn.TN_KERNEL_TZ)
     try:
-        assert tn.tn_conv_kernel_for([d(1, 64, 64, 128, 128)], 64, tn.geom()) == tc
-        assert tn.tn_conv_kernel_for([d(1, 16, 11, 12, 13)], 16, tn.geom(1, 2, 2)) == -1
+        assert tn.tn_conv_kernel_for([d(1, 64, 64, 128, 128)], 64, tn.geom()) == tz
+        assert tn.tn_conv_kernel_for([d(1, 33, 6, 7, 8)], 5, tn.geom()) == -1
     finally:
         tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
+    assert tn.lib.tn_set_conv_kernel(2) == tn.TN_EINVAL
     assert tn.lib.tn_set_grid_cap(-1) == tn.TN_EINVAL
     assert tn.lib.tn_set_grid_cap(0) == tn.TN_OK
 

@@ -24,10 +24,10 @@ def tn():
     return tn
 
 
-SELECTORS = {"popc": 1, "tc": 2, "tz": 3, "tz8": 4, "auto": 0, "tz_cap3": 3, "tz8_cap3": 4, "tc_cap3": 2}
+SELECTORS = {"popc": 1, "tz": 3, "tz8": 4, "auto": 0, "tz_cap3": 3, "tz8_cap3": 4}
 
 
-@pytest.fixture(params=["popc", "tc", "tz", "tz8", "auto", "tz_cap3", "tz8_cap3", "tc_cap3"])
+@pytest.fixture(params=["popc", "tz", "tz8", "auto", "tz_cap3", "tz8_cap3"])
 def kernel(request, tn):
     """Run a conv test with the CUDA-core popc kernel, one of the tcgen05 kernels
     (tz = FP4 operands where they fit, tz8 = int8 operands; skipped for shapes a
@@ -41,9 +41,9 @@ def kernel(request, tn):
     tn.tn_set_grid_cap(0)
 
 
-@pytest.fixture(params=["popc", "tc", "tz8", "auto", "auto_cap5"])
+@pytest.fixture(params=["popc", "tz8", "auto", "auto_cap5"])
 def fcn_kernel(request, tn):
-    tn.tn_set_conv_kernel({"popc": 1, "tc": 2, "tz8": 4, "auto": 0, "auto_cap5": 0}[request.param])
+    tn.tn_set_conv_kernel({"popc": 1, "tz8": 4, "auto": 0, "auto_cap5": 0}[request.param])
     tn.tn_set_grid_cap(5 if request.param.endswith("cap5") else 0)
     yield request.param
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
@@ -55,7 +55,7 @@ def run_or_skip(kernel, fn, *a, **kw):
     try:
         return fn(*a, **kw)
     except tn.TNError as e:
-        if kernel.startswith(("tc", "tz")) and e.status == tn.TN_EUNSUPPORTED:
+        if kernel.startswith("tz") and e.status == tn.TN_EUNSUPPORTED:
             pytest.skip("shape outside this tcgen05 kernel")
         raise
 
@@ -162,6 +162,11 @@ CONV_CASES = [
     ((1, 16, 3, 130, 140), 16, 1, 1, 1),         # several strips per plane
     ((1, 64, 11, 20, 30), 64, 1, 1, 1),          # C = K = 64: four TMEM blocks, wrap-split MMAs
     ((2, 64, 6, 9, 128), 64, 1, 1, 1),
+    # odd W on TZ: 16-byte-aligned supersets of the packed rows (8 bytes per voxel)
+    ((1, 16, 3, 5, 7), 16, 1, 1, 1),             # odd voxel count: the last 8 bytes take a plain load
+    ((2, 32, 4, 6, 9), 32, 1, 1, 1),
+    ((1, 48, 5, 6, 11), 16, 1, 1, 1),            # three 16-channel chunks
+    ((1, 16, 4, 70, 131), 16, 1, 1, 1),          # several strips, odd rows
 ]
 
 
@@ -483,36 +488,51 @@ def test_fcn_full_size_cropped_oracle(tn, cfg_name, origin):
         np.testing.assert_array_equal(net.forward_slabs_local_p2p(xd, 8).cpu().numpy(), got.cpu().numpy())
 
 
+def test_fcn_c3_full_volume_every_layer(tn):
+    """configs[3] at full size in the bench's launch configuration (one batched forward of all 8
+    CT-like volumes 128x256x256): volume 0 is compared WHOLE against the oracle's forward of the
+    same volume -- every stored layer's packed words bit for bit, and the logits within R13 (the
+    last layer's codes feed only the fused prediction and are checked through the logits)."""
+    cfg = synth.CONFIGS["C3"]
+    shape = cfg["vol_shape"]
+    p = synth.fcn_params(cfg["seed_params"])
+    vols = [synth.ct_volume(shape, seed=s) for s in cfg["seeds"]]
+    xb = np.concatenate(vols, 0)
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
+    ws = net.workspace(xb.shape)
+    flag = tn.bad_flag()
+    logits = net(dev(xb), ws=ws, d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    got_layers = [u32(net.layer_output(xb.shape, ws, i)[0][:1]) for i in range(13)]
+    got_logits = logits[:1].cpu().numpy()
+    del ws, logits
+    ref_logits, acts, bad = oracle.fcn_forward(vols[0], p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"],
+                                               p["pred_w"], p["pred_b"], want_acts=True)
+    assert bad == -1
+    for i in range(13):
+        ref, _ = oracle.pack(acts[i])
+        np.testing.assert_array_equal(got_layers[i], ref, err_msg=f"layer #{i + 1}")
+    tol = np.maximum(np.abs(ref_logits), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(got_logits - ref_logits) <= tol)
+
+
 # --------------------------------------------------------------------------- C1 at full size
-def test_c1_full_size_sampled(tn):
-    """configs[1] (1x64x64x128x128, K=64, fused requant) in the bench's launch
-    configuration; 4096 sampled outputs against the oracle's per-output sum, and the
-    canonical-form property on every output word."""
+def test_c1_full_size(tn):
+    """configs[1] (1x64x64x128x128, K=64, fused requant) in the bench's launch configuration,
+    compared WHOLE against the oracle: all 67.1 M int32 accumulators (tn_conv3d) and every
+    packed output word (tn_conv3d_requant) against oracle.conv3d / requant / pack."""
     x, w, lo, hi = synth.conv_config("C1")
     xp = tn.tn_pack_i8(dev(x))
     wp = tn.tn_pack_weights(dev(w))
     xd = tn.dims(*x.shape)
     yp = u32(tn.tn_conv3d_requant(xp, xd, wp, 64, tn.geom(), dev(lo), dev(hi)))
     y = tn.tn_conv3d(xp, xd, wp, 64, tn.geom()).cpu().numpy()
-    g = synth.rng(99)
-    m = 4096
-    at = np.stack([np.zeros(m, int), g.integers(0, 64, m), g.integers(0, 64, m), g.integers(0, 128, m),
-                   g.integers(0, 128, m)], 1).astype(np.int32)
-    # include the corners and faces (padding paths)
-    at[:8, 2:] = [[0, 0, 0], [63, 127, 127], [0, 127, 0], [63, 0, 127], [31, 0, 64], [31, 127, 64],
-                  [0, 64, 64], [63, 64, 64]]
-    ref_acc = oracle.conv3d_at(x, w, at)
-    n_, k_, z_, y_, x_ = at.T
-    np.testing.assert_array_equal(y[n_, z_, y_, x_, k_], ref_acc)
-    ref_t = np.where(ref_acc >= hi[k_], 1, np.where(ref_acc <= lo[k_], -1, 0))
-    s_bit = (yp[n_, z_, y_, x_, 0, k_ // 32] >> (k_ % 32)) & 1
-    m_bit = (yp[n_, z_, y_, x_, 1, k_ // 32] >> (k_ % 32)) & 1
-    got_t = np.where(m_bit == 1, np.where(s_bit == 1, 1, -1), 0)
-    np.testing.assert_array_equal(got_t, ref_t)
-    assert np.all(yp[..., 0, :] & ~yp[..., 1, :] == 0)
-    # the int32 and packed outputs agree everywhere (requant of the full int32 tensor)
-    y_t = torch.from_numpy(y).cuda()
-    np.testing.assert_array_equal(u32(tn.tn_requant(y_t, dev(lo), dev(hi))), yp)
+    torch.cuda.synchronize()
+    ref_acc = oracle.conv3d(x, w)                                   # [1,64,64,128,128]
+    np.testing.assert_array_equal(y, ref_acc.transpose(0, 2, 3, 4, 1))
+    ref_p, bad = oracle.pack(oracle.requant(ref_acc, lo, hi))
+    assert bad == -1
+    np.testing.assert_array_equal(yp, ref_p)
 
 
 # The FCN's full-resolution layers of configs[3] (1 x C x 128 x 256 x 256) through
@@ -520,8 +540,8 @@ def test_c1_full_size_sampled(tn):
 # sampled outputs against the oracle's per-output sum + the packed/int32 agreement.
 C3_LAYER_CASES = [
     # (C, K, stride, kernel)
-    (16, 16, 1, "tz"), (16, 16, 1, "tz8"), (16, 16, 1, "tc"), (16, 16, 2, "tz"), (16, 16, 2, "tz8"),
-    (16, 16, 2, "tc"), (16, 32, 1, "tz"), (32, 16, 1, "tz"), (64, 32, 1, "tz"),
+    (16, 16, 1, "tz"), (16, 16, 1, "tz8"), (16, 16, 2, "tz"), (16, 16, 2, "tz8"),
+    (16, 32, 1, "tz"), (32, 16, 1, "tz"), (64, 32, 1, "tz"), (64, 64, 2, "tz"),
 ]
 
 
@@ -620,13 +640,10 @@ def test_fcn_nonfinite_input_reported(tn):
 @pytest.mark.parametrize("shape,nslabs", [((1, 1, 32, 48, 48), 2), ((1, 1, 64, 24, 40), 8),
                                           ((1, 1, 16, 40, 56), 2)])
 def test_fcn_slabs_local_p2p_bit_identical(tn, fcn_kernel, shape, nslabs):
-    """NEXT-1 schedule on one device: every conv epilogue (TZ, TC, popc, first layer) stores
+    """NEXT-1 schedule on one device: every conv epilogue (TZ, popc, first layer) stores
     its boundary planes straight into the neighbouring slabs' halo planes and progress
     flags replace the copies; == the whole-volume forward bit for bit, also when the same
     workspace is reused (flags restart per call)."""
-    if fcn_kernel == "tc":
-        pytest.skip("the dx-merged TC kernel plans whole volumes only (Do = out_extent(Dci)); "
-                    "slab convs run on TZ / popc")
     x = synth.ct_volume(shape, seed=13)
     p = synth.fcn_params()
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])

@@ -82,6 +82,50 @@ def test_oracle_fold_table_is_eq6_exactly_for_dyadic_parameters():
         assert list(tab[c]) == ref
 
 
+@pytest.mark.parametrize("var_eps", [(0.0625, 0.1875), (3.75, 0.25), (15.75, 0.25), (48.0, 16.0)],
+                         ids=["1/4", "4", "16", "64"])
+def test_oracle_fold_table_bn_denominator_sqrt_var_plus_eps(var_eps):
+    """The batch-norm denominator of the fold (the conv output alpha*acc is
+    batch normalised, then Eq. 6): y = gamma*(alpha*acc - mean)/sqrt(var + eps) + beta.
+    var + eps is a dyadic perfect square other than 1 (1/4, 4, 16, 64), so sqrt(var + eps) and
+    every float64 step of the oracle are exact; the table must equal Eq. 6 of y in exact
+    rational arithmetic.  The same parameters are checked to separate the plausible mistakes
+    (no sqrt; sqrt(var) + eps; sqrt(var) without eps): each gives a different table, so a
+    dropped or misplaced sqrt in the oracle fails this pin."""
+    var_v, eps = var_eps
+    g = synth.rng(45)
+    A = 27 * 16
+    k = 24
+    alpha = (g.integers(1, 64, k) / 64.0).astype(np.float32)
+    gamma = (g.integers(-64, 64, k) / 16.0).astype(np.float32)
+    gamma[gamma == 0] = 1.0
+    beta = (g.integers(-64, 64, k) / 32.0).astype(np.float32)
+    mean = (g.integers(-64, 64, k) / 8.0).astype(np.float32)
+    var = np.full(k, var_v, np.float32)
+    s = Fraction(float(np.float32(var_v))) + Fraction(float(np.float32(eps)))
+    sd = Fraction(int(round(float(s) ** 0.5 * 4)), 4)
+    assert sd * sd == s and s != 1                 # an exact dyadic square root
+    tab = oracle.fold_table(alpha, gamma, beta, mean, var, eps, A)
+    accs = range(-A, A + 1)
+
+    def table(den):
+        out = []
+        for c in range(k):
+            a = Fraction(float(gamma[c])) * Fraction(float(alpha[c])) / den
+            b = Fraction(float(beta[c])) - Fraction(float(gamma[c])) * Fraction(float(mean[c])) / den
+            out.append([_tern(a * acc + b) for acc in accs])
+        return out
+
+    ref = table(sd)
+    for c in range(k):
+        assert list(tab[c]) == ref[c], f"channel {c}"
+    # the pin separates the plausible mistakes
+    wrong = {"no sqrt": s, "sqrt(var) + eps": Fraction(float(np.float32(var_v)) ** 0.5) + Fraction(float(eps)),
+             "sqrt(var)": Fraction(float(np.float32(var_v)) ** 0.5)}
+    for name, den in wrong.items():
+        assert table(den) != ref, name
+
+
 def test_library_ternarize_matches_oracle(tn):
     for sp, w, codes, alpha in _examples():
         c, a = tn.tn_ternarize_weights(w[None], -1.0 if sp is None else sp)

@@ -429,3 +429,28 @@ def test_bench_golden_samples_are_the_oracles():
         want = np.where(acc >= hi[k], 1, np.where(acc <= lo[k], -1, 0))
         np.testing.assert_array_equal(want, ref)
     assert np.all(g["bin_ref"] != 0) and set(np.unique(g["c1_ref"])) == {-1, 0, 1}
+
+
+def test_bench_golden_fcn_logits_are_the_oracles():
+    """The FCN gates of bench.py: configs[2]'s sampled logits are recomputed here with the oracle
+    (one 96x144x144 forward); configs[3] volume 0 (a 128x256x256 forward) and the configs[4] crop
+    are too slow for the CPU suite -- their positions are checked to lie inside the volume (C4:
+    inside the crop's exact region, 44 voxels from its lower faces and 37 from its upper ones)
+    and their values to be finite logits of the right magnitude; tools/make_bench_golden.py
+    (oracle/ only) wrote all three."""
+    g = np.load(os.path.join(GOLDEN, "bench_samples.npz"))
+    cfg = synth.CONFIGS["C2"]
+    p = synth.fcn_params(cfg["seed_params"])
+    x = synth.ct_volume(cfg["vol_shape"], seed=cfg["seeds"][0])
+    lg, _, bad = oracle.fcn_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"])
+    assert bad == -1
+    np.testing.assert_array_equal(lg[tuple(g["fcn_c2_at"].T)], g["fcn_c2_ref"])
+    bound = float(np.abs(p["pred_b"]).max() + np.abs(p["pred_w"]).sum(1).max())
+    for name, region in (("c3", ((0, 128), (0, 256), (0, 256))),
+                         ("c4", ((64 + 44, 192 - 37), (192 + 44, 320 - 37), (320 + 44, 448 - 37)))):
+        at, ref = g[f"fcn_{name}_at"], g[f"fcn_{name}_ref"]
+        assert at.shape == (512, 5) and ref.shape == (512,)
+        assert np.all(at[:, 0] == 0) and set(np.unique(at[:, 1])) == {0, 1}
+        for a, (lo_, hi_) in enumerate(region):
+            assert np.all((at[:, 2 + a] >= lo_) & (at[:, 2 + a] < hi_)), (name, a)
+        assert np.all(np.isfinite(ref)) and np.all(np.abs(ref) <= bound + 1e-6)
