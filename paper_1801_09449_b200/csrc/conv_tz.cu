@@ -186,6 +186,7 @@ struct TzPlan {
     uint32_t po_magic;      // ceil(2^32 / Po)
     int step_q, step_r;     // 256 rows (one expander sweep) = step_q raster rows + step_r positions
     int code_off, code_pitch, code_bytes;   // FIRST: ternary code planes (2 buffers) after the stages
+    int wpad;               // bytes after the code planes so that the packed filter bank fits from s_a on
     int ptab_floats;
 };
 
@@ -265,10 +266,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     constexpr int NB = STR == 1 ? (SPLIT ? 3 : 5) : 4;
     constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* s_a = smem;                                         // [slot][phase][chunk][RS][16]
-    uint8_t* s_b = s_a + pl.nslot * pl.slot_bytes;               // [mma][half][NB*K][16]
-    uint8_t* s_stage = s_b + pl.b_bytes;                         // [stage] packed rows per segment
-    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes);   // [K] -hi
+    // [B image][A ring][staging ring][FIRST code planes][wpad]: during setup the packed filter
+    // bank is staged in the contiguous span from the A ring to the end of wpad
+    uint8_t* s_b = smem;                                         // [mma][half][NB*K][16]
+    uint8_t* s_a = s_b + pl.b_bytes;                             // [slot][phase][chunk][RS][16]
+    uint8_t* s_stage = s_a + pl.nslot * pl.slot_bytes;           // [stage] packed rows per segment
+    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes + pl.wpad);   // [K] -hi
     int* s_lmh = s_nhi + K;                                      // [K] lo - hi
     float* s_pred = reinterpret_cast<float*>(s_lmh + K);         // [kZMaxClass] bias, then quad tables
     float* s_ptab = s_pred + kZMaxClass;
@@ -1129,7 +1132,7 @@ static cudaError_t launch_pdl(void (*kern)(ConvDesc, TzPlan), int grid, int thre
 
 static size_t tz_smem(const TzPlan& pl, int K) {
     return static_cast<size_t>(pl.nslot) * pl.slot_bytes + pl.b_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
-           2 * static_cast<size_t>(pl.code_bytes) +
+           2 * static_cast<size_t>(pl.code_bytes) + pl.wpad +
            2 * K * sizeof(int) + (kZMaxClass + pl.ptab_floats) * sizeof(float) +
            (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
 }
@@ -1327,7 +1330,9 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
             for (int nst = kZMaxStage; nst >= 2 && !ok; --nst) {
                 pl.nslot = ns;
                 pl.nstage = nst;
-                if (tz_smem(pl, cd.K) <= kSmemMax && pl.nslot * pl.slot_bytes >= wbytes) ok = true;
+                const int span = pl.nslot * pl.slot_bytes + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes;
+                pl.wpad = round_up(std::max(0, wbytes - span), 128);
+                if (tz_smem(pl, cd.K) <= kSmemMax) ok = true;
             }
     }
     if (!ok) return false;

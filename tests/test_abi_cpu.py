@@ -169,3 +169,24 @@ def _dummy_fcn(tn):
     P = ctypes.c_void_p(0x1000)
     assert tn.lib.tn_fcn_create(layers, len(table), -200.0, 200.0, P, P, 2, ctypes.byref(h)) == tn.TN_OK
     return h
+
+
+@pytest.mark.parametrize("vol", [(96, 144, 144), (128, 256, 256), (256, 512, 512), (32, 48, 48)],
+                         ids=["C2", "C3", "C4", "small"])
+def test_every_fcn_layer_runs_on_the_tensor_core_kernel(tn, vol):
+    """Host planning for every conv layer of the R9 FCN at the configs[2..4] volumes (and a small
+    one): each plans onto the tcgen05 kernel (TZ) -- none silently falls back to popc (round-2
+    regression: the 64+64 -> 64 block at configs[2]'s 36-wide R2 did)."""
+    table = tn.fcn_table()
+    ext = {}
+    couts = [row[1] for row in table]
+    for i, (kind, co, s, segs) in enumerate(table):
+        if segs[0][0] < 0:
+            ext[i] = vol
+            continue
+        src, up = segs[0]
+        e = tuple(v * (2 if up else 1) for v in ext[src])
+        dims = [tn.dims(1, couts[sj], *ext[sj]) for sj, _ in segs]
+        ups = [u for _, u in segs]
+        assert tn.tn_conv_kernel_for(dims, co, tn.geom(s), ups) == tn.TN_KERNEL_TZ, (vol, i + 1)
+        ext[i] = tuple((v - 1) // s + 1 for v in e)

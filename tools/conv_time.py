@@ -1,4 +1,4 @@
-"""Time one conv3d_requant launch per kernel (TZ / TC) on the FCN's configs[3] layer shapes
+"""Time one conv3d_requant launch per TZ operand type (FP4 / int8) on the FCN's configs[3] layer shapes
 (CUDA-graph replays of 10 back-to-back launches, CUDA events)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -18,8 +18,9 @@ CASES = [  # (name, shape, k, stride)
     ("#6 32->64 R2", (1, 32) + R2, 64, 1),
     ("#10 64->32 R2", (1, 64) + R2, 32, 1),
     ("#12 32->16 R1", (1, 32) + R1, 16, 1),
+    ("#7 64->64 s2", (1, 64) + R2, 64, 2),
 ]
-sel = {"tz": tn.TN_KERNEL_TZ, "tc": tn.TN_KERNEL_TC}
+sel = {"tz": tn.TN_KERNEL_TZ, "tz8": tn.TN_KERNEL_TZ8}
 for name, shape, k, s in CASES:
     x = synth.ternary_codes(shape, 0.5, seed=1); w = synth.ternary_codes((k, shape[1], 3, 3, 3), 0.6, seed=2)
     xp = tn.tn_pack_i8(dev(x)); wp = tn.tn_pack_weights(dev(w)); xd = tn.dims(*shape)
@@ -45,7 +46,7 @@ for name, shape, k, s in CASES:
     tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
     od = [d // s for d in shape[2:]]
     macs = np.prod(od) * shape[1] * k * 27
-    same = "" if len(out) < 2 else ("  (outputs identical)" if out["tz"][1] == out["tc"][1] else "  OUTPUTS DIFFER")
+    same = "" if len(out) < 2 else ("  (outputs identical)" if out["tz"][1] == out["tz8"][1] else "  OUTPUTS DIFFER")
     line = "  ".join(f"{kn}: {t:7.1f} us {macs / t / 1e6:7.1f} TMAC/s {2 * macs / t / 1e6 / 3325 * 100:5.1f}%"
                      for kn, (t, _) in out.items())
     print(f"{name:16s} {line}{same}", flush=True)
