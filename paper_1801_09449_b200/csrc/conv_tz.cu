@@ -53,110 +53,26 @@
 #include <climits>
 #include <vector>
 
-#ifndef TN_EXP_PROF
-#define TN_EXP_PROF 0
-#endif
-#if TN_EXP_PROF
-__device__ long long g_tztrace[148 * 16];
-#define ZSTAMP(v) long long v = clock64()
-#define ZACC(acc, t0) acc += clock64() - (t0)
-#else
-#define ZSTAMP(v) do { } while (0)
-#define ZACC(acc, t0) do { } while (0)
-#endif
-#ifndef TZ_EXP_NOEPI
-#define TZ_EXP_NOEPI 0
-#endif
-#ifndef TZ_EXP_NOEXP
-#define TZ_EXP_NOEXP 0
-#endif
-// Tiles per synchronisation unit: the MMA issuers and the epilogue hand TMEM
-// blocks over per unit of TU consecutive tiles (one mbarrier wait / commit /
-// arrive per unit instead of per tile).  Measured: 3 for the one-segment K = 16
-// layers (#1 -4 %, #2 -5 %), 1 elsewhere (C1 with two tiles per strip needs the
-// per-tile hand-over).
-#ifndef TZ_TU
-#define TZ_TU ((K == 16 && NSEG == 1) ? 3 : 1)
-#endif
-#ifndef TZ_EXP_NOFENCE
-#define TZ_EXP_NOFENCE 0
-#endif
-#ifndef TZ_EXP_NOMMA
-#define TZ_EXP_NOMMA 0
-#endif
-#ifndef TZ_EXP_NOACCWAIT
-#define TZ_EXP_NOACCWAIT 0
-#endif
-#ifndef TZ_WAIT
-#ifndef TZ_DEBUG_WAIT
-#define TZ_DEBUG_WAIT 0
-#endif
-#if TZ_DEBUG_WAIT
-// debug build: a wait that sees no progress for 2 s records (block, thread, line, parity,
-// barrier offset) into pinned host memory (readable while the kernel hangs) and keeps waiting
-__device__ unsigned int* g_tz_dbg = nullptr;
-__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int line) {
-    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    bool reported = false;
-    while (true) {
-        uint32_t ok;
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-        if (ok) return;
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (!reported && t - t0 > 2000000000ull && g_tz_dbg != nullptr) {
-            reported = true;
-            const unsigned slot = atomicAdd(g_tz_dbg, 1u);
-            if (slot < 4000) {
-                volatile unsigned int* r = g_tz_dbg + 16 + 8 * slot;
-                r[0] = blockIdx.x; r[1] = threadIdx.x; r[2] = line; r[3] = parity; r[4] = a;
-                __threadfence_system();
-            }
-        }
-    }
-}
-#define TZ_WAIT(b, p) mbar_wait_dbg(b, p, __LINE__)
-extern "C" int tn_exp_set_tz_dbg(void* p) { return static_cast<int>(cudaMemcpyToSymbol(g_tz_dbg, &p, sizeof(p))); }
-#else
-#define TZ_WAIT mbar_wait
-#endif
-#endif
-
 namespace tn {
 namespace {
 
 // MMA issuers (tiles t % kZMmaWarps): one thread's per-tile wait / commit
 // overhead exceeds the 5 x 44 cycles a K = 16 tile keeps the tensor pipe busy.
-#ifndef TZ_MMA_WARPS
-#define TZ_MMA_WARPS 2
-#endif
-constexpr int kZMmaWarps = TZ_MMA_WARPS;
+constexpr int kZMmaWarps = 2;
 // Expander warps: the expansion is latency-bound per warp, so as many as the
 // register budget allows (the fused-prediction variants need more registers).
 // Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
 // strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
-#ifndef TZ_EPI_GROUPS1
-#define TZ_EPI_GROUPS1 2
-#endif
-#ifndef TZ_EXP_WARPS1
-#define TZ_EXP_WARPS1 12
-#endif
-__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : (ct == 1 ? TZ_EXP_WARPS1 : 12); }
+__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
-__host__ __device__ constexpr int tz_epi_groups(bool pred, int ct) { return (!pred && ct == 1) ? TZ_EPI_GROUPS1 : 2; }
+__host__ __device__ constexpr int tz_epi_groups(bool, int) { return 2; }
 __host__ __device__ constexpr int tz_threads(bool pred, int ct) {
     return (4 * tz_epi_groups(pred, ct) + tz_exp_warps(pred, ct) + kZMmaWarps + 1) * 32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
 constexpr int kZMaxSlot = 4;          // A ring
-#ifndef TZ_MAX_STAGE
-#define TZ_MAX_STAGE 4
-#endif
-constexpr int kZMaxStage = TZ_MAX_STAGE;         // packed staging ring
+constexpr int kZMaxStage = 4;         // packed staging ring
 constexpr int kZMaxClass = 8;
 
 struct TzPlan {
@@ -288,12 +204,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     const int lane = threadIdx.x & 31;
     const bool fused = cd.yp != nullptr;
     const int T = pl.T;
-    const int NU = (T + TZ_TU - 1) / TZ_TU;   // synchronisation units per strip
-#if TN_EXP_PROF
-    const long long k_begin = clock64();
-    long long k_gstart = 0;
-    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_gstart));
-#endif
+    const int NU = T;      // synchronisation units per strip: one per tile
 
     // ---- setup: stage the packed filter bank (cp.async) in the A ring, expand it
     // into the B image, thresholds, barriers, TMEM.
@@ -317,13 +228,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             ofs += 4 * n4;
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-#if TN_EXP_PROF
-        if (threadIdx.x == 0) g_tztrace[16 * blockIdx.x + 15] = clock64() - k_begin;
-#endif
         if (threadIdx.x < K) {
-            if (F4) {   // f32 accumulators: the same integers as floats (exact, +0.0 for 0)
-                s_nhi[threadIdx.x] = __float_as_int(fused ? static_cast<float>(-hi_r) : 0.0f);
-                s_lmh[threadIdx.x] = __float_as_int(static_cast<float>(lo_r - hi_r));
+            if (F4) {   // f32 accumulators: acc - hi + 1/2 (exact: |hi|, |lo| <= 2^20, |acc| < 2^12)
+                s_nhi[threadIdx.x] = __float_as_int(fused ? 0.5f - static_cast<float>(hi_r) : 0.0f);
+                s_lmh[threadIdx.x] = __float_as_int(static_cast<float>(lo_r - hi_r + 1));
             } else {
                 s_nhi[threadIdx.x] = fused ? -hi_r : 0;
                 s_lmh[threadIdx.x] = lo_r - hi_r;
@@ -432,7 +340,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
         for (int k = 0; k < K; ++k) iv[k] = s_nhi[k];
         for (int t = 0; t < T; ++t)
-            if ((t / TZ_TU) % kZEpiGroups == g)
+            if (t % kZEpiGroups == g)
             for (int b = 0; b < RO; ++b)
 #pragma unroll
                 for (int c = 0; c < K; c += 16)
@@ -452,18 +360,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     __syncthreads();
     tc_fence_after();
 
-#if TN_EXP_PROF
-    if (threadIdx.x == 0) g_tztrace[16 * blockIdx.x + 11] = clock64() - k_begin;
-#endif
     const uint32_t two_po = 2u * pl.Po;
     if (warp == kZLoadWarp) {
         // ================= loader: per plane and segment one bulk copy of the
         // contiguous packed rows the strip reads (zero-size outside the buffer)
         if (lane == 0) {
-#if TN_EXP_PROF
-            long long l_wait = 0;
-            const long long l_begin = clock64();
-#endif
             ZWalk wk(pl.units, cd.Do, pl.nstrip);
             int n, strip, zf, zl;
             uint32_t st = 0, st_r = 0;
@@ -474,9 +375,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
                 for (int i = i0; i <= i1; ++i) {
-                    ZSTAMP(w0);
-                    if (st_r > 0) TZ_WAIT(staged_empty + st, (st_r - 1) & 1);
-                    ZACC(l_wait, w0);
+                    if (st_r > 0) mbar_wait(staged_empty + st, (st_r - 1) & 1);
                     uint32_t bytes[kMaxSeg];
                     const uint32_t* src[kMaxSeg];
                     uint32_t total = 0;
@@ -522,18 +421,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                 }
             }
-#if TN_EXP_PROF
-            g_tztrace[16 * blockIdx.x + 0] = clock64() - l_begin;
-            g_tztrace[16 * blockIdx.x + 1] = l_wait;
-#endif
         }
     } else if (warp >= kZExpWarp0 && warp < kZMmaWarp) {
         // ================= expanders: staged packed rows -> int8 strip of one plane
         const int et = threadIdx.x - kZExpWarp0 * 32;
-#if TN_EXP_PROF
-        long long e_w1 = 0, e_w2 = 0, e_planes = 0;
-        const long long e_begin = clock64();
-#endif
         ZWalk wk(pl.units, cd.Do, pl.nstrip);
         int n, strip, zf, zl;
         uint32_t st = 0, st_r = 0, as = 0, as_r = 0;
@@ -547,15 +438,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
             const int qa = strip * 128 * T - pl.Po - 1;
             for (int i = i0; i <= i1; ++i) {
-                ZSTAMP(x0);
-                TZ_WAIT(staged_full + st, st_r & 1);
-                ZACC(e_w1, x0);
-                ZSTAMP(x1);
-                if (as_r > 0) TZ_WAIT(plane_free + as, (as_r - 1) & 1);
-                ZACC(e_w2, x1);
-#if TN_EXP_PROF
-                ++e_planes;
-#endif
+                mbar_wait(staged_full + st, st_r & 1);
+                if (as_r > 0) mbar_wait(plane_free + as, (as_r - 1) & 1);
                 bool zok[kMaxSeg];
                 uint32_t head[kMaxSeg];    // the loader's 16-byte alignment head of each segment's rows
 #pragma unroll
@@ -631,8 +515,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 // A nearest-x2 upsampled C = 16 segment feeds 4 positions per source
                 // voxel and plane: its staged words are converted to FP4 in place first
                 // (packed 16 channels and FP4 16 channels are both 8 bytes).
-                const bool up_conv = NSEG == 2 && cd.seg[0].c == 16;
-                if (up_conv) {
+                constexpr int CS = 16 * CT / NSEG;            // channels per segment (FP4 plans: 16, 32, 64)
+                constexpr int BPV = CS > 32 ? 16 : 8;         // staged bytes per voxel
+                constexpr bool UPC = NSEG == 2 && CS == 16;
+                if constexpr (UPC) {
                     uint2* p0 = reinterpret_cast<uint2*>(const_cast<uint8_t*>(stg) + pl.seg_off[0] + head[0]);
                     const int nv = nr[0] * cd.seg[0].W;
                     for (int e = et; e < nv; e += kZExpThreads) {
@@ -641,58 +527,72 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     }
                     asm volatile("bar.sync 1, %0;" ::"r"(kZExpThreads) : "memory");
                 }
-                int r = TZ_EXP_NOEXP ? pl.RS : et;
+                // Row r of the strip = output raster position (y, x) (pitch Po); the plain
+                // segment's staged voxel index L = y * Wp + x (stride 2: phase (py, px) reads
+                // 2L + py * Wp + px) and the row's A address advance incrementally.
+                int r = et;
                 int y, x;
                 {
                     const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
                     y = div_po(tq, pl.po_magic) - 2;
                     x = static_cast<int>(tq) - (y + 2) * pl.Po;
                 }
+                const int Wp = cd.seg[NSEG - 1].W;
+                int L = y * Wp + x;
+                const int dL = pl.step_q * Wp + pl.step_r, dLw = Wp - pl.Po;
+                uint32_t pbase[NSEG];
+#pragma unroll
+                for (int sg = 0; sg < NSEG; ++sg)
+                    pbase[sg] = smem_u32(stg + pl.seg_off[sg] + head[sg]) - static_cast<uint32_t>(ya[sg] * cd.seg[sg].W * BPV);
+                const uint32_t a0 = smem_u32(slot) + 16;
+                const int Wo = cd.Wo;
+                const unsigned Ho = static_cast<unsigned>(cd.Ho);
                 for (; r < pl.RS; r += kZExpThreads) {
-                    const bool vx = x < cd.Wo && y >= 0;
+                    const bool v = x < Wo && static_cast<unsigned>(y) < Ho;
+                    const uint32_t arow = a0 + r * 16;
 #pragma unroll
                     for (int ph = 0; ph < NPH; ++ph) {
-                        const int py = ph >> 1, px = ph & 1;
-                        const int yi = STR == 2 ? 2 * y + py : y, xi = STR == 2 ? 2 * x + px : x;
-                        const bool v = vx && yi < cd.Hci && xi < cd.Wci;
 #pragma unroll
                         for (int sg = 0; sg < NSEG; ++sg) {
-                            const SegDesc& sd = cd.seg[sg];
-                            constexpr bool kUp0 = NSEG == 2;
-                            const bool up = sg == 0 && kUp0;
-                            const int ys = up ? (yi >> 1) : yi, xs = up ? (xi >> 1) : xi;
+                            uint32_t src;
+                            if (NSEG == 2 && sg == 0)     // nearest x2 (stride 1 only)
+                                src = pbase[0] + static_cast<uint32_t>(((y >> 1) * cd.seg[0].W + (x >> 1)) * BPV);
+                            else if (STR == 2)
+                                src = pbase[sg] + static_cast<uint32_t>((2 * L + (ph >> 1) * Wp + (ph & 1)) * BPV);
+                            else
+                                src = pbase[sg] + static_cast<uint32_t>(L * BPV);
                             const bool ok = v && zok[sg];
-                            const uint8_t* sp = stg + pl.seg_off[sg] + head[sg] + ((ys - ya[sg]) * sd.W + xs) * 8 * sd.cw;
-                            uint8_t* rb = slot + (ph * pl.nreg + pl.reg0[sg]) * pl.REG + 16 + r * 16;
-                            if (sd.c == 16) {
+                            const uint32_t dst = arow + (ph * pl.nreg + pl.reg0[sg]) * pl.REG;
+                            if constexpr (CS == 16) {
                                 uint2 w = make_uint2(0u, 0u);
-                                if (ok) w = *reinterpret_cast<const uint2*>(sp);
-                                const uint2 e = (up && up_conv) ? w : expand16_f4(w.x, w.y, 0);
-                                *reinterpret_cast<uint2*>(rb) = e;
-                                *reinterpret_cast<uint2*>(rb - 8) = e;
-                            } else if (sd.cw == 1) {
+                                if (ok) w = lds64(src);
+                                const uint2 e = (NSEG == 2 && sg == 0) ? w : expand16_f4(w.x, w.y, 0);
+                                sts64(dst, e);
+                                sts64(dst - 8, e);
+                            } else if constexpr (CS == 32) {
                                 uint2 w = make_uint2(0u, 0u);
-                                if (ok) w = *reinterpret_cast<const uint2*>(sp);
+                                if (ok) w = lds64(src);
                                 const uint2 e0 = expand16_f4(w.x, w.y, 0), e1 = expand16_f4(w.x, w.y, 16);
-                                *reinterpret_cast<uint4*>(rb) = make_uint4(e0.x, e0.y, e1.x, e1.y);
+                                sts128(dst, make_uint4(e0.x, e0.y, e1.x, e1.y));
                             } else {
                                 uint4 w = make_uint4(0u, 0u, 0u, 0u);
-                                if (ok) w = *reinterpret_cast<const uint4*>(sp);
+                                if (ok) w = lds128(src);
                                 const uint2 e0 = expand16_f4(w.x, w.z, 0), e1 = expand16_f4(w.x, w.z, 16);
                                 const uint2 e2 = expand16_f4(w.y, w.w, 0), e3 = expand16_f4(w.y, w.w, 16);
-                                *reinterpret_cast<uint4*>(rb) = make_uint4(e0.x, e0.y, e1.x, e1.y);
-                                *reinterpret_cast<uint4*>(rb + pl.REG) = make_uint4(e2.x, e2.y, e3.x, e3.y);
+                                sts128(dst, make_uint4(e0.x, e0.y, e1.x, e1.y));
+                                sts128(dst + pl.REG, make_uint4(e2.x, e2.y, e3.x, e3.y));
                             }
                         }
                     }
                     x += pl.step_r;
                     y += pl.step_q;
-                    if (x >= pl.Po) { x -= pl.Po; ++y; }
+                    L += dL;
+                    if (x >= pl.Po) { x -= pl.Po; ++y; L += dLw; }
                 }
                 } else {
                 // Rows r = et + 256 j: (y, x) of the output raster tracked incrementally
                 // (256 = qd * Po + rd), all phases of a row from the same (y, x).
-                int r = TZ_EXP_NOEXP ? pl.RS : et;
+                int r = et;
                 int y, x;
                 {
                     const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
@@ -739,20 +639,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }   // !F4
                 }   // !FIRST
                 mbar_arrive(staged_empty + st);
-                if (!TZ_EXP_NOFENCE) fence_proxy_async();
+                fence_proxy_async();
                 mbar_arrive(plane_full + as);
                 if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                 if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
             }
         }
-#if TN_EXP_PROF
-        if (et == 0) {
-            g_tztrace[16 * blockIdx.x + 2] = clock64() - e_begin;
-            g_tztrace[16 * blockIdx.x + 3] = e_w1;
-            g_tztrace[16 * blockIdx.x + 4] = e_w2;
-            g_tztrace[16 * blockIdx.x + 5] = e_planes;
-        }
-#endif
     } else if (warp >= kZMmaWarp && warp < kZMmaWarp + kZMmaWarps) {
         // ================= MMA issuers (warp mw takes the tiles t % 2 == mw).  Descriptor low words are precomputed per
         // K-slice pair (start address and LBO); per (slot, tile) only an add remains,
@@ -764,15 +656,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         const uint32_t sfa = tmem_base + 480, sfb = tmem_base + 496;
         auto idesc_n = [](uint32_t n) { return F4 ? idesc_mxf4(static_cast<int>(n)) : idesc_i8(static_cast<int>(n)); };
         auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id) {
-            if (TZ_EXP_NOMMA) return;
             if constexpr (F4) tc_mma_mxf4(d, a, b, id, sfa, sfb);
             else tc_mma_i8(d, a, b, id, 1u);
         };
         const bool leader = elect_one();
-#if TN_EXP_PROF
-        long long m_w1 = 0, m_w2 = 0;
-        const long long m_begin = clock64();
-#endif
         const uint32_t a_base = smem_u32(s_a), b_base = smem_u32(s_b);
         const uint32_t b_half = NB * K * 16;          // LBO of B (bytes between the two K halves)
         const uint32_t b_mma16 = (2 * b_half) >> 4;   // descriptor step per MMA's B operand
@@ -844,9 +731,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         const uint32_t b0 = STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
                         bl_full = b_lo0 + b0 * K;
                     }
-                    ZSTAMP(y0);
-                    TZ_WAIT(plane_full + as, as_r & 1);
-                    ZACC(m_w1, y0);
+                    mbar_wait(plane_full + as, as_r & 1);
                     const uint32_t a_slot16 = (as * pl.slot_bytes) >> 4;
                     // steady-state fast path (stride 1, rotated B): the plane starts output
                     // i+1 (one wait per tile) and completes output i-1 (one commit per tile);
@@ -864,10 +749,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         constexpr uint32_t kBarStep = 8 * kZMmaWarps;
                         int k = 0;
                         for (int v = v0; v < NU; v += kZMmaWarps, ++k) {   // (units past Tv: empty commit)
-                            if (!TZ_EXP_NOACCWAIT) mbar_wait_addr(wbar + k * kBarStep, wpar);
+                            mbar_wait_addr(wbar + k * kBarStep, wpar);
                             tc_fence_after();
-                            const int t1 = min((v + 1) * TZ_TU, Tv);
-                            for (int t = v * TZ_TU; t < t1; ++t) {
+                            const int t1 = min(v + 1, Tv);
+                            for (int t = v; t < t1; ++t) {
                                 const uint32_t a_add = t * 128;
                                 const uint32_t d_tile = tmem_base + t * RO * K;
 #pragma unroll
@@ -882,14 +767,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     // barriers then advance one phase per output plane in every strip, which the
                     // parities assume when a CTA's range continues into a full strip (n > 1)
                     for (int v = warp - kZMmaWarp; v < NU; v += kZMmaWarps) {
-                        ZSTAMP(y1);
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (is_new[j] && !TZ_EXP_NOACCWAIT) TZ_WAIT(acc_empty + new_bar[j] + v, new_par[j]);
-                        ZACC(m_w2, y1);
+                            if (is_new[j]) mbar_wait(acc_empty + new_bar[j] + v, new_par[j]);
                         tc_fence_after();
-                        const int t1 = min((v + 1) * TZ_TU, Tv);
-                        for (int t = v * TZ_TU; t < t1; ++t) {
+                        const int t1 = min(v + 1, Tv);
+                        for (int t = v; t < t1; ++t) {
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
                         if constexpr (SPLIT) {
@@ -933,27 +816,16 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             }
         }
         __syncwarp();
-#if TN_EXP_PROF
-        if (leader && warp == kZMmaWarp) {
-            g_tztrace[16 * blockIdx.x + 6] = clock64() - m_begin;
-            g_tztrace[16 * blockIdx.x + 7] = m_w1;
-            g_tztrace[16 * blockIdx.x + 8] = m_w2;
-        }
-#endif
     } else {
         // ================= epilogue
         const int q = warp & 3, g = warp >> 2;
-#if TN_EXP_PROF
-        long long p_w = 0;
-        const long long p_begin = clock64();
-#endif
         ZWalk wk(pl.units, cd.Do, pl.nstrip);
         int n, strip, zf, zl;
         uint32_t u = 0;
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         // K = 16: thresholds and the re-init values live in registers
         constexpr bool REGT = K == 16;
-        int r_lmh[REGT ? 16 : 1], r_nhi[REGT ? 16 : 1];
+        int r_lmh[16], r_nhi[16];
         if constexpr (REGT) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) { r_lmh[k] = s_lmh[k]; r_nhi[k] = s_nhi[k]; }
@@ -965,16 +837,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
                 for (int v = g; v < NU; v += kZEpiGroups) {   // all units (see the MMA issuer)
-                    ZSTAMP(p0);
-                    TZ_WAIT(acc_full + sgm * NU + v, par);
-                    ZACC(p_w, p0);
+                    mbar_wait(acc_full + sgm * NU + v, par);
                     tc_fence_after();
-#if TZ_EXP_NOEPI
-                    mbar_arrive(acc_empty + sgm * NU + v);
-                    continue;
-#endif
-                    const int t1 = min((v + 1) * TZ_TU, Tv);
-                    for (int t = v * TZ_TU; t < t1; ++t) {
+                    const int t = v;                      // one tile per unit
+                    if (t >= Tv) {                        // past a ragged strip's last tile: no MMAs ran,
+                        mbar_arrive(acc_empty + sgm * NU + v);   // the block still holds its initial values
+                        continue;
+                    }
                     const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
                     const int qpos = q_lane + t * 128;
                     const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
@@ -982,28 +851,59 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     const bool vpos = x < cd.Wo && y < cd.Ho;
                     const int voff = y * cd.Wo + x;
                     uint32_t sbits[CWO], mbits[CWO];
+                    // K <= 32: the whole tile's accumulators go to registers first and the block is
+                    // re-initialised and handed back to the MMA issuer at once, so the next MMAs into
+                    // it overlap this tile's requant / stores.  K = 64: chunk by chunk (registers).
+                    constexpr bool EARLY = K <= 32;
+                    constexpr int NCH = EARLY ? K / 16 : 1;
+                    int accs[NCH][16];
+                    auto reinit = [&](int c) {            // the output that reuses the block starts at -hi
+                        if constexpr (REGT) {
+                            tmem_st16(taddr + c, r_nhi);
+                        } else {
+                            int nhv[16];
+#pragma unroll
+                            for (int i4 = 0; i4 < 4; ++i4) {
+                                const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
+                                nhv[4 * i4] = h4.x; nhv[4 * i4 + 1] = h4.y; nhv[4 * i4 + 2] = h4.z; nhv[4 * i4 + 3] = h4.w;
+                            }
+                            tmem_st16(taddr + c, nhv);
+                        }
+                    };
+                    if constexpr (EARLY) {
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) tmem_ld16(taddr + 16 * ch, accs[ch]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) reinit(16 * ch);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(acc_empty + sgm * NU + v);
+                    }
 #pragma unroll
                     for (int c = 0; c < K; c += 16) {
-                        int acc[16];
-                        tmem_ld16(taddr + c, acc);
-                        tmem_wait_ld();
-                        int lmh[16], nhv[16];
+                        int* acc = accs[EARLY ? c / 16 : 0];
+                        if constexpr (!EARLY) {
+                            tmem_ld16(taddr + c, accs[0]);
+                            tmem_wait_ld();
+                        }
+                        int lmh[16];
                         if constexpr (REGT) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) { lmh[i] = r_lmh[i]; nhv[i] = r_nhi[i]; }
+                            for (int i = 0; i < 16; ++i) lmh[i] = r_lmh[i];
                         } else {
 #pragma unroll
                             for (int i4 = 0; i4 < 4; ++i4) {
                                 const int4 l4 = *reinterpret_cast<const int4*>(s_lmh + c + 4 * i4);
-                                const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
                                 lmh[4 * i4] = l4.x; lmh[4 * i4 + 1] = l4.y; lmh[4 * i4 + 2] = l4.z; lmh[4 * i4 + 3] = l4.w;
-                                nhv[4 * i4] = h4.x; nhv[4 * i4 + 1] = h4.y; nhv[4 * i4 + 2] = h4.z; nhv[4 * i4 + 3] = h4.w;
                             }
                         }
                         if (fused) {
                             // acc holds acc - hi (initialised to -hi).  A4 (reading R5):
                             // +1 if acc >= hi; else -1 if acc <= lo; else 0.  Bit k of nhi =
                             // (acc_k < hi_k); bit k of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).
+                            // F4: f32 accumulators start at 0.5 - hi and lmh = lo - hi + 1, so d and
+                            // lmh - d are never zero (acc integer): no sign-of-zero ambiguity.
                             uint32_t nhi = 0u, nlo = 0u;
 #pragma unroll
                             for (int i = 15; i >= 0; --i) {
@@ -1026,8 +926,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             for (int i = 0; i < 4; ++i)
                                 dst[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
                         }
-                        // re-initialise the block for the output that reuses it
-                        tmem_st16(taddr + c, nhv);
+                        if constexpr (!EARLY) reinit(c);
+                    }
+                    if constexpr (!EARLY) {
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(acc_empty + sgm * NU + v);
                     }
                     if (fused && vpos) {
                         if (PRED) {
@@ -1074,32 +978,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             halo_store_words(cd.halo_lo, cd.halo_hi, z, cd.Do, voff, wds, 2 * CWO);
                         }
                     }
-                    }   // tiles of the unit
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(acc_empty + sgm * NU + v);
                 }
             }
         }
-#if TN_EXP_PROF
-        if (warp == 0 && lane == 0) {
-            g_tztrace[16 * blockIdx.x + 9] = clock64() - p_begin;
-            g_tztrace[16 * blockIdx.x + 10] = p_w;
-        }
-#endif
     }
 
     tc_fence_before();
     __syncthreads();
-#if TN_EXP_PROF
-    if (threadIdx.x == 0) {
-        long long g_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-        g_tztrace[16 * blockIdx.x + 12] = clock64() - k_begin;
-        g_tztrace[16 * blockIdx.x + 13] = k_gstart;
-        g_tztrace[16 * blockIdx.x + 14] = g_end;
-    }
-#endif
     if (warp == kZMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
@@ -1533,8 +1418,3 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
 
 }  // namespace tn
 
-#if TN_EXP_PROF
-extern "C" int tn_exp_tztrace(long long* host, int n) {
-    return static_cast<int>(cudaMemcpyFromSymbol(host, g_tztrace, sizeof(long long) * (n < 148 * 16 ? n : 148 * 16)));
-}
-#endif

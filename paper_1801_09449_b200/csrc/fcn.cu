@@ -222,10 +222,7 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         cd.Do = o.d; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = 0;
         cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
         cd.cwo = (ly.c_out + 31) / 32;
-#ifndef TN_EXP_NOFUSEPRED
-#define TN_EXP_NOFUSEPRED 0
-#endif
-        if (i == L - 1 && !TN_EXP_NOFUSEPRED) {   // A8 fused into the last block's epilogue
+        if (i == L - 1) {   // A8 fused into the last block's epilogue
             cd.logits = logits;
             cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
             cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
@@ -234,7 +231,7 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         st = run_conv(cd, s, "tn_fcn_forward");
         if (st != TN_OK) return st;
     }
-    if (last == L && (net->layers[L - 1].kind == TN_LAYER_FIRST || TN_EXP_NOFUSEPRED)) {
+    if (last == L && net->layers[L - 1].kind == TN_LAYER_FIRST) {
         const LayerPlan& last = P[L - 1];
         cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(base + last.off), last.out,
                                        net->pred_w, net->pred_b, net->nclass, logits, s);

@@ -38,20 +38,9 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra TN_WAITS_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
 }
-// 8 ternary lanes (bits of a mask / negative byte) -> 8 FP4 E2M1 nibbles:
-// +1 -> 0x2 (1.0), -1 -> 0xA (-1.0), 0 -> 0x0; nibble k = lane k (k even in the
-// low nibble of byte k/2, the element order of packed e2m1 operands).
-__device__ __forceinline__ uint32_t spread8_nib(uint32_t t) {
-    t &= 0xFFu;
-    t = (t | (t << 12)) & 0x000F000Fu;
-    t = (t | (t << 6)) & 0x03030303u;
-    t = (t | (t << 3)) & 0x11111111u;
-    return t;
-}
-// 16 ternary lanes (bits sh..sh+15 of a sign / mask word pair) -> 16 FP4 nibbles
-#ifndef TN_F4_PRMT
-#define TN_F4_PRMT 1
-#endif
+// 16 ternary lanes (bits sh..sh+15 of a sign / mask word pair) -> 16 FP4 E2M1 nibbles:
+// +1 -> 0x2 (1.0), -1 -> 0xA (-1.0), 0 -> 0x0; nibble k = lane k (k even in the low
+// nibble of byte k/2, the element order of packed e2m1 operands).
 // 8 lanes -> a PRMT selector whose nibble k is the lane pair (2k+1, 2k) of x (bits 0..7)
 __device__ __forceinline__ uint32_t pair_selector(uint32_t x) {
     x &= 0xFFu;
@@ -60,17 +49,12 @@ __device__ __forceinline__ uint32_t pair_selector(uint32_t x) {
 }
 __device__ __forceinline__ uint2 expand16_f4(uint32_t s, uint32_t m, int sh) {
     const uint32_t mm = m >> sh, nn = (m & ~s) >> sh;
-    if (TN_F4_PRMT) {
-        // byte k of the result = FP4 lanes 2k (low nibble) and 2k+1: each lane pair picks one
-        // of four bytes with PRMT -- mask: {00, 02, 20, 22}, negative: {00, 08, 80, 88}
-        const uint32_t lo = __byte_perm(0x22200200u, 0u, pair_selector(mm)) |
-                            __byte_perm(0x88800800u, 0u, pair_selector(nn));
-        const uint32_t hi = __byte_perm(0x22200200u, 0u, pair_selector(mm >> 8)) |
-                            __byte_perm(0x88800800u, 0u, pair_selector(nn >> 8));
-        return make_uint2(lo, hi);
-    }
-    const uint32_t lo = (spread8_nib(mm) << 1) | (spread8_nib(nn) << 3);
-    const uint32_t hi = (spread8_nib(mm >> 8) << 1) | (spread8_nib(nn >> 8) << 3);
+    // byte k of the result = FP4 lanes 2k (low nibble) and 2k+1: each lane pair picks one
+    // of four bytes with PRMT -- mask: {00, 02, 20, 22}, negative: {00, 08, 80, 88}
+    const uint32_t lo = __byte_perm(0x22200200u, 0u, pair_selector(mm)) |
+                        __byte_perm(0x88800800u, 0u, pair_selector(nn));
+    const uint32_t hi = __byte_perm(0x22200200u, 0u, pair_selector(mm >> 8)) |
+                        __byte_perm(0x88800800u, 0u, pair_selector(nn >> 8));
     return make_uint2(lo, hi);
 }
 __device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -178,6 +162,23 @@ __device__ __forceinline__ uint4 expand16(uint32_t s, uint32_t m, int sh) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// Shared-memory loads / stores by 32-bit shared-window address.
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
