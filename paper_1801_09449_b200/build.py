@@ -72,4 +72,8 @@ def build_library(force: bool = False, extra=None, lib_path: str = None, obj_dir
 
 
 if __name__ == "__main__":
-    print(build_library(force="--force" in sys.argv))
+    if "--trace" in sys.argv:   # profiling build: per-role wait counters (TN_TRACE), libtn_trace.so
+        print(build_library(force="--force" in sys.argv, extra=["-DTN_TRACE"],
+                            lib_path=os.path.join(HERE, "libtn_trace.so"), obj_dir=os.path.join(HERE, "build_trace")))
+    else:
+        print(build_library(force="--force" in sys.argv))

@@ -53,6 +53,31 @@
 #include <climits>
 #include <vector>
 
+// TN_TRACE builds (profiling only; python paper_1801_09449_b200/build.py --trace writes
+// libtn_trace.so): per-CTA cycle counters of each warp role's barrier waits, read back with
+// tn_trace_read().  Slots: 0 kernel, 1 loader waits, 2 expander staged waits, 3 expander
+// slot waits, 4 MMA plane waits, 5 MMA accumulator waits, 6 epilogue waits, 7 epilogue busy.
+#ifdef TN_TRACE
+__device__ unsigned long long g_tn_trace[1024 * 8];
+#define TN_TW(slot, rec, stmt)                                                           \
+    do {                                                                                 \
+        const long long _t0 = clock64();                                                 \
+        stmt;                                                                            \
+        if (rec) atomicAdd(&g_tn_trace[blockIdx.x * 8 + (slot)], clock64() - _t0);      \
+    } while (0)
+extern "C" int tn_trace_read(unsigned long long* host, int n, int reset) {
+    const int m = n < 1024 * 8 ? n : 1024 * 8;
+    cudaError_t e = cudaMemcpyFromSymbol(host, g_tn_trace, sizeof(unsigned long long) * m);
+    if (reset) {
+        static unsigned long long zero[1024 * 8];
+        cudaMemcpyToSymbol(g_tn_trace, zero, sizeof(zero));
+    }
+    return static_cast<int>(e);
+}
+#else
+#define TN_TW(slot, rec, stmt) stmt
+#endif
+
 namespace tn {
 namespace {
 
@@ -63,11 +88,12 @@ constexpr int kZMmaWarps = 2;
 // register budget allows (the fused-prediction variants need more registers).
 // Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
 // strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
-__host__ __device__ constexpr int tz_exp_warps(bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
+__host__ __device__ constexpr int tz_exp_warps(int, bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
-__host__ __device__ constexpr int tz_epi_groups(bool, int) { return 2; }
-__host__ __device__ constexpr int tz_threads(bool pred, int ct) {
-    return (4 * tz_epi_groups(pred, ct) + tz_exp_warps(pred, ct) + kZMmaWarps + 1) * 32;
+// (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
+__host__ __device__ constexpr int tz_epi_groups(int, bool, int) { return 2; }
+__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct) {
+    return (4 * tz_epi_groups(k, pred, ct) + tz_exp_warps(k, pred, ct) + kZMmaWarps + 1) * 32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
@@ -156,15 +182,15 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
-__global__ void __launch_bounds__(tz_threads(PRED, CT), 1)
+__global__ void __launch_bounds__(tz_threads(K, PRED, CT), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
-    constexpr int kZExpThreads = tz_exp_warps(PRED, CT) * 32;
-    constexpr int kZEpiGroups = tz_epi_groups(PRED, CT);
+    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT);
     constexpr int kZEpiWarps = 4 * kZEpiGroups;
     constexpr int kZExpWarp0 = kZEpiWarps;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(PRED, CT);
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(PRED, CT);
+    constexpr int kZThreads = tz_threads(K, PRED, CT);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -331,6 +357,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         tc_fence_after();
     }
     const uint32_t tmem_base = *s_tmem;
+#ifdef TN_TRACE
+    const long long k_t0 = clock64();
+#endif
     pdl_launch_dependents();
 
     if (warp < kZEpiWarps) {
@@ -438,8 +467,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
             const int qa = strip * 128 * T - pl.Po - 1;
             for (int i = i0; i <= i1; ++i) {
-                mbar_wait(staged_full + st, st_r & 1);
-                if (as_r > 0) mbar_wait(plane_free + as, (as_r - 1) & 1);
+                TN_TW(2, et == 0, mbar_wait(staged_full + st, st_r & 1));
+                if (as_r > 0) TN_TW(3, et == 0, mbar_wait(plane_free + as, (as_r - 1) & 1));
                 bool zok[kMaxSeg];
                 uint32_t head[kMaxSeg];    // the loader's 16-byte alignment head of each segment's rows
 #pragma unroll
@@ -523,7 +552,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     const int nv = nr[0] * cd.seg[0].W;
                     for (int e = et; e < nv; e += kZExpThreads) {
                         const uint2 w = p0[e];
-                        p0[e] = expand16_f4(w.x, w.y, 0);
+                        p0[e] = expand16_f4_c16(w.x, w.y);
                     }
                     asm volatile("bar.sync 1, %0;" ::"r"(kZExpThreads) : "memory");
                 }
@@ -566,7 +595,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             if constexpr (CS == 16) {
                                 uint2 w = make_uint2(0u, 0u);
                                 if (ok) w = lds64(src);
-                                const uint2 e = (NSEG == 2 && sg == 0) ? w : expand16_f4(w.x, w.y, 0);
+                                const uint2 e = (NSEG == 2 && sg == 0) ? w : expand16_f4_c16(w.x, w.y);
                                 sts64(dst, e);
                                 sts64(dst - 8, e);
                             } else if constexpr (CS == 32) {
@@ -731,7 +760,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         const uint32_t b0 = STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
                         bl_full = b_lo0 + b0 * K;
                     }
-                    mbar_wait(plane_full + as, as_r & 1);
+                    TN_TW(4, warp == kZMmaWarp, mbar_wait(plane_full + as, as_r & 1));
                     const uint32_t a_slot16 = (as * pl.slot_bytes) >> 4;
                     // steady-state fast path (stride 1, rotated B): the plane starts output
                     // i+1 (one wait per tile) and completes output i-1 (one commit per tile);
@@ -749,7 +778,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         constexpr uint32_t kBarStep = 8 * kZMmaWarps;
                         int k = 0;
                         for (int v = v0; v < NU; v += kZMmaWarps, ++k) {   // (units past Tv: empty commit)
-                            mbar_wait_addr(wbar + k * kBarStep, wpar);
+                            TN_TW(5, warp == kZMmaWarp, mbar_wait_addr(wbar + k * kBarStep, wpar));
                             tc_fence_after();
                             const int t1 = min(v + 1, Tv);
                             for (int t = v; t < t1; ++t) {
@@ -769,7 +798,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     for (int v = warp - kZMmaWarp; v < NU; v += kZMmaWarps) {
 #pragma unroll
                         for (int j = 0; j < 3; ++j)
-                            if (is_new[j]) mbar_wait(acc_empty + new_bar[j] + v, new_par[j]);
+                            if (is_new[j]) TN_TW(5, warp == kZMmaWarp, mbar_wait(acc_empty + new_bar[j] + v, new_par[j]));
                         tc_fence_after();
                         const int t1 = min(v + 1, Tv);
                         for (int t = v; t < t1; ++t) {
@@ -836,8 +865,80 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
                 const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
+                // raster position of this lane in tile t -> (offset within the plane, valid)
+                auto position = [&](int t, int& voff) {
+                    const int qpos = q_lane + t * 128;
+                    const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
+                    const int x = qpos - y * pl.Po;
+                    voff = y * cd.Wo + x;
+                    return x < cd.Wo && y < cd.Ho;
+                };
+                // the requantised codes of one position: A8 prediction (last layer), packed store,
+                // NEXT-1 halo stores
+                auto finish = [&](int voff, const uint32_t (&sbits)[CWO], const uint32_t (&mbits)[CWO]) {
+                    if (PRED) {
+                        // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
+                        const int64_t v = static_cast<int64_t>(z) * cd.Ho * cd.Wo + voff;
+                        if (cd.nclass == 2 && K == 16) {
+                            // quad indices (mask nibble | sign nibble << 4): bytes of q02 = quads 0, 2;
+                            // bytes of q13 = quads 1, 3
+                            const uint32_t q02 = (mbits[0] & 0x0F0Fu) | ((sbits[0] & 0x0F0Fu) << 4);
+                            const uint32_t q13 = ((mbits[0] >> 4) & 0x0F0Fu) | (sbits[0] & 0xF0F0u);
+                            const uint32_t idx[4] = {q02 & 0xFFu, q13 & 0xFFu, (q02 >> 8) & 0xFFu, (q13 >> 8) & 0xFFu};
+                            float a0 = s_pred[0], a1 = s_pred[1];
+#pragma unroll
+                            for (int qd = 0; qd < 4; ++qd) {
+                                const float2 e2 = *reinterpret_cast<const float2*>(s_ptab + (qd * 256 + idx[qd]) * 2);
+                                a0 += e2.x;
+                                a1 += e2.y;
+                            }
+                            float* lg = cd.logits + static_cast<int64_t>(n) * 2 * cd.lstride + v;
+                            lg[0] = a0;
+                            lg[cd.lstride] = a1;
+                        } else {
+                            for (int j = 0; j < cd.nclass; ++j) {
+                                float a = s_pred[j];
+                                const float* tab = s_ptab + j * (K / 4) * 256;
+#pragma unroll
+                                for (int qd = 0; qd < K / 4; ++qd) {
+                                    const uint32_t w = qd >> 3, sh = 4 * (qd & 7);
+                                    const uint32_t ix = ((mbits[w] >> sh) & 0xFu) | (((sbits[w] >> sh) & 0xFu) << 4);
+                                    a += tab[qd * 256 + ix];
+                                }
+                                cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
+                            }
+                        }
+                        if (cd.no_yp) return;   // last FCN layer: only the logits are consumed
+                    }
+                    uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
+                    if constexpr (CWO == 1) {
+                        *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
+                    } else {
+                        *reinterpret_cast<uint4*>(dst) = make_uint4(sbits[0], sbits[1], mbits[0], mbits[1]);
+                    }
+                    if (cd.halo_lo != nullptr || cd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes
+                        const uint32_t wds[4] = {sbits[0], CWO == 1 ? mbits[0] : sbits[CWO - 1], mbits[0], mbits[CWO - 1]};
+                        halo_store_words(cd.halo_lo, cd.halo_hi, z, cd.Do, voff, wds, 2 * CWO);
+                    }
+                };
+                // A4 (reading R5) on one 16-channel chunk: acc holds acc - hi (initialised to -hi).
+                // +1 if acc >= hi; else -1 if acc <= lo; else 0.  Bit k of nhi = (acc_k < hi_k); bit k
+                // of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).  F4: f32 accumulators start at 0.5 - hi
+                // and lmh = lo - hi + 1, so d and lmh - d are never zero (acc integer): no
+                // sign-of-zero ambiguity.  Returns sign bits (low 16) and mask bits (high 16).
+                auto requant16 = [&](const int* acc, const int* lmh) {
+                    uint32_t nhi = 0u, nlo = 0u;
+#pragma unroll
+                    for (int i = 15; i >= 0; --i) {
+                        const int d = acc[i];
+                        nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
+                        const int e = F4 ? __float_as_int(__int_as_float(lmh[i]) - __int_as_float(d)) : lmh[i] - d;
+                        nlo = __funnelshift_l(static_cast<uint32_t>(e), nlo, 1);
+                    }
+                    return (~nhi & 0xFFFFu) | ((~(nhi & nlo) & 0xFFFFu) << 16);
+                };
                 for (int v = g; v < NU; v += kZEpiGroups) {   // all units (see the MMA issuer)
-                    mbar_wait(acc_full + sgm * NU + v, par);
+                    TN_TW(6, threadIdx.x == 0, mbar_wait(acc_full + sgm * NU + v, par));
                     tc_fence_after();
                     const int t = v;                      // one tile per unit
                     if (t >= Tv) {                        // past a ragged strip's last tile: no MMAs ran,
@@ -845,11 +946,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         continue;
                     }
                     const uint32_t taddr = tmem_base + lane_base + (t * RO + sgm) * K;
-                    const int qpos = q_lane + t * 128;
-                    const int y = div_po(static_cast<uint32_t>(qpos), pl.po_magic);
-                    const int x = qpos - y * pl.Po;
-                    const bool vpos = x < cd.Wo && y < cd.Ho;
-                    const int voff = y * cd.Wo + x;
+                    int voff;
+                    const bool vpos = position(t, voff);
                     uint32_t sbits[CWO], mbits[CWO];
                     // K <= 32: the whole tile's accumulators go to registers first and the block is
                     // re-initialised and handed back to the MMA issuer at once, so the next MMAs into
@@ -899,21 +997,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             }
                         }
                         if (fused) {
-                            // acc holds acc - hi (initialised to -hi).  A4 (reading R5):
-                            // +1 if acc >= hi; else -1 if acc <= lo; else 0.  Bit k of nhi =
-                            // (acc_k < hi_k); bit k of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).
-                            // F4: f32 accumulators start at 0.5 - hi and lmh = lo - hi + 1, so d and
-                            // lmh - d are never zero (acc integer): no sign-of-zero ambiguity.
-                            uint32_t nhi = 0u, nlo = 0u;
-#pragma unroll
-                            for (int i = 15; i >= 0; --i) {
-                                const int d = acc[i];
-                                nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
-                                const int e = F4 ? __float_as_int(__int_as_float(lmh[i]) - __int_as_float(d)) : lmh[i] - d;
-                                nlo = __funnelshift_l(static_cast<uint32_t>(e), nlo, 1);
-                            }
+                            const uint32_t bits = requant16(acc, lmh);
                             const int w = c >> 5, sh = c & 31;
-                            const uint32_t sb = (~nhi & 0xFFFFu) << sh, mb = (~(nhi & nlo) & 0xFFFFu) << sh;
+                            const uint32_t sb = (bits & 0xFFFFu) << sh, mb = (bits >> 16) << sh;
                             if (sh == 0) { sbits[w] = sb; mbits[w] = mb; }
                             else { sbits[w] |= sb; mbits[w] |= mb; }
                         } else if (vpos) {
@@ -933,58 +1019,20 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         tc_fence_before();
                         mbar_arrive(acc_empty + sgm * NU + v);
                     }
-                    if (fused && vpos) {
-                        if (PRED) {
-                            // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
-                            const int64_t v = static_cast<int64_t>(z) * cd.Ho * cd.Wo + voff;
-                            if (cd.nclass == 2 && K == 16) {
-                                // quad indices (mask nibble | sign nibble << 4): bytes of q02 = quads 0, 2;
-                                // bytes of q13 = quads 1, 3
-                                const uint32_t q02 = (mbits[0] & 0x0F0Fu) | ((sbits[0] & 0x0F0Fu) << 4);
-                                const uint32_t q13 = ((mbits[0] >> 4) & 0x0F0Fu) | (sbits[0] & 0xF0F0u);
-                                const uint32_t idx[4] = {q02 & 0xFFu, q13 & 0xFFu, (q02 >> 8) & 0xFFu, (q13 >> 8) & 0xFFu};
-                                float a0 = s_pred[0], a1 = s_pred[1];
-#pragma unroll
-                                for (int qd = 0; qd < 4; ++qd) {
-                                    const float2 e2 = *reinterpret_cast<const float2*>(s_ptab + (qd * 256 + idx[qd]) * 2);
-                                    a0 += e2.x;
-                                    a1 += e2.y;
-                                }
-                                cd.logits[(static_cast<int64_t>(n) * 2) * cd.lstride + v] = a0;
-                                cd.logits[(static_cast<int64_t>(n) * 2 + 1) * cd.lstride + v] = a1;
-                            } else {
-                                for (int j = 0; j < cd.nclass; ++j) {
-                                    float a = s_pred[j];
-                                    const float* tab = s_ptab + j * (K / 4) * 256;
-#pragma unroll
-                                    for (int qd = 0; qd < K / 4; ++qd) {
-                                        const uint32_t w = qd >> 3, sh = 4 * (qd & 7);
-                                        const uint32_t ix = ((mbits[w] >> sh) & 0xFu) | (((sbits[w] >> sh) & 0xFu) << 4);
-                                        a += tab[qd * 256 + ix];
-                                    }
-                                    cd.logits[(static_cast<int64_t>(n) * cd.nclass + j) * cd.lstride + v] = a;
-                                }
-                            }
-                        }
-                        if (PRED && cd.no_yp) continue;   // last FCN layer: only the logits are consumed
-                        uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
-                        if constexpr (CWO == 1) {
-                            *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
-                        } else {
-                            *reinterpret_cast<uint4*>(dst) = make_uint4(sbits[0], sbits[1], mbits[0], mbits[1]);
-                        }
-                        if (cd.halo_lo != nullptr || cd.halo_hi != nullptr) {   // NEXT-1 slab boundary planes
-                            const uint32_t wds[4] = {sbits[0], CWO == 1 ? mbits[0] : sbits[CWO - 1], mbits[0], mbits[CWO - 1]};
-                            halo_store_words(cd.halo_lo, cd.halo_hi, z, cd.Do, voff, wds, 2 * CWO);
-                        }
-                    }
+                    if (fused && vpos) finish(voff, sbits, mbits);
                 }
             }
         }
     }
 
+#ifdef TN_TRACE
+    if (threadIdx.x == 0) atomicAdd(&g_tn_trace[blockIdx.x * 8 + 7], clock64() - k_t0);   // epilogue warp 0 done
+#endif
     tc_fence_before();
     __syncthreads();
+#ifdef TN_TRACE
+    if (threadIdx.x == 0) atomicAdd(&g_tn_trace[blockIdx.x * 8 + 0], clock64() - k_t0);
+#endif
     if (warp == kZMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
@@ -1086,7 +1134,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(cd.logits != nullptr && !first, ct) * 32;
+    const int exp_threads = tz_exp_warps(cd.K, cd.logits != nullptr && !first, ct) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1285,7 +1333,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
         for (void*& f : configured)
             if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
     }
-    return launch_pdl(kern, grid, tz_threads(pred && K <= 32, ct), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(K, pred && K <= 32, ct), smem, st, cd, pl);
 }
 
 static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
@@ -1361,7 +1409,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    return launch_pdl(kern, grid, tz_threads(false, 1), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
