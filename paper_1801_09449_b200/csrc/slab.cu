@@ -27,9 +27,14 @@ using namespace tn;
 
 
 
+// The communicator owns a comm stream and a pool of events: halo exchanges run on the comm
+// stream, overlapping the interior planes computed on the caller's stream (tn_fcn_forward_slab).
+constexpr int kCommEvents = 96;
 struct tn_comm {
     ncclComm_t comm;
     int rank, nranks;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[kCommEvents] = {};
 };
 
 namespace {
@@ -41,6 +46,7 @@ struct SlabPlan {
     tn_dims g;                               // global input dims
     int z0, z1;
     size_t x_off, x_bytes, x_plane;          // extended float input [z0-1, z1+1)
+    int x_halo;                              // halo sides of the input (bit 0 lower, bit 1 upper)
     std::vector<tn_slab_layer> L;
     size_t total;
 };
@@ -86,10 +92,22 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
         s.c = out[i].c; s.h = out[i].h; s.w = out[i].w;
         s.gd = out[i].d;
         s.z0 = z0 / scale; s.z1 = z1 / scale;
-        s.halo = (i + 1 < nl) ? 1 : 0;       // the last layer only feeds the 1x1x1 prediction
+        s.halo = 0;                          // sides its consumers read (below); the last layer feeds only A8
         s.plane_bytes = static_cast<int64_t>(s.h) * s.w * 2 * ((s.c + 31) / 32) * 4;
         s.offset = static_cast<int64_t>(off);
         off = align_up(off + static_cast<size_t>(s.plane_bytes) * (s.z1 - s.z0 + 2));
+    }
+    // Halo sides each tensor's consumers read: a stride-1 conv (or a nearest-x2 upsampled segment)
+    // reads one plane below and one above its owned range, a stride-2 conv only the plane below
+    // (slab starts are even).  Bit 0 = lower halo, bit 1 = upper halo.
+    sp.x_halo = 0;
+    for (int j = 0; j < nl; ++j) {
+        const tn_layer& ly = net->layers[j];
+        for (int sgi = 0; sgi < ly.nseg; ++sgi) {
+            const int sides = (ly.stride == 1 || ly.upsample[sgi]) ? 3 : 1;
+            if (ly.kind == TN_LAYER_FIRST) sp.x_halo |= sides;
+            else sp.L[ly.src[sgi]].halo |= sides;
+        }
     }
     sp.total = align_up(off);
     return TN_OK;
@@ -98,12 +116,17 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
 // Queue layer i's kernel for one slab (n = 1); the caller then fills the
 // layer's halo planes (if sp.L[i].halo) before any consumer runs.
 // logits/lstride: when i is the last layer, the A8 prediction is fused into it.
+// za, zb: owned output planes [za, zb) of the layer (relative to its slab start; zb < 0 = all).
 tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i, int64_t* d_bad, cudaStream_t s,
-                         float* logits, int64_t lstride, uint32_t* halo_lo = nullptr, uint32_t* halo_hi = nullptr) {
+                         float* logits, int64_t lstride, uint32_t* halo_lo = nullptr, uint32_t* halo_hi = nullptr,
+                         int za = 0, int zb = -1) {
     {
         const tn_layer& ly = net->layers[i];
         const tn_slab_layer& o = sp.L[i];
-        uint32_t* outp = reinterpret_cast<uint32_t*>(ws + o.offset + o.plane_bytes);   // skip the lower halo
+        if (zb < 0) zb = o.z1 - o.z0;
+        if (za >= zb) return TN_OK;
+        uint32_t* outp = reinterpret_cast<uint32_t*>(ws + o.offset + o.plane_bytes * (1 + za));   // skip the lower halo
+        if (logits != nullptr) logits += static_cast<int64_t>(za) * o.h * o.w;
         if (ly.kind == TN_LAYER_FIRST) {
             FirstDesc fd{};
             fd.x = reinterpret_cast<const float*>(ws + sp.x_off);
@@ -112,7 +135,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             fd.t_lo = net->t_lo; fd.t_hi = net->t_hi; fd.wp = ly.wp[0];
             fd.N = 1; fd.K = ly.c_out;
             for (int a = 0; a < 3; ++a) { fd.s[a] = ly.stride; fd.p[a] = 1; fd.dl[a] = 1; }
-            fd.Do = o.z1 - o.z0; fd.Ho = o.h; fd.Wo = o.w; fd.zo_beg = o.z0;
+            fd.Do = zb - za; fd.Ho = o.h; fd.Wo = o.w; fd.zo_beg = o.z0 + za;
             fd.lo = ly.lo; fd.hi = ly.hi; fd.yp = outp; fd.d_bad = d_bad;
             fd.bad_base = static_cast<int64_t>(sp.z0 - 1) * sp.g.h * sp.g.w;
             fd.bad_nstride = static_cast<int64_t>(sp.g.d) * sp.g.h * sp.g.w;
@@ -139,7 +162,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             const int f = ly.upsample[0] ? 2 : 1;
             cd.Dci = s0.gd * f; cd.Hci = s0.h * f; cd.Wci = s0.w * f;
             for (int a = 0; a < 3; ++a) { cd.s[a] = ly.stride; cd.p[a] = 1; cd.dl[a] = 1; }
-            cd.Do = o.z1 - o.z0; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = o.z0;
+            cd.Do = zb - za; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = o.z0 + za;
             cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
             cd.cwo = (ly.c_out + 31) / 32;
             cd.halo_lo = halo_lo; cd.halo_hi = halo_hi;
@@ -163,17 +186,20 @@ tn_status nccl_status(ncclResult_t r, const char* where) {
 
 // Fill the lower / upper halo plane of a buffer of (planes) planes from the
 // neighbouring ranks: my first owned plane goes down, my last goes up.
-tn_status exchange_halo(tn_comm* c, char* buf, int64_t plane_bytes, int planes, cudaStream_t s) {
+// sides: bit 0 = my lower halo is read (so it is received from below, and the rank below
+// receives my first plane as its upper halo only if it reads that side: both ranks derive the
+// same plan, so a send is posted exactly when the peer posts the matching receive).
+tn_status exchange_halo(tn_comm* c, char* buf, int64_t plane_bytes, int planes, int sides, cudaStream_t s) {
     const size_t pb = static_cast<size_t>(plane_bytes);
     ncclResult_t r = ncclGroupStart();
     if (r != ncclSuccess) return nccl_status(r, "ncclGroupStart");
     if (c->rank > 0) {
-        ncclSend(buf + pb, pb, ncclUint8, c->rank - 1, c->comm, s);
-        ncclRecv(buf, pb, ncclUint8, c->rank - 1, c->comm, s);
+        if (sides & 2) ncclSend(buf + pb, pb, ncclUint8, c->rank - 1, c->comm, s);
+        if (sides & 1) ncclRecv(buf, pb, ncclUint8, c->rank - 1, c->comm, s);
     }
     if (c->rank + 1 < c->nranks) {
-        ncclSend(buf + pb * (planes - 2), pb, ncclUint8, c->rank + 1, c->comm, s);
-        ncclRecv(buf + pb * (planes - 1), pb, ncclUint8, c->rank + 1, c->comm, s);
+        if (sides & 1) ncclSend(buf + pb * (planes - 2), pb, ncclUint8, c->rank + 1, c->comm, s);
+        if (sides & 2) ncclRecv(buf + pb * (planes - 1), pb, ncclUint8, c->rank + 1, c->comm, s);
     }
     return nccl_status(ncclGroupEnd(), "halo exchange");
 }
@@ -276,11 +302,11 @@ tn_status p2p_layer(const tn_fcn* net, const SlabView& me, const SlabView& lower
     const tn_slab_layer& o = me.p->L[i];
     uint32_t* hlo = nullptr;
     uint32_t* hhi = nullptr;
-    if (o.halo && lower.base) {
+    if ((o.halo & 2) && lower.base) {       // my first plane = the lower neighbour's upper halo
         const tn_slab_layer& lo = lower.p->L[i];
         hlo = reinterpret_cast<uint32_t*>(lower.base + lo.offset + lo.plane_bytes * (lo.z1 - lo.z0 + 1));
     }
-    if (o.halo && upper.base) hhi = reinterpret_cast<uint32_t*>(upper.base + upper.p->L[i].offset);
+    if ((o.halo & 1) && upper.base) hhi = reinterpret_cast<uint32_t*>(upper.base + upper.p->L[i].offset);
     return run_slab_layer(net, *me.p, me.base, i, d_bad, s, logits, lstride, hlo, hhi);
 }
 
@@ -320,12 +346,23 @@ tn_status tn_comm_init(const void* nccl_unique_id, int32_t rank, int32_t nranks,
     if (st != TN_OK) { delete c; return st; }
     c->rank = rank;
     c->nranks = nranks;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+    for (int i = 0; i < kCommEvents && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        set_error("comm stream/events: %s", cudaGetErrorString(e));
+        tn_comm_destroy(c);
+        return TN_ECUDA;
+    }
     *out = c;
     return TN_OK;
 }
 
 void tn_comm_destroy(tn_comm* c) {
     if (c == nullptr) return;
+    if (c->cs) cudaStreamSynchronize(c->cs);
+    for (int i = 0; i < kCommEvents; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->cs) cudaStreamDestroy(c->cs);
     ncclCommDestroy(c->comm);
     delete c;
 }
@@ -361,24 +398,68 @@ tn_status tn_fcn_forward_slab(const tn_fcn* net, tn_comm* comm, const float* x_s
     if (x_slab == nullptr || logits_slab == nullptr) { set_error("x/logits NULL"); return TN_EINVAL; }
     if ((reinterpret_cast<uintptr_t>(x_slab) | reinterpret_cast<uintptr_t>(logits_slab) |
          reinterpret_cast<uintptr_t>(ws)) & 15u) { set_error("pointers must be 16-byte aligned"); return TN_EALIGN; }
+    const int nl = static_cast<int>(net->layers.size());
+    if (2 * nl + 2 > kCommEvents) { set_error("too many layers for the comm event pool"); return TN_EUNSUPPORTED; }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     char* base = static_cast<char*>(ws);
+    // Overlapped schedule.  Per layer: the interior output planes (which read no halo) are
+    // computed on `s` while the comm stream exchanges the previous layers' halos; then `s`
+    // waits for the halos of this layer's inputs and computes the two boundary planes; their
+    // event starts this layer's exchange (only the sides its consumers read) on the comm
+    // stream.  Event pool: ev[2i] = layer i's boundary planes done, ev[2i+1] = layer i's halos
+    // in place; ev[2nl] / ev[2nl+1] the same for the float input.
+    cudaEvent_t* ev = comm->ev;
+    auto check = [](cudaError_t e, const char* what) -> tn_status {
+        if (e == cudaSuccess) return TN_OK;
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return TN_ECUDA;
+    };
+    auto post_exchange = [&](cudaEvent_t ready, cudaEvent_t done, char* buf, int64_t pb, int planes,
+                             int sides) -> tn_status {
+        tn_status st2 = check(cudaEventRecord(ready, s), "event record");
+        if (st2 == TN_OK) st2 = check(cudaStreamWaitEvent(comm->cs, ready, 0), "comm wait");
+        if (st2 == TN_OK) st2 = exchange_halo(comm, buf, pb, planes, sides, comm->cs);
+        if (st2 == TN_OK) st2 = check(cudaEventRecord(done, comm->cs), "event record");
+        return st2;
+    };
     // own input planes into the extended buffer, then the float halo planes
     cudaError_t e = cudaMemcpyAsync(base + sp.x_off + sp.x_plane, x_slab, sp.x_plane * (z1 - z0),
                                     cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) { set_error("input copy: %s", cudaGetErrorString(e)); return TN_ECUDA; }
-    st = exchange_halo(comm, base + sp.x_off, static_cast<int64_t>(sp.x_plane), z1 - z0 + 2, s);
-    if (st != TN_OK) return st;
-    const int64_t lstride = static_cast<int64_t>(z1 - z0) * global.h * global.w;
-    for (int i = 0; i < static_cast<int>(net->layers.size()); ++i) {
-        st = run_slab_layer(net, sp, base, i, d_bad, s, logits_slab, lstride);
+    if (sp.x_halo) {
+        st = post_exchange(ev[2 * nl], ev[2 * nl + 1], base + sp.x_off, static_cast<int64_t>(sp.x_plane), z1 - z0 + 2,
+                           sp.x_halo);
         if (st != TN_OK) return st;
+    }
+    const int64_t lstride = static_cast<int64_t>(z1 - z0) * global.h * global.w;
+    for (int i = 0; i < nl; ++i) {
+        const tn_layer& ly = net->layers[i];
         const tn_slab_layer& o = sp.L[i];
+        const int dz = o.z1 - o.z0;
+        // interior planes [1, dz - 1): no halo reads
+        if (dz > 2) {
+            st = run_slab_layer(net, sp, base, i, d_bad, s, logits_slab, lstride, nullptr, nullptr, 1, dz - 1);
+            if (st != TN_OK) return st;
+        }
+        // the halos this layer's boundary planes read
+        if (ly.kind == TN_LAYER_FIRST) {
+            if (sp.x_halo && (st = check(cudaStreamWaitEvent(s, ev[2 * nl + 1], 0), "halo wait")) != TN_OK) return st;
+        } else {
+            for (int sgi = 0; sgi < ly.nseg; ++sgi)
+                if ((st = check(cudaStreamWaitEvent(s, ev[2 * ly.src[sgi] + 1], 0), "halo wait")) != TN_OK) return st;
+        }
+        st = run_slab_layer(net, sp, base, i, d_bad, s, logits_slab, lstride, nullptr, nullptr, 0, 1);
+        if (st == TN_OK && dz > 1)
+            st = run_slab_layer(net, sp, base, i, d_bad, s, logits_slab, lstride, nullptr, nullptr, dz - 1, dz);
+        if (st != TN_OK) return st;
         if (o.halo) {
-            st = exchange_halo(comm, base + o.offset, o.plane_bytes, o.z1 - o.z0 + 2, s);
+            st = post_exchange(ev[2 * i], ev[2 * i + 1], base + o.offset, o.plane_bytes, dz + 2, o.halo);
             if (st != TN_OK) return st;
         }
     }
+    // the caller's stream ends after every exchange this forward posted (workspace reuse)
+    for (int i = 0; i < nl; ++i)
+        if (sp.L[i].halo && (st = check(cudaStreamWaitEvent(s, ev[2 * i + 1], 0), "halo wait")) != TN_OK) return st;
     return TN_OK;
 }
 
@@ -418,17 +499,18 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
         return TN_OK;
     };
     // halo exchange of one buffer kind across all slabs (device copies)
-    auto exchange_all = [&](auto offset_of, auto plane_of, auto planes_of) -> tn_status {
+    // (only the halo sides the consumers read: bit 0 lower, bit 1 upper)
+    auto exchange_all = [&](auto offset_of, auto plane_of, auto planes_of, int sides) -> tn_status {
         for (int r = 0; r < nslabs; ++r) {
             const size_t pb = plane_of(r);
             char* mine = B[r] + offset_of(r);
             const int np = planes_of(r);
-            if (r > 0) {
+            if (r > 0 && (sides & 1)) {
                 char* lower = B[r - 1] + offset_of(r - 1);
                 tn_status st = copy(mine, lower + pb * (planes_of(r - 1) - 2), pb);
                 if (st != TN_OK) return st;
             }
-            if (r + 1 < nslabs) {
+            if (r + 1 < nslabs && (sides & 2)) {
                 char* upper = B[r + 1] + offset_of(r + 1);
                 tn_status st = copy(mine + pb * (np - 1), upper + pb, pb);
                 if (st != TN_OK) return st;
@@ -441,26 +523,45 @@ tn_status tn_fcn_forward_slabs_local(const tn_fcn* net, const float* x, tn_dims 
         tn_status st = copy(B[r] + P[r].x_off + xplane, reinterpret_cast<const char*>(x) + xplane * r * dz, xplane * dz);
         if (st != TN_OK) return st;
     }
-    tn_status st = exchange_all([&](int r) { return P[r].x_off; }, [&](int) { return xplane; },
-                                [&](int) { return dz + 2; });
-    if (st != TN_OK) return st;
-    // layer-major across slabs: all slabs' layer i, then exchange its halos
+    // The overlapped schedule of tn_fcn_forward_slab, layer-major across the slabs on one
+    // stream: every slab's interior planes of layer i run BEFORE the halos of layer i - 1 are
+    // copied in (the copies stand for the exchange in flight), then the boundary planes; so
+    // an interior plane that read a halo would see stale data and break bit-identity.
     const int nl = static_cast<int>(net->layers.size());
-    for (int i = 0; i < nl; ++i) {
-        for (int r = 0; r < nslabs; ++r) {
-            const int64_t cstride = static_cast<int64_t>(global.d) * global.h * global.w;
-            float* lg = logits + static_cast<int64_t>(P[r].L.back().z0) * global.h * global.w;
-            st = run_slab_layer(net, P[r], B[r], i, d_bad, s, lg, cstride);
-            if (st != TN_OK) return st;
-        }
-        if (P[0].L[i].halo) {
-            st = exchange_all([&](int r) { return static_cast<size_t>(P[r].L[i].offset); },
+    const int64_t cstride = static_cast<int64_t>(global.d) * global.h * global.w;
+    int pending = -1;                                  // layer whose halo copies are outstanding (-1: input)
+    tn_status st = TN_OK;
+    auto flush = [&]() -> tn_status {
+        tn_status s2 = TN_OK;
+        if (pending < 0) {
+            if (P[0].x_halo)
+                s2 = exchange_all([&](int r) { return P[r].x_off; }, [&](int) { return xplane; },
+                                  [&](int) { return dz + 2; }, P[0].x_halo);
+        } else if (P[0].L[pending].halo) {
+            const int i = pending;
+            s2 = exchange_all([&](int r) { return static_cast<size_t>(P[r].L[i].offset); },
                               [&](int r) { return static_cast<size_t>(P[r].L[i].plane_bytes); },
-                              [&](int r) { return P[r].L[i].z1 - P[r].L[i].z0 + 2; });
-            if (st != TN_OK) return st;
+                              [&](int r) { return P[r].L[i].z1 - P[r].L[i].z0 + 2; }, P[0].L[i].halo);
         }
+        return s2;
+    };
+    for (int i = 0; i < nl && st == TN_OK; ++i) {
+        const int ldz = P[0].L[i].z1 - P[0].L[i].z0;
+        for (int r = 0; r < nslabs && st == TN_OK && ldz > 2; ++r) {
+            float* lg = logits + static_cast<int64_t>(P[r].L.back().z0) * global.h * global.w;
+            st = run_slab_layer(net, P[r], B[r], i, d_bad, s, lg, cstride, nullptr, nullptr, 1, ldz - 1);
+        }
+        if (st == TN_OK) st = flush();
+        for (int r = 0; r < nslabs && st == TN_OK; ++r) {
+            float* lg = logits + static_cast<int64_t>(P[r].L.back().z0) * global.h * global.w;
+            st = run_slab_layer(net, P[r], B[r], i, d_bad, s, lg, cstride, nullptr, nullptr, 0, 1);
+            if (st == TN_OK && ldz > 1)
+                st = run_slab_layer(net, P[r], B[r], i, d_bad, s, lg, cstride, nullptr, nullptr, ldz - 1, ldz);
+        }
+        pending = i;
     }
-    return TN_OK;
+    if (st == TN_OK) st = flush();
+    return st;
 }
 
 tn_status tn_fcn_forward_slabs_local_p2p(const tn_fcn* net, const float* x, tn_dims global, int32_t nslabs,

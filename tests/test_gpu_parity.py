@@ -582,15 +582,19 @@ def test_c3_layer_full_size_sampled(tn, case):
 @pytest.mark.parametrize("shape,nslabs", [((1, 1, 32, 48, 48), 2), ((1, 1, 32, 48, 48), 4),
                                           ((1, 1, 64, 24, 40), 8)])
 def test_fcn_slabs_local_bit_identical(tn, shape, nslabs):
-    """All z-slabs on one device with halos exchanged by device copies (the schedule
-    tn_fcn_forward_slab runs over NCCL) == the whole-volume forward, bit for bit."""
+    """All z-slabs on one device with halos exchanged by device copies (the overlapped schedule
+    tn_fcn_forward_slab runs over NCCL: every interior plane is computed before the previous
+    layer's halos are copied in, the boundary planes after) == the whole-volume forward, bit for
+    bit.  The workspace starts as garbage, so an interior plane that read a halo would differ."""
     x = synth.ct_volume(shape, seed=11)
     p = synth.fcn_params()
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
     xd = dev(x)
     whole = net(xd).cpu().numpy()
     flag = tn.bad_flag()
-    slabs = net.forward_slabs_local(xd, nslabs, d_bad=flag).cpu().numpy()
+    nb = int(tn.lib.tn_fcn_slabs_local_workspace_bytes(net.handle, tn.dims(*shape), nslabs))
+    ws = torch.full((nb,), 0x5A, dtype=torch.uint8, device="cuda")
+    slabs = net.forward_slabs_local(xd, nslabs, ws=ws, d_bad=flag).cpu().numpy()
     assert bad_value(flag) == tn.INT64_MAX
     np.testing.assert_array_equal(slabs, whole)
     ref, _, _ = oracle.fcn_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"])
