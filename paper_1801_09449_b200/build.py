@@ -75,5 +75,8 @@ if __name__ == "__main__":
     if "--trace" in sys.argv:   # profiling build: per-role wait counters (TN_TRACE), libtn_trace.so
         print(build_library(force="--force" in sys.argv, extra=["-DTN_TRACE"],
                             lib_path=os.path.join(HERE, "libtn_trace.so"), obj_dir=os.path.join(HERE, "build_trace")))
+    elif "--check" in sys.argv:  # device bounds checks (TN_CHECK), libtn_check.so
+        print(build_library(force="--force" in sys.argv, extra=["-DTN_CHECK"],
+                            lib_path=os.path.join(HERE, "libtn_check.so"), obj_dir=os.path.join(HERE, "build_check")))
     else:
         print(build_library(force="--force" in sys.argv))

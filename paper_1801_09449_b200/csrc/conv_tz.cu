@@ -46,6 +46,7 @@
 //               of the contiguous packed rows a strip needs, per plane and segment
 #include "tn_internal.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 #include "tc_ptx.cuh"
 
@@ -76,6 +77,23 @@ extern "C" int tn_trace_read(unsigned long long* host, int n, int reset) {
 }
 #else
 #define TN_TW(slot, rec, stmt) stmt
+#endif
+
+// TN_CHECK builds (python paper_1801_09449_b200/build.py --check writes libtn_check.so): device
+// bounds checks on every bulk copy, staged read, A-operand write and output store of the TZ
+// kernel; a violation traps (a loud CUDA error).  The stand-in for compute-sanitizer, which is
+// closed on this GPU pool.
+#ifdef TN_CHECK
+#define TN_ASSERT(c)                                                                                 \
+    do {                                                                                             \
+        if (!(c)) {                                                                                  \
+            printf("TN_CHECK failed: %s (conv_tz.cu:%d) block %d thread %d\n", #c, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                     \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define TN_ASSERT(c) do { } while (0)
 #endif
 
 namespace tn {
@@ -444,9 +462,20 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     }
                     mbar_arrive_expect_tx(staged_full + st, total);
 #pragma unroll
-                    for (int sg = 0; sg < NSEG; ++sg)
+                    for (int sg = 0; sg < NSEG; ++sg) {
+#ifdef TN_CHECK
+                        const char* b0 = FIRST ? reinterpret_cast<const char*>(cd.xf) : reinterpret_cast<const char*>(cd.seg[sg].xp);
+                        const char* s0 = reinterpret_cast<const char*>(src[sg]);
+                        TN_ASSERT(bytes[sg] == 0 ||
+                                  (s0 >= b0 - 15 && s0 + bytes[sg] <= b0 + static_cast<int64_t>(cd.N) * cd.seg[sg].D *
+                                                                             cd.seg[sg].H * cd.seg[sg].W *
+                                                                             (FIRST ? 4 : 8 * cd.seg[sg].cw)));
+                        TN_ASSERT(pl.seg_off[sg] + static_cast<int>(bytes[sg]) <=
+                                  (sg + 1 < NSEG ? pl.seg_off[sg + 1] : pl.stage_bytes));
+#endif
                         if (bytes[sg]) bulk_g2s(s_stage + st * pl.stage_bytes + pl.seg_off[sg], src[sg], bytes[sg],
                                                 staged_full + st);
+                    }
                     if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                 }
             }
@@ -592,6 +621,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 src = pbase[sg] + static_cast<uint32_t>(L * BPV);
                             const bool ok = v && zok[sg];
                             const uint32_t dst = arow + (ph * pl.nreg + pl.reg0[sg]) * pl.REG;
+                            TN_ASSERT(dst + (CS > 32 ? pl.REG + 16 : 16) <= smem_u32(slot) + pl.slot_bytes && dst >= smem_u32(slot) + 8);
+                            TN_ASSERT(!(v && zok[sg]) || (src >= smem_u32(stg) + pl.seg_off[sg] &&
+                                                          src + BPV <= smem_u32(stg) + pl.stage_bytes));
                             if constexpr (CS == 16) {
                                 uint2 w = make_uint2(0u, 0u);
                                 if (ok) w = lds64(src);
@@ -910,6 +942,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         }
                         if (cd.no_yp) return;   // last FCN layer: only the logits are consumed
                     }
+                    TN_ASSERT(voff >= 0 && voff < cd.Ho * cd.Wo && vplane + voff < static_cast<int64_t>(cd.N) * cd.Do * cd.Ho * cd.Wo);
                     uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
                     if constexpr (CWO == 1) {
                         *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
@@ -1007,6 +1040,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                                 for (int i = 0; i < 16; ++i) acc[i] = __float2int_rn(__int_as_float(acc[i]));
                             }
+                            TN_ASSERT(vplane + voff < static_cast<int64_t>(cd.N) * cd.Do * cd.Ho * cd.Wo);
                             int4* dst = reinterpret_cast<int4*>(cd.y + (vplane + voff) * K + c);
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
