@@ -148,6 +148,9 @@ struct TzPlan {
     int code_off, code_pitch, code_bytes;   // FIRST: ternary code planes (2 buffers) after the stages
     int wpad;               // bytes after the code planes so that the packed filter bank fits from s_a on
     int ptab_floats;
+    int kp;                 // output channels padded to the kernel's K (16 / 32 / 64)
+    int dil;                // in-plane dilation (taps dy*dil*Po + dx*dil); z dilation = residue classes
+    int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
 };
 
 // q / Po for 0 <= q with q * Po < 2^32
@@ -184,11 +187,11 @@ __device__ __forceinline__ void run_planes(const TzPlan& pl, const ConvDesc& cd,
 // Source rows of segment sg that the strip's A rows read: [ya, ya + nrows).
 __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd, int strip, int sg, int& ya,
                                            int& nrows) {
-    const int qa = strip * 128 * pl.T - pl.Po - 1;
+    const int qa = strip * 128 * pl.T - pl.qoff;
     const int qb = qa + pl.RS - 1;
-    const uint32_t two = 2u * pl.Po;
-    int ylo = div_po(static_cast<uint32_t>(qa) + two, pl.po_magic) - 2;
-    int yhi = div_po(static_cast<uint32_t>(qb) + two, pl.po_magic) - 2;
+    const uint32_t two = static_cast<uint32_t>(pl.yoff * pl.Po);
+    int ylo = div_po(static_cast<uint32_t>(qa) + two, pl.po_magic) - pl.yoff;
+    int yhi = div_po(static_cast<uint32_t>(qb) + two, pl.po_magic) - pl.yoff;
     if (pl.s == 2) { ylo = 2 * ylo; yhi = 2 * yhi + 1; }
     ylo = max(ylo, 0);
     yhi = min(yhi, cd.Hci - 1);
@@ -249,12 +252,15 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     const bool fused = cd.yp != nullptr;
     const int T = pl.T;
     const int NU = T;      // synchronisation units per strip: one per tile
+    const int zst = cd.zstep > 0 ? cd.zstep : 1;           // dilation: plane step of the residue class
+    const int64_t dbuf = cd.Dbuf > 0 ? cd.Dbuf : cd.Do;    // output buffer depth
 
     // ---- setup: stage the packed filter bank (cp.async) in the A ring, expand it
     // into the B image, thresholds, barriers, TMEM.
     {
-        int hi_r = 0, lo_r = 0;
-        if (fused && threadIdx.x < K) {
+        // channels k >= cd.K (K padded to 16 / 32 / 64) have zero filters and "always 0" thresholds
+        int hi_r = 1 << 20, lo_r = -(1 << 20);
+        if (fused && threadIdx.x < cd.K) {
             lo_r = clamp_threshold(__ldg(cd.lo + threadIdx.x));
             hi_r = clamp_threshold(__ldg(cd.hi + threadIdx.x));
         }
@@ -263,13 +269,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         int ofs = 0;
 #pragma unroll
         for (int sg = 0; sg < NSEG; ++sg) {
-            const int n4 = K * 27 * 2 * (FIRST ? 1 : cd.seg[sg].cw) / 4;
+            const int nw = cd.K * 27 * 2 * (FIRST ? 1 : cd.seg[sg].cw);   // words (odd K: not a multiple of 4)
+            const int n4 = nw / 4;
             const uint4* g = reinterpret_cast<const uint4*>(cd.seg[sg].wp);
             for (int i = threadIdx.x; i < n4; i += kZThreads)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_wp + ofs + 4 * i)), "l"(g + i)
                              : "memory");
+            for (int i = 4 * n4 + threadIdx.x; i < nw; i += kZThreads)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_wp + ofs + i)),
+                             "l"(cd.seg[sg].wp + i)
+                             : "memory");
             wsrc[sg] = s_wp + ofs;
-            ofs += 4 * n4;
+            ofs += (nw + 3) & ~3;
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
         if (threadIdx.x < K) {
@@ -305,7 +316,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             const int b = row / K, k = row - b * K;
             const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            const int tap = pl.sl_tap[j];
+            const int tap = k < cd.K ? pl.sl_tap[j] : -1;    // padded output channels: zero filters
             if (FIRST) {
                 if (j == 0) {   // byte (dy*3 + dx) = w[k][0][dz][dy][dx]
                     uint32_t wv[4] = {0u, 0u, 0u, 0u};
@@ -322,7 +333,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     const int sg = pl.sl_seg[j];
                     const int cw = cd.seg[sg].cw;
                     const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
-                    if (cd.seg[sg].c == 16) {       // [tap a ch 0-15 | tap b ch 0-15]
+                    if (cd.seg[sg].c <= 16) {       // [tap a ch 0-15 | tap b ch 0-15]
                         const uint2 a2 = expand16_f4(src[0], src[cw], 0);
                         uint2 b2 = make_uint2(0u, 0u);
                         const int tb = pl.sl_tapb[j];
@@ -407,7 +418,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     __syncthreads();
     tc_fence_after();
 
-    const uint32_t two_po = 2u * pl.Po;
+    const uint32_t two_po = static_cast<uint32_t>(pl.yoff * pl.Po);   // keeps raster dividends >= 0
     if (warp == kZLoadWarp) {
         // ================= loader: per plane and segment one bulk copy of the
         // contiguous packed rows the strip reads (zero-size outside the buffer)
@@ -429,7 +440,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                     for (int sg = 0; sg < NSEG; ++sg) {
                         const SegDesc& sd = cd.seg[sg];
-                        const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
+                        const int zs = (sd.up ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
                         const bool ok = zs >= 0 && zs < sd.D && nr[sg] > 0;
                         if (FIRST) {
                             bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 4u : 0u;
@@ -494,7 +505,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             int ya[kMaxSeg], nr[kMaxSeg];
 #pragma unroll
             for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
-            const int qa = strip * 128 * T - pl.Po - 1;
+            const int qa = strip * 128 * T - pl.qoff;
             for (int i = i0; i <= i1; ++i) {
                 TN_TW(2, et == 0, mbar_wait(staged_full + st, st_r & 1));
                 if (as_r > 0) TN_TW(3, et == 0, mbar_wait(plane_free + as, (as_r - 1) & 1));
@@ -503,7 +514,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) {
                     const SegDesc& sd = cd.seg[sg];
-                    const int zs = (sd.up ? (i >> 1) : i) - sd.zbeg;
+                    const int zs = (sd.up ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
                     zok[sg] = zs >= 0 && zs < sd.D;
                     head[sg] = FIRST ? 0u : static_cast<uint32_t>(reinterpret_cast<uintptr_t>(
                         sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw)) & 15u;
@@ -592,8 +603,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 int y, x;
                 {
                     const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
-                    y = div_po(tq, pl.po_magic) - 2;
-                    x = static_cast<int>(tq) - (y + 2) * pl.Po;
+                    y = div_po(tq, pl.po_magic) - pl.yoff;
+                    x = static_cast<int>(tq) - (y + pl.yoff) * pl.Po;
                 }
                 const int Wp = cd.seg[NSEG - 1].W;
                 int L = y * Wp + x;
@@ -657,8 +668,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 int y, x;
                 {
                     const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
-                    y = div_po(tq, pl.po_magic) - 2;
-                    x = static_cast<int>(tq) - (y + 2) * pl.Po;
+                    y = div_po(tq, pl.po_magic) - pl.yoff;
+                    x = static_cast<int>(tq) - (y + pl.yoff) * pl.Po;
                 }
                 for (; r < pl.RS; r += kZExpThreads) {
                     const bool vx = x < cd.Wo && y >= 0;
@@ -896,7 +907,8 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             const int q_lane = strip * 128 * T + 32 * q + lane;
             for (int z = zf; z <= zl; ++z, ++u) {
                 const uint32_t sgm = u % RO, par = (u / RO) & 1;
-                const int64_t vplane = (static_cast<int64_t>(n) * cd.Do + z) * cd.Ho * cd.Wo;
+                const int zg = cd.zres + z * zst;                   // output plane in the buffer
+                const int64_t vplane = (static_cast<int64_t>(n) * dbuf + zg) * cd.Ho * cd.Wo;
                 // raster position of this lane in tile t -> (offset within the plane, valid)
                 auto position = [&](int t, int& voff) {
                     const int qpos = q_lane + t * 128;
@@ -910,7 +922,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 auto finish = [&](int voff, const uint32_t (&sbits)[CWO], const uint32_t (&mbits)[CWO]) {
                     if (PRED) {
                         // A8 (reading R12): b + sum_k w_k t_k in fp32, k ascending (quad tables)
-                        const int64_t v = static_cast<int64_t>(z) * cd.Ho * cd.Wo + voff;
+                        const int64_t v = static_cast<int64_t>(zg) * cd.Ho * cd.Wo + voff;
                         if (cd.nclass == 2 && K == 16) {
                             // quad indices (mask nibble | sign nibble << 4): bytes of q02 = quads 0, 2;
                             // bytes of q13 = quads 1, 3
@@ -942,7 +954,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         }
                         if (cd.no_yp) return;   // last FCN layer: only the logits are consumed
                     }
-                    TN_ASSERT(voff >= 0 && voff < cd.Ho * cd.Wo && vplane + voff < static_cast<int64_t>(cd.N) * cd.Do * cd.Ho * cd.Wo);
+                    TN_ASSERT(voff >= 0 && voff < cd.Ho * cd.Wo && vplane + voff < static_cast<int64_t>(cd.N) * dbuf * cd.Ho * cd.Wo);
                     uint32_t* dst = cd.yp + (vplane + voff) * 2 * CWO;
                     if constexpr (CWO == 1) {
                         *reinterpret_cast<uint2*>(dst) = make_uint2(sbits[0], mbits[0]);
@@ -1040,11 +1052,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                                 for (int i = 0; i < 16; ++i) acc[i] = __float2int_rn(__int_as_float(acc[i]));
                             }
-                            TN_ASSERT(vplane + voff < static_cast<int64_t>(cd.N) * cd.Do * cd.Ho * cd.Wo);
-                            int4* dst = reinterpret_cast<int4*>(cd.y + (vplane + voff) * K + c);
+                            TN_ASSERT(vplane + voff < static_cast<int64_t>(cd.N) * dbuf * cd.Ho * cd.Wo);
+                            if (cd.K == K) {
+                                int4* dst = reinterpret_cast<int4*>(cd.y + (vplane + voff) * K + c);
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                dst[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+                                for (int i = 0; i < 4; ++i)
+                                    dst[i] = make_int4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+                            } else {   // padded K: the logical channels only (row pitch cd.K)
+                                int32_t* dst = cd.y + (vplane + voff) * cd.K;
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (c + i < cd.K) dst[c + i] = acc[i];
+                            }
                         }
                         if constexpr (!EARLY) reinit(c);
                     }
@@ -1118,23 +1137,30 @@ static int tz_num_sms() {
 static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 = false) {
     constexpr size_t kSmemMax = 227 * 1024;
     if (cd.nseg < 1 || cd.nseg > 2) return false;
+    // isotropic: stride 1 or 2 with pad 1, or stride 1 with pad = dilation > 1 (int8 operands,
+    // one plain segment; the caller launches each z residue class mod the dilation separately)
     for (int a = 0; a < 3; ++a)
-        if (cd.s[a] != cd.s[0] || cd.p[a] != 1 || cd.dl[a] != 1) return false;
+        if (cd.s[a] != cd.s[0] || cd.p[a] != cd.dl[0] || cd.dl[a] != cd.dl[0]) return false;
     pl.s = cd.s[0];
+    pl.dil = cd.dl[0];
+    if (pl.dil < 1 || (pl.dil > 1 && (pl.s != 1 || f4 || first || cd.nseg != 1))) return false;
     if (pl.s != 1 && !(pl.s == 2 && cd.nseg == 1 && cd.seg[0].up == 0)) return false;
     // the kernel fixes the segment pattern: one plain segment, or [nearest-x2 upsampled, plain]
     if (cd.nseg == 1 ? cd.seg[0].up != 0 : (cd.seg[0].up != 1 || cd.seg[1].up != 0)) return false;
-    if (cd.K != 16 && cd.K != 32 && cd.K != 64) return false;
-    if (cd.logits != nullptr && (cd.K > 32 || cd.nclass < 1 || cd.nclass > kZMaxClass || cd.yp == nullptr ||
-                                 cd.nclass * cd.K > 64))
+    // K padded to the next of 16 / 32 / 64 (zero filters, "always 0" thresholds for the pad)
+    if (cd.K < 1 || cd.K > 64) return false;
+    pl.kp = cd.K <= 16 ? 16 : (cd.K <= 32 ? 32 : 64);
+    if (cd.logits != nullptr && (cd.K != pl.kp || cd.K > 32 || cd.nclass < 1 || cd.nclass > kZMaxClass ||
+                                 cd.yp == nullptr || cd.nclass * cd.K > 64))
         return false;
     int ct = 0;
     pl.cch[1] = 0;
     for (int i = 0; i < cd.nseg && !first; ++i) {
         const SegDesc& sd = cd.seg[i];
-        if (sd.c <= 0 || sd.c % 16 != 0 || (sd.c + 31) / 32 != sd.cw) return false;
+        // 16-channel chunks; padding lanes are zero in the packed format (reading R4)
+        if (sd.c <= 0 || sd.c > 64 || (sd.c + 31) / 32 != sd.cw) return false;
         if ((reinterpret_cast<uintptr_t>(sd.xp) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
-        pl.cch[i] = sd.c / 16;
+        pl.cch[i] = (sd.c + 15) / 16;
         ct += pl.cch[i];
     }
     if (first) {   // one float input channel; 9 in-plane taps per 16-byte A row
@@ -1150,25 +1176,27 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.nreg = 0;
     for (int i = 0; i < cd.nseg; ++i) {
         pl.reg0[i] = pl.nreg;
-        pl.nreg += f4 ? std::max(1, cd.seg[i].c / 32) : 0;
+        pl.nreg += f4 ? (cd.seg[i].c + 31) / 32 : 0;
     }
     // z-slabs: the launch covers global output planes [zo_beg, zo_beg + Do) of the layer
     // (segment buffers start at global plane zbeg); y and x are always whole
     if (cd.zo_beg < 0 || cd.zo_beg + cd.Do > out_extent(cd.Dci, pl.s, 1, 1) ||
-        cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) || cd.Wo != out_extent(cd.Wci, pl.s, 1, 1))
+        cd.Ho != out_extent(cd.Hci, pl.s, pl.dil, pl.dil) || cd.Wo != out_extent(cd.Wci, pl.s, pl.dil, pl.dil))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    const bool split = pl.s == 1 && cd.K == 64;
+    const bool split = pl.s == 1 && pl.kp == 64;
     pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
-    pl.Po = cd.Wo + 1;
+    pl.Po = cd.Wo + pl.dil;                    // dil zero separator columns per raster row
+    pl.qoff = pl.dil * pl.Po + pl.dil;
+    pl.yoff = pl.dil + 1;
     const int64_t npo = static_cast<int64_t>(cd.Ho) * pl.Po;
-    if (npo + 4 * pl.Po > (1 << 22) || pl.Po > 1024) return false;   // div_po range: q * Po < 2^32
+    if (npo + (2 * pl.yoff + 2) * pl.Po > (1 << 22) || pl.Po > 1024) return false;   // div_po range: q * Po < 2^32
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(cd.K, cd.logits != nullptr && !first, ct) * 32;
+    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1186,7 +1214,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                 ox = dx == 0 ? 0 : 1;
                 ph = py * 2 + px;
             }
-            for (int c = 0; c < ct; ++c) sl.push_back({ph, c, oy * pl.Po + ox, dy * 3 + dx});
+            for (int c = 0; c < ct; ++c) sl.push_back({ph, c, pl.dil * (oy * pl.Po + ox), dy * 3 + dx});
         }
     std::sort(sl.begin(), sl.end(), [](const Sl& a, const Sl& b) {
         if (a.ph != b.ph) return a.ph < b.ph;
@@ -1218,7 +1246,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                 std::sort(tp.begin(), tp.end(), [](const Tp& a, const Tp& b) {
                     return a.ph != b.ph ? a.ph < b.ph : a.ox < b.ox;
                 });
-                if (C == 16) {
+                if (C <= 16) {
                     for (size_t i = 0; i < tp.size();) {
                         const bool pair = i + 1 < tp.size() && tp[i + 1].ph == tp[i].ph && tp[i + 1].ox == tp[i].ox + 1;
                         sl4.push_back({tp[i].ph, pl.reg0[sg], tp[i].oy * pl.Po + tp[i].ox, tp[i].tap,
@@ -1227,7 +1255,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                     }
                 } else {
                     for (const Tp& t : tp)
-                        for (int c = 0; c < C / 32; ++c)
+                        for (int c = 0; c < (C + 31) / 32; ++c)
                             sl4.push_back({t.ph, pl.reg0[sg] + c, t.oy * pl.Po + t.ox, t.tap, -1, sg, c});
                 }
             }
@@ -1245,12 +1273,12 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
             cd.nseg == 1 ? (ct == 1 ? 3 : (ct == 2 ? 5 : 9)) : (ct == 2 ? 6 : (ct == 3 ? 8 : (ct == 4 ? 9 : 18)));
         if (pl.nmma > kZMaxMma || pl.nmma != (f4 ? nmma_f4 : first ? 1 : (9 * ct + 1) / 2)) return false;   // kernel unrolls
     }
-    pl.b_bytes = pl.nmma * 2 * pl.NB * cd.K * 16;
-    const int ptab = cd.logits != nullptr ? cd.nclass * (cd.K / 4) * 256 : 0;
+    pl.b_bytes = pl.nmma * 2 * pl.NB * pl.kp * 16;
+    const int ptab = cd.logits != nullptr ? cd.nclass * (pl.kp / 4) * 256 : 0;
     pl.ptab_floats = ptab;
 
     // strip size: the most tiles that fit TMEM (RO*K*T <= 512) and shared memory
-    const int tmax = std::min((f4 ? 480 : 512) / (pl.RO * cd.K), kZMaxAcc / pl.RO);   // F4: scales at 480..511
+    const int tmax = std::min((f4 ? 480 : 512) / (pl.RO * pl.kp), kZMaxAcc / pl.RO);   // F4: scales at 480..511
     bool ok = false;
     // smaller strips when the layer would otherwise give fewer units than SMs (the
     // R3 layers: 16 planes of 9 tiles), so every SM gets work
@@ -1262,7 +1290,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     for (int T = tstart; T >= 1 && !ok; --T) {
         pl.T = T;
         pl.nstrip = (pl.NT + T - 1) / T;
-        pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.Po + 2 : pl.Po + 1);
+        pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.qoff : pl.Po + 1);
         pl.REG = round_up((pl.RS + (f4 ? 1 : 0)) * 16, 128);    // F4: a 16-byte guard row first
         pl.slot_bytes = first ? 128 * T * 16 + 256 : pl.nph * (f4 ? pl.nreg : ct) * pl.REG + 256;
         // staging: the most rows any strip reads, per segment
@@ -1271,8 +1299,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
             const SegDesc& sd = cd.seg[sg];
             int maxr = 0;
             for (int st = 0; st < pl.nstrip; ++st) {
-                const int qa = st * 128 * T - pl.Po - 1, qb = qa + pl.RS - 1;
-                int ylo = (qa + 2 * pl.Po) / pl.Po - 2, yhi = (qb + 2 * pl.Po) / pl.Po - 2;
+                const int qa = st * 128 * T - pl.qoff, qb = qa + pl.RS - 1;
+                int ylo = (qa + pl.yoff * pl.Po) / pl.Po - pl.yoff, yhi = (qb + pl.yoff * pl.Po) / pl.Po - pl.yoff;
                 if (pl.s == 2) { ylo *= 2; yhi = 2 * yhi + 1; }
                 ylo = std::max(ylo, 0);
                 yhi = std::min(yhi, cd.Hci - 1);
@@ -1292,14 +1320,14 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         pl.code_off = 0;
         // packed filter bank staged in the A ring during setup
         int wbytes = 0;
-        for (int sg = 0; sg < cd.nseg; ++sg) wbytes += cd.K * 27 * 2 * (first ? 1 : cd.seg[sg].cw) * 4;
+        for (int sg = 0; sg < cd.nseg; ++sg) wbytes += ((cd.K * 27 * 2 * (first ? 1 : cd.seg[sg].cw) + 3) & ~3) * 4;
         for (int ns = kZMaxSlot; ns >= 2 && !ok; --ns)
             for (int nst = kZMaxStage; nst >= 2 && !ok; --nst) {
                 pl.nslot = ns;
                 pl.nstage = nst;
                 const int span = pl.nslot * pl.slot_bytes + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes;
                 pl.wpad = round_up(std::max(0, wbytes - span), 128);
-                if (tz_smem(pl, cd.K) <= kSmemMax) ok = true;
+                if (tz_smem(pl, pl.kp) <= kSmemMax) ok = true;
             }
     }
     if (!ok) return false;
@@ -1374,11 +1402,11 @@ static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
     int ct = 0;
     for (int i = 0; i < cd.nseg; ++i) {
         ct += pl.cch[i];
-        // FP4 rows hold 16 channels (two positions) or whole 32-channel groups
-        if (pl.f4 && cd.seg[i].c != 16 && cd.seg[i].c % 32 != 0) return false;
+        // FP4 rows hold up to 16 channels (two positions) or whole 32-channel groups
+        if (pl.f4 && pl.cch[i] != 1 && pl.cch[i] % 2 != 0) return false;
     }
     if (pl.f4 && ct == 3) return false;
-    if (ct == 8) return pl.f4 && cd.K == 64 && pl.s == 1 && cd.nseg == 2;
+    if (ct == 8) return pl.f4 && pl.kp == 64 && pl.s == 1 && cd.nseg == 2;
     if (cd.nseg == 1) return ct >= 1 && ct <= 4;
     return pl.s == 1 && ct >= 2;
 }
@@ -1419,14 +1447,14 @@ bool conv_tz_first_supported(const FirstDesc& fd) {
     if (fd.K != 16 && fd.K != 32) return false;
     const ConvDesc cd = first_desc(fd);
     TzPlan pl{};
-    return plan_tz(cd, pl, true) && tz_smem(pl, cd.K) <= 227 * 1024;
+    return plan_tz(cd, pl, true) && tz_smem(pl, pl.kp) <= 227 * 1024;
 }
 
 cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
     const ConvDesc cd = first_desc(fd);
     TzPlan pl{};
     if ((fd.K != 16 && fd.K != 32) || !plan_tz(cd, pl, true)) return cudaErrorNotSupported;
-    const size_t smem = tz_smem(pl, cd.K);
+    const size_t smem = tz_smem(pl, pl.kp);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     if (g_num_sms_z == 0) {
         int dev = 0;
@@ -1457,30 +1485,63 @@ static bool plan_any(const ConvDesc& cd, TzPlan& pl, bool allow_f4) {
     for (int i = 0; i < cd.nseg; ++i) c_tot += cd.seg[i].c;
     // C > 64 (the 64 + 64 -> 64 decoder block) only fits with FP4 operands (half the B bytes)
     allow_f4 = allow_f4 && ((cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16)) || c_tot > 64);
-    if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024)
+    if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, pl.kp) <= 227 * 1024)
         return true;
     pl = TzPlan{};
-    if (plan_tz(cd, pl, false, false) && tz_instantiated(cd, pl) && tz_smem(pl, cd.K) <= 227 * 1024) return true;
+    if (plan_tz(cd, pl, false, false) && tz_instantiated(cd, pl) && tz_smem(pl, pl.kp) <= 227 * 1024) return true;
     // shapes the int8 operands do not fit (e.g. 64 -> 64 at stride 2): FP4 if allowed at all
     pl = TzPlan{};
     return allow_any_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) &&
-           tz_smem(pl, cd.K) <= 227 * 1024;
+           tz_smem(pl, pl.kp) <= 227 * 1024;
+}
+
+// Dilation d > 1 (stride 1, pad d): output plane z reads input planes z - d, z, z + d, all in
+// z's residue class mod d, so class r (planes r, r + d, ...) is an undilated-in-z conv of
+// ceil((D - r) / d) planes; one launch per class.  Whole volumes only (no z-slabs).
+static int dil_classes(const ConvDesc& cd) { return cd.dl[0] > 1 ? cd.dl[0] : 1; }
+static ConvDesc dil_class(const ConvDesc& cd, int r) {
+    ConvDesc c = cd;
+    if (cd.dl[0] <= 1) return c;
+    const int d = cd.dl[0];
+    c.zstep = d;
+    c.zres = r;
+    c.Dbuf = cd.Do;
+    c.Do = cd.Do > r ? (cd.Do - r + d - 1) / d : 0;
+    c.Dci = c.Do;
+    c.zo_beg = 0;
+    return c;
+}
+static bool dil_ok(const ConvDesc& cd) {
+    return cd.dl[0] <= 1 || (cd.zo_beg == 0 && cd.Do == cd.Dci && cd.nseg == 1 && cd.seg[0].zbeg == 0);
 }
 
 bool conv_tz_supported(const ConvDesc& cd, bool allow_f4) {
     TzPlan pl{};
-    return plan_any(cd, pl, allow_f4);
+    return dil_ok(cd) && plan_any(dil_class(cd, 0), pl, allow_f4);
 }
 
 bool conv_tz_uses_f4(const ConvDesc& cd, bool allow_f4) {
     TzPlan pl{};
-    return plan_any(cd, pl, allow_f4) && pl.f4;
+    return dil_ok(cd) && plan_any(dil_class(cd, 0), pl, allow_f4) && pl.f4;
 }
 
+static cudaError_t launch_conv_tz_one(const ConvDesc& cd, cudaStream_t st, bool allow_f4);
+
 cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
+    if (!dil_ok(cd)) return cudaErrorNotSupported;
+    for (int r = 0; r < dil_classes(cd); ++r) {
+        const ConvDesc c = dil_class(cd, r);
+        if (c.Do == 0) continue;
+        cudaError_t e = launch_conv_tz_one(c, st, allow_f4);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+static cudaError_t launch_conv_tz_one(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
     TzPlan pl{};
     if (!plan_any(cd, pl, allow_f4)) return cudaErrorNotSupported;
-    const size_t smem = tz_smem(pl, cd.K);
+    const size_t smem = tz_smem(pl, pl.kp);
     if (g_num_sms_z == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1490,7 +1551,7 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
     const int grid = static_cast<int>(std::min<int64_t>(pl.units, cap));
     int ct = 0;
     for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
-    switch (cd.K) {
+    switch (pl.kp) {
         case 16: return launch_tz_k<16>(cd, pl, ct, grid, smem, st);
         case 32: return launch_tz_k<32>(cd, pl, ct, grid, smem, st);
         case 64: return launch_tz_k<64>(cd, pl, ct, grid, smem, st);

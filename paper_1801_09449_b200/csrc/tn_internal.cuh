@@ -64,6 +64,10 @@ struct ConvDesc {
     // slabs' halo planes, in peer memory over NVLink (or another slab's buffer on one device).
     uint32_t* halo_lo;
     uint32_t* halo_hi;
+    // Dilation (tensor-core kernel, stride 1, pad = dilation): a launch covers one residue class
+    // of planes z = zres + j * zstep; Do / Dci / zo_beg then count class planes and Dbuf is the
+    // output buffer's depth.  zstep == 0 means 1 (no classes), Dbuf == 0 means Do.
+    int zstep, zres, Dbuf;
 };
 
 struct FirstDesc {

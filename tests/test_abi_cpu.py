@@ -121,8 +121,12 @@ def test_kernel_selection_host_logic(tn):
         ([d(1, 16, 9, 17, 35)], None, 16, tn.geom(), tz),                  # odd W: aligned bulk rows
         ([d(1, 48, 9, 17, 35)], None, 32, tn.geom(), tz),                  # three 16-channel chunks
         ([d(1, 64, *R2)], None, 64, tn.geom(2), tz),                       # #7
-        ([d(1, 16, 11, 12, 13)], None, 16, tn.geom(1, 2, 2), popc),        # dilation 2
-        ([d(1, 33, 6, 7, 8)], None, 5, tn.geom(), popc),                   # ragged C, K = 5
+        ([d(1, 16, 11, 12, 13)], None, 16, tn.geom(1, 2, 2), tz),          # dilation 2: z residue classes
+        ([d(1, 16, 11, 12, 13)], None, 16, tn.geom(1, 1, 2), popc),        # pad != dilation
+        ([d(1, 33, 6, 7, 8)], None, 5, tn.geom(), tz),                     # ragged C, K = 5: padded chunks
+        ([d(1, 1, 5, 6, 7)], None, 3, tn.geom(), tz),                      # one channel, K = 3
+        ([d(1, 128, 4, 5, 6)], None, 16, tn.geom(), popc),                 # C > 64: beyond the filter bank
+        ([d(1, 16, 5, 6, 7)], None, 7, tn.geom((1, 2, 1), (0, 1, 2), (1, 1, 2)), popc),   # anisotropic
     ]
     for segs, up, k, g, want in cases:
         assert tn.tn_conv_kernel_for(segs, k, g, up) == want, (segs[0].c, k, want)
@@ -130,7 +134,7 @@ def test_kernel_selection_host_logic(tn):
     tn.tn_set_conv_kernel(tn.TN_KERNEL_TZ)
     try:
         assert tn.tn_conv_kernel_for([d(1, 64, 64, 128, 128)], 64, tn.geom()) == tz
-        assert tn.tn_conv_kernel_for([d(1, 33, 6, 7, 8)], 5, tn.geom()) == -1
+        assert tn.tn_conv_kernel_for([d(1, 128, 4, 5, 6)], 16, tn.geom()) == -1
     finally:
         tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
     assert tn.lib.tn_set_conv_kernel(2) == tn.TN_EINVAL

@@ -167,6 +167,11 @@ CONV_CASES = [
     ((2, 32, 4, 6, 9), 32, 1, 1, 1),
     ((1, 48, 5, 6, 11), 16, 1, 1, 1),            # three 16-channel chunks
     ((1, 16, 4, 70, 131), 16, 1, 1, 1),          # several strips, odd rows
+    # dilation on TZ (stride 1, pad = dilation): in-plane taps at dilated offsets, z residue classes
+    ((1, 32, 10, 14, 16), 32, 1, 3, 3),
+    ((2, 16, 7, 9, 20), 64, 1, 2, 2),
+    ((1, 64, 9, 40, 36), 24, 1, 2, 2),           # padded K, several strips
+    ((1, 20, 2, 5, 6), 16, 1, 4, 4),             # fewer planes than the dilation, padded C
 ]
 
 
