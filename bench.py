@@ -401,6 +401,11 @@ def main():
     if not args.no_binary:
         binary = bench_binary(args, tn, torch, dist, world, rank, dev, stream, flush)
 
+    # ---- NEXT-4: Table 1's 2.5D network over one ROI's 138 stacks
+    fcn25 = None
+    if not args.no_fcn:
+        fcn25 = bench_fcn25(args, tn, torch, dist, world, rank, dev, stream)
+
     # ---- configs[4]: one 256x512x512 volume, z-slabs over the ranks (NCCL halos)
     c4 = None
     if not args.no_c4:
@@ -466,6 +471,7 @@ def main():
             "binary": binary,
             "c0": c0,
             "fcn_c2": c2,
+            "fcn25_table1": fcn25,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -509,31 +515,33 @@ def logits_gate(torch, logits, name, p, z0=0, z1=None, dist=None, world=1):
     return f"passed ({checked} sampled logits vs the oracle's values, reading R13 tolerance)"
 
 
-def fcn_layer_work(table, shape, nclass):
-    """Per layer of one forward over `shape` (n,1,D,H,W): algorithmic ternary MACs
-    (27 * C_in * C_out per output voxel) and algorithmic HBM bytes (each input segment's packed
-    buffer read once at its own resolution -- the float volume for the first layer -- plus the
-    packed output written once; the last layer writes fp32 logits instead)."""
-    n, _, D, H, W = shape
+def fcn_layer_work(table, shape, nclass, taps=None):
+    """Per layer of one forward over `shape` (n,C,D,H,W): algorithmic ternary MACs
+    (taps * C_in * C_out per output voxel: 27 for the 3D FCN; 9 / 1 for Table 1's 2D 3x3 / 1x1
+    layers) and algorithmic HBM bytes (each input segment's packed buffer read once at its own
+    resolution -- the float input for the first layer -- plus the packed output written once;
+    the last layer writes fp32 logits instead)."""
+    n, C, D, H, W = shape
     cwb = lambda c: 8 * ((c + 31) // 32)
     outs, res = [], []
     for i, (kind, co, s, segs) in enumerate(table):
         if segs[0][0] < 0:
-            d, h, w, cin, b_in = D, H, W, 1, n * D * H * W * 4
+            d, h, w, cin, b_in = D, H, W, C, n * C * D * H * W * 4
         else:
-            f = 2 if segs[0][1] else 1
-            d, h, w = (outs[segs[0][0]][a] * f for a in (1, 2, 3))
+            f, fz = (2 if segs[0][1] else 1), (2 if segs[0][1] == 1 else 1)
+            d, h, w = outs[segs[0][0]][1] * fz, outs[segs[0][0]][2] * f, outs[segs[0][0]][3] * f
             cin = sum(outs[sj][0] for sj, _ in segs)
             b_in = sum(n * outs[sj][1] * outs[sj][2] * outs[sj][3] * cwb(outs[sj][0]) for sj, _ in segs)
         do, ho, wo = ((v - 1) // s + 1 for v in (d, h, w))
         outs.append((co, do, ho, wo))
         last = i == len(table) - 1
         b_out = n * do * ho * wo * (4 * nclass if last else cwb(co))
-        res.append({"layer": i + 1, "macs": n * do * ho * wo * co * 27 * cin, "bytes": b_in + b_out})
+        tp = 27 if taps is None else taps[i]
+        res.append({"layer": i + 1, "macs": n * do * ho * wo * co * tp * cin, "bytes": b_in + b_out})
     return res
 
 
-def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3):
+def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3, taps=None):
     """Per-layer binding roofline of one FCN forward: each layer's bound is the larger of its
     algorithmic MACs at the fp4 dense tensor peak (4 x measured bf16, the guide's nominal
     ratio; every layer's ternary products are exact in E2M1) and its algorithmic bytes at the
@@ -553,7 +561,7 @@ def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3):
     hbm = peaks.get("hbm_gbs", 6548.2) * 1e9
     mac_peak = FP4_PER_BF16 * peaks.get("bf16_tflops", 1662.6) * 1e12 / 2.0
     per, bound_ms = [], 0.0
-    for wk, t in zip(fcn_layer_work(net.table, tuple(x.shape), net.nclass), ms):
+    for wk, t in zip(fcn_layer_work(net.table, tuple(x.shape), net.nclass, taps), ms):
         tt, th = wk["macs"] / mac_peak * 1e3, wk["bytes"] / hbm * 1e3
         b = max(tt, th)
         bound_ms += b
@@ -601,6 +609,69 @@ def bench_c2(args, tn, torch, dev, stream):
             "config": "C2: one CT-like volume 1x1x96x144x144 (BASELINE configs[2]); every layer bit-exact at "
                       "this size in test_fcn_c2_full_size_matches_oracle", "steps": steps, "parity": parity,
             "roofline": roof}
+
+
+FCN25_TAPS = [9, 9, 9, 9, 9, 9, 1, 1, 9, 9, 9, 9, 9, 9]      # Table 1: 3x3 layers, 1x1 at #7 / #8
+
+
+def bench_fcn25(args, tn, torch, dist, world, rank, dev, stream):
+    """NEXT-4: Table 1's own network (reading R18) -- the ternary 2.5D U-Net on
+    15-slice stacks of 240 x 176 -- over the 138 stacks of one CT-like ROI volume,
+    sharded over the ranks by stack.  Parity-gated on the oracle's logits of stacks 0-3."""
+    p = synth.fcn25_params()
+    x_all = synth.ct_stacks(synth.ROI_STACKS, synth.STACK_H, synth.STACK_W, seed=300)
+    mine = [i for i in range(synth.ROI_STACKS) if i % world == rank]
+    x = torch.from_numpy(np.ascontiguousarray(x_all[mine])).to(dev)
+    del x_all
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"],
+                        table=tn.fcn25_table(), device=dev, c_in=15)
+    ws = net.workspace(tuple(x.shape), dev)
+    logits = torch.empty((x.shape[0], 2, 1, synth.STACK_H, synth.STACK_W), dtype=torch.float32, device=dev)
+    net(x, logits=logits, ws=ws)
+    torch.cuda.synchronize()
+    # stacks 0-3 are this rank's local stacks 0..: rank r holds global stack r at local 0
+    gold = golden()
+    at, ref = gold["fcn25_at"], gold["fcn25_ref"]
+    sel = np.isin(at[:, 0], mine)
+    ok = True
+    if sel.any():
+        a = at[sel].astype(np.int64)
+        a[:, 0] = [mine.index(v) for v in a[:, 0]]
+        idx = tuple(torch.from_numpy(a[:, j]).to(dev) for j in range(5))
+        got = logits[idx].cpu().numpy().astype(np.float64)
+        r = ref[sel].astype(np.float64)
+        scale = np.abs(p["pred_b"]).astype(np.float64)[a[:, 1]] + np.abs(p["pred_w"]).astype(np.float64).sum(1)[a[:, 1]]
+        ok = bool(np.all(np.abs(got - r) <= 1e-5 * np.maximum(np.abs(r), scale)))
+    if world > 1:
+        f = torch.tensor([int(ok)], device=dev)
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+        ok = bool(f.item())
+    if not ok:
+        print(json.dumps({"error": "Table-1 2.5D network logits differ from the oracle; refusing to report"}), flush=True)
+        sys.exit(1)
+    steps = max(2, args.fcn_steps)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        net(x, logits=logits, ws=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    macs = sum(w["macs"] for w in fcn_layer_work(net.table, (1, 15, 1, synth.STACK_H, synth.STACK_W), 2, FCN25_TAPS))
+    roof = fcn_roofline(torch, net, x, logits, ws, stream, ms, bench_peaks(), taps=FCN25_TAPS) if world == 1 else None
+    return {"metric": "Table-1 2.5D U-Net stacks/s", "value": synth.ROI_STACKS / (ms / 1e3), "unit": "stacks/s",
+            "ms_per_volume": ms, "effective_gmacs": synth.ROI_STACKS * macs / (ms / 1e3) / 1e9,
+            "macs_per_stack": macs, "roofline": roof, "steps": steps,
+            "parity": f"passed ({int(sel.sum())} sampled logits of stacks 0-3 vs the oracle's values, R13)",
+            "config": f"{synth.ROI_STACKS} stacks of 15 x {synth.STACK_H} x {synth.STACK_W} (one 138-slice ROI), "
+                      "Table 1 channels 32-64-128-256, 2D convs (3x3, 1x1 at the lowest level), stride-2 rows "
+                      "for AvgPool2D, nearest x2 Upsample2D; layers above 64 channels run on the popc kernel"}
 
 
 def bench_c0(args, tn, torch, dev):

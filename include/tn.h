@@ -124,7 +124,8 @@ tn_status tn_requant(const int32_t* y, tn_dims yd, const int32_t* lo, const int3
 typedef struct {
     const uint32_t* xp;   /* packed segment; if upsample, at LOW resolution      */
     tn_dims d;            /* its dims (low-resolution dims if upsample)          */
-    int32_t upsample;     /* 0 = none, 1 = nearest x2 in z, y and x              */
+    int32_t upsample;     /* 0 = none, 1 = nearest x2 in z, y and x, 2 = nearest x2
+                             in y and x only (the 2D decoders of Table 1, reading R18) */
     const uint32_t* wp;   /* packed weights of this segment [k][27][2][ceil(d.c/32)] */
 } tn_segment;
 tn_status tn_conv3d_seg(const tn_segment* segs /*host array*/, int32_t nseg, int32_t k,
@@ -139,9 +140,9 @@ tn_status tn_conv3d_first(const float* x, tn_dims xd, float t_lo, float t_hi, co
                           uint32_t* yp, int64_t* d_bad, tn_stream stream);
 
 /* ---- A8: prediction, 1x1x1 float conv (reading R12) --- */
-/* tp packed [n][d][h][w][2][1] (td.c <= 32); w float [nclass][td.c]; b float
- * [nclass]; logits float NCDHW [n][nclass][d][h][w].  Sum order: b, then c
- * ascending, fp32.                                                            */
+/* tp packed [n][d][h][w][2][ceil(td.c/32)] (td.c <= 64); w float [nclass][td.c];
+ * b float [nclass]; logits float NCDHW [n][nclass][d][h][w].  Sum order: b, then
+ * channel quads ascending, fp32.                                              */
 tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
                      int32_t nclass, float* logits, tn_stream stream);
 
@@ -156,18 +157,23 @@ typedef struct {
     int32_t dil;             /* >= 1                                              */
     int32_t nseg;            /* 1 or 2 input segments (concatenated in this order) */
     int32_t src[2];          /* producing layer index, or -1 for the input        */
-    int32_t upsample[2];     /* nearest x2 of that segment                        */
+    int32_t upsample[2];     /* nearest x2 of that segment (0 / 1 / 2 as in tn_segment) */
     const uint32_t* wp[2];   /* packed weights per segment (borrowed)             */
     const int32_t* lo;       /* [c_out] (borrowed)                                */
     const int32_t* hi;       /* [c_out] (borrowed)                                */
 } tn_layer;
 typedef struct tn_fcn tn_fcn;
 /* layers: host array, copied.  pred_w [nclass][c_out of the last layer] and
- * pred_b [nclass] are device pointers (borrowed).  t_lo/t_hi: Eq. 6 input band. */
+ * pred_b [nclass] are device pointers (borrowed).  t_lo/t_hi: Eq. 6 input band.
+ * The input may have c >= 1 float channels (e.g. Table 1's 15-slice stacks,
+ * reading R18): layer 0's packed weights are then [c_out][27][2][ceil(c/32)]; with
+ * c == 1 layer 0 is the fused A7 kernel (c_out <= 32), with c > 1 the input is
+ * ternarised and packed first (tn_pack_f32's kernel) and layer 0 is a regular conv.
+ * The last layer has c_out <= 64 (the prediction's input).                     */
 tn_status tn_fcn_create(const tn_layer* layers, int32_t n_layers, float t_lo, float t_hi,
                         const float* pred_w, const float* pred_b, int32_t nclass, tn_fcn** out);
 size_t    tn_fcn_workspace_bytes(const tn_fcn* net, tn_dims xd);
-/* x float [n][1][d][h][w] -> logits float [n][nclass][d][h][w]. */
+/* x float [n][c][d][h][w] -> logits float [n][nclass][d][h][w]. */
 tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
                          size_t ws_bytes, int64_t* d_bad, tn_stream stream);
 void      tn_fcn_destroy(tn_fcn* net);

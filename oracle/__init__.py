@@ -64,6 +64,8 @@ def _load():
     lib.oracle_requant.restype = None
     lib.oracle_upsample2.argtypes = [_i8p, _I, _I, _I, _I, _I, _i8p]
     lib.oracle_upsample2.restype = None
+    lib.oracle_upsample2_yx.argtypes = [_i8p, _I, _I, _I, _I, _I, _i8p]
+    lib.oracle_upsample2_yx.restype = None
     lib.oracle_concat.argtypes = [_i8p, _I, _i8p, _I, _I, _L, _i8p]
     lib.oracle_concat.restype = None
     lib.oracle_predict.argtypes = [_i8p, _I, _I, _L, _I, _f32p, _f32p, _f32p]
@@ -190,6 +192,15 @@ def upsample2(x):
     return y
 
 
+def upsample2_yx(x):
+    """Upsample2D of Table 1 (reading R18): nearest x2 in y and x."""
+    x = np.ascontiguousarray(x, dtype=np.int8)
+    n, c, d, h, w = x.shape
+    y = np.empty((n, c, d, 2 * h, 2 * w), dtype=np.int8)
+    _load().oracle_upsample2_yx(x, n, c, d, h, w, y)
+    return y
+
+
 def concat(a, b):
     """Channel concatenation [a, b] (Table 1 skips)."""
     a = np.ascontiguousarray(a, dtype=np.int8)
@@ -305,3 +316,38 @@ def fold_table(alpha, gamma, beta, mean, var, eps, max_abs_acc):
         y = a * acc + b
         out[c] = np.where(y > 0.5, 1, np.where(y < -0.5, -1, 0))
     return out
+
+
+# --------------------------------------------------------------------------- NEXT-4: Table 1's 2.5D U-Net
+# The paper's own network (Table 1) with ternary blocks, reading R18: each
+# input is a stack of 15 neighbouring CT slices whose slices are the channels of
+# layer #1 ("3x3x15"); every layer is a 2D conv (3x3, or 1x1 at the lowest level as the caption
+# says); the three AvgPool2D rows are stride-2 convs (reading R8); Upsample2D is nearest x2 in y
+# and x; skips #2->#13, #4->#11, #6->#9 concatenated [upsampled, skip]; same padding (R11);
+# 2-class 1x1 float prediction (R12).  A 2D conv here is conv3d on one-plane volumes
+# (d = 1, pad 1 in z: only the kernel's middle plane dz = 1 meets data), so the weights are
+# [cout][cin][3][3][3] whose other planes do not contribute; 1x1 layers use the centre tap only.
+# Entries: (cin, cout, kernel, stride, skip source or None).
+FCN25_LAYERS = [(15, 32, 3, 1, None), (32, 64, 3, 1, None), (64, 64, 3, 2, None), (64, 128, 3, 1, None),
+                (128, 128, 3, 2, None), (128, 256, 3, 1, None), (256, 256, 1, 2, None), (256, 256, 1, 1, None),
+                (512, 256, 3, 1, 5), (256, 128, 3, 1, None), (256, 128, 3, 1, 3), (128, 64, 3, 1, None),
+                (128, 64, 3, 1, 1), (64, 64, 3, 1, None)]
+
+
+def fcn25_forward(x, t_lo, t_hi, weights, lo, hi, pred_w, pred_b, want_acts=False):
+    """Table 1's ternary 2.5D U-Net (reading R18) on stacks x float32 [n][15][1][h][w]:
+    Eq. 6 on the normalised slices, then the 14 blocks (conv -> integer-threshold requant)
+    in table order, the decoder inputs being concat(upsample2_yx(previous), skip), then the
+    1x1 prediction.  Plain composition of the pinned primitives above.
+    Returns (logits [n][2][1][h][w], acts or None, bad index)."""
+    t, bad = tern_f32(x, t_lo, t_hi)
+    acts = []
+    cur = t
+    for i, (cin, cout, k, s, skip) in enumerate(FCN25_LAYERS):
+        inp = concat(upsample2_yx(cur), acts[skip]) if skip is not None else cur
+        assert inp.shape[1] == cin, (i, inp.shape, cin)
+        acc = conv3d(inp, weights[i], stride=s, pad=1)
+        cur = requant(acc, lo[i], hi[i])
+        acts.append(cur)
+    logits = predict(cur, pred_w, pred_b)
+    return logits, (acts if want_acts else None), bad

@@ -261,6 +261,19 @@ void oracle_upsample2(const int8_t* x, int n, int c, int d, int h, int w, int8_t
         y[IDX5(in, ch, z, yy, xx, c, d2, h2, w2)] = x[IDX5(in, ch, z / 2, yy / 2, xx / 2, c, d, h, w)];
 }
 
+/* Upsample2D of Table 1 (the 2D decoder's 2x2     */
+/* upsampling; reading R18): nearest x2 in y and x only, planes unchanged.    */
+void oracle_upsample2_yx(const int8_t* x, int n, int c, int d, int h, int w, int8_t* y)
+{
+    int h2 = 2 * h, w2 = 2 * w;
+    for (int in = 0; in < n; ++in)
+    for (int ch = 0; ch < c; ++ch)
+    for (int z = 0; z < d; ++z)
+    for (int yy = 0; yy < h2; ++yy)
+    for (int xx = 0; xx < w2; ++xx)
+        y[IDX5(in, ch, z, yy, xx, c, d, h2, w2)] = x[IDX5(in, ch, z, yy / 2, xx / 2, c, d, h, w)];
+}
+
 /* Channel concatenation [a, b] ("skip connections ... dense   */
 /* feature concatenation"; Table 1 skip column PAPER.md:154-171).           */
 void oracle_concat(const int8_t* a, int ca, const int8_t* b, int cb, int n, int64_t dhw, int8_t* y)

@@ -360,6 +360,31 @@ def fcn_table():
     ]
 
 
+def fcn25_table():
+    """Table 1's 2.5D U-Net (reading R18) for one-plane inputs [n][15][1][h][w]
+    (15-slice stacks, the slices as layer 1's channels): 2D layers as 3x3x3 convs on one-plane
+    volumes (only the middle kernel plane meets data), channels 32-64-128-256, stride-2 convs for
+    the three AvgPool2D rows, nearest x2 in y and x (upsample 2) for the Upsample2D rows, skips
+    #2->#13, #4->#11, #6->#9 as [upsampled, skip], the 1x1 layers #7/#8 as centre-tap filters."""
+    F, C = TN_LAYER_FIRST, TN_LAYER_CONV
+    return [
+        (F, 32, 1, [(-1, 0)]),           # 1  15 slices -> 32
+        (C, 64, 1, [(0, 0)]),            # 2  -> skip to 13
+        (C, 64, 2, [(1, 0)]),            # 3  (+ AvgPool2D) /2
+        (C, 128, 1, [(2, 0)]),           # 4  -> skip to 11
+        (C, 128, 2, [(3, 0)]),           # 5  /4
+        (C, 256, 1, [(4, 0)]),           # 6  -> skip to 9
+        (C, 256, 2, [(5, 0)]),           # 7  1x1, /8
+        (C, 256, 1, [(6, 0)]),           # 8  1x1
+        (C, 256, 1, [(7, 2), (5, 0)]),   # 9  [up2d(8) | 6]
+        (C, 128, 1, [(8, 0)]),           # 10
+        (C, 128, 1, [(9, 2), (3, 0)]),   # 11 [up2d(10) | 4]
+        (C, 64, 1, [(10, 0)]),           # 12
+        (C, 64, 1, [(11, 2), (1, 0)]),   # 13 [up2d(12) | 2]
+        (C, 64, 1, [(12, 0)]),           # 14
+    ]
+
+
 def fcn_macs_per_voxel(table=None) -> int:
     """Ternary MACs of one forward per input voxel (27 * cin * cout per output voxel,
     output voxels at 1/8^level of the input)."""
@@ -388,7 +413,7 @@ class TernaryFCN:
     skip layers, channel order [upsampled, skip]); lo/hi: int32 [cout]; pred_w
     float [nclass][16], pred_b float [nclass].  Tensors may be numpy or torch."""
 
-    def __init__(self, weights, lo, hi, pred_w, pred_b, t_lo, t_hi, table=None, device="cuda"):
+    def __init__(self, weights, lo, hi, pred_w, pred_b, t_lo, t_hi, table=None, device="cuda", c_in=1):
         self.table = table or fcn_table()
         dev = torch.device(device)
         as_t = lambda a, dt: torch.as_tensor(a).to(device=dev, dtype=dt).contiguous()
@@ -397,7 +422,7 @@ class TernaryFCN:
         couts = [row[1] for row in self.table]
         for i, (kind, co, s, segs) in enumerate(self.table):
             w = as_t(weights[i], torch.int8)
-            cins = [1] if segs[0][0] < 0 else [couts[sj] for sj, _ in segs]
+            cins = [c_in] if segs[0][0] < 0 else [couts[sj] for sj, _ in segs]
             assert w.shape == (co, sum(cins), 3, 3, 3), (i, tuple(w.shape), cins)
             L = layers[i]
             L.kind, L.c_out, L.stride, L.dil, L.nseg = kind, co, s, 1, len(segs)

@@ -232,10 +232,10 @@ tn_status build_conv(const tn_segment* segs, int nseg, int k, tn_geom g, const i
     for (int i = 0; i < nseg; ++i) {
         const tn_segment& s = segs[i];
         TN_TRY(check_dims(s.d, "segment dims"));
-        if (s.upsample != 0 && s.upsample != 1) return fail(TN_EINVAL, "upsample must be 0 or 1");
-        const int f = s.upsample ? 2 : 1;
-        if (i == 0) { Dci = s.d.d * f; Hci = s.d.h * f; Wci = s.d.w * f; N = s.d.n; }
-        if (s.d.d * f != Dci || s.d.h * f != Hci || s.d.w * f != Wci || s.d.n != N)
+        if (s.upsample < 0 || s.upsample > 2) return fail(TN_EINVAL, "upsample must be 0, 1 or 2");
+        const int f = s.upsample ? 2 : 1, fz = s.upsample == 1 ? 2 : 1;   // 2: in-plane only (2D)
+        if (i == 0) { Dci = s.d.d * fz; Hci = s.d.h * f; Wci = s.d.w * f; N = s.d.n; }
+        if (s.d.d * fz != Dci || s.d.h * f != Hci || s.d.w * f != Wci || s.d.n != N)
             return fail(TN_ESHAPE, "segment %d extents differ from segment 0 after upsampling", i);
         SegDesc& sd = cd.seg[i];
         sd.xp = s.xp; sd.wp = s.wp;
@@ -333,7 +333,7 @@ tn_status tn_conv3d_first(const float* x, tn_dims xd, float t_lo, float t_hi, co
 tn_status tn_predict(const uint32_t* tp, tn_dims td, const float* w, const float* b,
                      int32_t nclass, float* logits, tn_stream stream) {
     TN_TRY(check_dims(td, "td"));
-    if (td.c > 32) return fail(TN_EUNSUPPORTED, "tn_predict supports c <= 32 (got %d)", td.c);
+    if (td.c > 64) return fail(TN_EUNSUPPORTED, "tn_predict supports c <= 64 (got %d)", td.c);
     if (nclass < 1 || nclass > 8) return fail(TN_EUNSUPPORTED, "tn_predict supports 1..8 classes");
     if (w == nullptr || b == nullptr) return fail(TN_EINVAL, "w/b is NULL");
     if (empty(td)) return TN_OK;

@@ -72,7 +72,8 @@ __device__ void stage_brick(uint32_t* __restrict__ dst, const SegDesc& sg, const
         uint32_t* d = dst + static_cast<int64_t>(i) * 2 * CW;
         bool inb = zi >= 0 && zi < cd.Dci && yi >= 0 && yi < cd.Hci && xi >= 0 && xi < cd.Wci;
         int zs = zi, ys = yi, xs = xi;
-        if (sg.up) { zs >>= 1; ys >>= 1; xs >>= 1; }
+        if (sg.up == 1) zs >>= 1;              // up 2: nearest x2 in y and x only
+        if (sg.up) { ys >>= 1; xs >>= 1; }
         zs -= sg.zbeg;
         inb = inb && zs >= 0 && zs < sg.D && ys < sg.H && xs < sg.W;
         if (inb) {

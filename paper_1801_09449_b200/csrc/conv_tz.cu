@@ -440,7 +440,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                     for (int sg = 0; sg < NSEG; ++sg) {
                         const SegDesc& sd = cd.seg[sg];
-                        const int zs = (sd.up ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
+                        const int zs = (sd.up == 1 ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
                         const bool ok = zs >= 0 && zs < sd.D && nr[sg] > 0;
                         if (FIRST) {
                             bytes[sg] = ok ? static_cast<uint32_t>(nr[sg]) * sd.W * 4u : 0u;
@@ -514,7 +514,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 #pragma unroll
                 for (int sg = 0; sg < NSEG; ++sg) {
                     const SegDesc& sd = cd.seg[sg];
-                    const int zs = (sd.up ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
+                    const int zs = (sd.up == 1 ? (i >> 1) : cd.zres + i * zst) - sd.zbeg;
                     zok[sg] = zs >= 0 && zs < sd.D;
                     head[sg] = FIRST ? 0u : static_cast<uint32_t>(reinterpret_cast<uintptr_t>(
                         sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[sg]) * sd.W * 2 * sd.cw)) & 15u;
@@ -1146,7 +1146,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     if (pl.dil < 1 || (pl.dil > 1 && (pl.s != 1 || f4 || first || cd.nseg != 1))) return false;
     if (pl.s != 1 && !(pl.s == 2 && cd.nseg == 1 && cd.seg[0].up == 0)) return false;
     // the kernel fixes the segment pattern: one plain segment, or [nearest-x2 upsampled, plain]
-    if (cd.nseg == 1 ? cd.seg[0].up != 0 : (cd.seg[0].up != 1 || cd.seg[1].up != 0)) return false;
+    // (up 1 = nearest x2 in z, y, x; up 2 = in y and x only, the 2D decoders of Table 1)
+    if (cd.nseg == 1 ? cd.seg[0].up != 0 : (cd.seg[0].up == 0 || cd.seg[1].up != 0)) return false;
     // K padded to the next of 16 / 32 / 64 (zero filters, "always 0" thresholds for the pad)
     if (cd.K < 1 || cd.K > 64) return false;
     pl.kp = cd.K <= 16 ? 16 : (cd.K <= 32 ? 32 : 64);

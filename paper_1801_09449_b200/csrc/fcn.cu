@@ -43,10 +43,10 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
             d = h = w = -1;
             for (int sgi = 0; sgi < ly.nseg; ++sgi) {
                 const tn_dims& sd = P[ly.src[sgi]].out;
-                const int f = ly.upsample[sgi] ? 2 : 1;
-                if (sgi == 0) { d = sd.d * f; h = sd.h * f; w = sd.w * f; }
-                else if (sd.d * f != d || sd.h * f != h || sd.w * f != w) {
-                    set_error("layer %d: segment extents differ (%dx%dx%d vs %dx%dx%d)", i, sd.d * f,
+                const int f = ly.upsample[sgi] ? 2 : 1, fz = ly.upsample[sgi] == 1 ? 2 : 1;
+                if (sgi == 0) { d = sd.d * fz; h = sd.h * f; w = sd.w * f; }
+                else if (sd.d * fz != d || sd.h * f != h || sd.w * f != w) {
+                    set_error("layer %d: segment extents differ (%dx%dx%d vs %dx%dx%d)", i, sd.d * fz,
                               sd.h * f, sd.w * f, d, h, w);
                     return TN_ESHAPE;
                 }
@@ -64,7 +64,10 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
         P[i].bytes = tn_packed_bytes(o);
         off = align_up(off + P[i].bytes);
     }
+    // a multi-channel float input (e.g. Table 1's 15-slice stacks) is ternarised and packed
+    // into this buffer first; layer 0 is then a regular conv from it
     *scratch_off = off;
+    if (xd.c > 1) off = align_up(off + tn_packed_bytes(xd));
     *total = align_up(off);
     return TN_OK;
 }
@@ -101,7 +104,6 @@ tn_status tn_fcn_create(const tn_layer* layers, int32_t n_layers, float t_lo, fl
                 set_error("layer %d: the first layer must be entry 0 with one segment from input -1", i);
                 return bad(TN_EINVAL);
             }
-            if (ly.c_out > 32) { set_error("first layer supports c_out <= 32"); return bad(TN_EUNSUPPORTED); }
             if (ly.wp[0] == nullptr) { set_error("layer 0: wp NULL"); return bad(TN_EINVAL); }
             net->cin[0][0] = 1;
         } else if (ly.kind == TN_LAYER_CONV) {
@@ -112,7 +114,7 @@ tn_status tn_fcn_create(const tn_layer* layers, int32_t n_layers, float t_lo, fl
                     set_error("layer %d: src[%d] = %d must name an earlier layer", i, s, ly.src[s]);
                     return bad(TN_EINVAL);
                 }
-                if (ly.upsample[s] != 0 && ly.upsample[s] != 1) { set_error("layer %d: bad upsample", i); return bad(TN_EINVAL); }
+                if (ly.upsample[s] < 0 || ly.upsample[s] > 2) { set_error("layer %d: bad upsample", i); return bad(TN_EINVAL); }
                 if (ly.wp[s] == nullptr) { set_error("layer %d: wp[%d] NULL", i, s); return bad(TN_EINVAL); }
                 net->cin[s][i] = layers[ly.src[s]].c_out;
             }
@@ -125,7 +127,7 @@ tn_status tn_fcn_create(const tn_layer* layers, int32_t n_layers, float t_lo, fl
             return bad(TN_EINVAL);
         }
     }
-    if (layers[n_layers - 1].c_out > 32) { set_error("prediction needs c_out <= 32 on the last layer"); return bad(TN_EUNSUPPORTED); }
+    if (layers[n_layers - 1].c_out > 64) { set_error("prediction needs c_out <= 64 on the last layer"); return bad(TN_EUNSUPPORTED); }
     *out = net;
     return TN_OK;
 }
@@ -164,7 +166,7 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         set_error("layer range [%d, %d) outside [0, %d)", first, last, nl);
         return TN_EINVAL;
     }
-    if (xd.c != 1) { set_error("FCN input must have c == 1 (got %d)", xd.c); return TN_ESHAPE; }
+    if (xd.c < 1 || xd.c > 64) { set_error("FCN input needs 1 <= c <= 64 (got %d)", xd.c); return TN_ESHAPE; }
     if (xd.n < 1 || xd.d < 1 || xd.h < 1 || xd.w < 1) { set_error("FCN input must be non-empty"); return TN_ESHAPE; }
     std::vector<LayerPlan> P;
     size_t total = 0;
@@ -188,7 +190,8 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         const tn_layer& ly = net->layers[i];
         uint32_t* outp = reinterpret_cast<uint32_t*>(base + P[i].off);
         const tn_dims& o = P[i].out;
-        if (ly.kind == TN_LAYER_FIRST) {
+        if (ly.kind == TN_LAYER_FIRST && xd.c == 1) {
+            if (ly.c_out > 32) { set_error("a one-channel first layer supports c_out <= 32"); return TN_EUNSUPPORTED; }
             FirstDesc fd{};
             fd.x = x; fd.D = xd.d; fd.H = xd.h; fd.W = xd.w; fd.zbeg = 0; fd.Dg = xd.d;
             fd.t_lo = net->t_lo; fd.t_hi = net->t_hi; fd.wp = ly.wp[0];
@@ -205,7 +208,17 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         cd.nseg = ly.nseg;
         cd.N = xd.n;
         cd.K = ly.c_out;
-        for (int sgi = 0; sgi < ly.nseg; ++sgi) {
+        if (ly.kind == TN_LAYER_FIRST) {
+            // A7 on a multi-channel float input (PAPER.md:180, 15 neighbouring slices per stack):
+            // Eq. 6 + pack (tn_pack_f32's kernel, NaN -> d_bad), then layer 0 as a regular conv
+            uint32_t* xpk = reinterpret_cast<uint32_t*>(base + soff);
+            cudaError_t e = launch_pack_f32(x, xd, net->t_lo, net->t_hi, xpk, d_bad, s);
+            if (e != cudaSuccess) { set_error("input pack: %s", cudaGetErrorString(e)); return TN_ECUDA; }
+            SegDesc& sd = cd.seg[0];
+            sd.xp = xpk; sd.wp = ly.wp[0]; sd.c = xd.c; sd.cw = (xd.c + 31) / 32;
+            sd.D = xd.d; sd.H = xd.h; sd.W = xd.w; sd.zbeg = 0; sd.up = 0;
+        }
+        for (int sgi = 0; sgi < ly.nseg && ly.kind != TN_LAYER_FIRST; ++sgi) {
             const LayerPlan& sp = P[ly.src[sgi]];
             SegDesc& sd = cd.seg[sgi];
             sd.xp = reinterpret_cast<const uint32_t*>(base + sp.off);
@@ -216,8 +229,8 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
             sd.zbeg = 0;
             sd.up = ly.upsample[sgi];
         }
-        const int f = ly.upsample[0] ? 2 : 1;
-        cd.Dci = cd.seg[0].D * f; cd.Hci = cd.seg[0].H * f; cd.Wci = cd.seg[0].W * f;
+        const int f = ly.upsample[0] ? 2 : 1, fz = ly.upsample[0] == 1 ? 2 : 1;
+        cd.Dci = cd.seg[0].D * fz; cd.Hci = cd.seg[0].H * f; cd.Wci = cd.seg[0].W * f;
         for (int a = 0; a < 3; ++a) { cd.s[a] = ly.stride; cd.p[a] = ly.dil; cd.dl[a] = ly.dil; }
         cd.Do = o.d; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = 0;
         cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
@@ -231,7 +244,7 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         st = run_conv(cd, s, "tn_fcn_forward");
         if (st != TN_OK) return st;
     }
-    if (last == L && net->layers[L - 1].kind == TN_LAYER_FIRST) {
+    if (last == L && net->layers[L - 1].kind == TN_LAYER_FIRST && xd.c == 1) {
         const LayerPlan& last = P[L - 1];
         cudaError_t e = launch_predict(reinterpret_cast<const uint32_t*>(base + last.off), last.out,
                                        net->pred_w, net->pred_b, net->nclass, logits, s);

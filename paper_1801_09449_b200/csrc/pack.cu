@@ -452,14 +452,16 @@ __global__ void __launch_bounds__(kThreads)
 predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t total,
                const float* __restrict__ w, const float* __restrict__ b, int nclass,
                float* __restrict__ logits, int64_t cstride) {
-    __shared__ float sw[kMaxClass * 32];
+    __shared__ float sw[kMaxClass * 64];
     __shared__ float sb[kMaxClass];
     for (int i = threadIdx.x; i < nclass * C; i += kThreads) sw[i] = w[i];
     if (threadIdx.x < nclass) sb[threadIdx.x] = b[threadIdx.x];
     __syncthreads();
     const int64_t g = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     if (g >= total) return;
-    const uint2 sm = *reinterpret_cast<const uint2*>(tp + g * 2);
+    const int cw = (C + 31) / 32;                 // C <= 64: one or two words per plane
+    uint32_t ws[2] = {0u, 0u}, wm[2] = {0u, 0u};
+    for (int q = 0; q < cw; ++q) { ws[q] = tp[g * 2 * cw + q]; wm[q] = tp[g * 2 * cw + cw + q]; }
     const int64_t n = g / DHW;
     const int64_t v = g - n * DHW;
     for (int j = 0; j < nclass; ++j) {
@@ -470,8 +472,8 @@ predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t tota
             float part = 0.0f;
             for (int c = c0; c < c0 + 4 && c < C; ++c) {
                 const float wv = sw[j * C + c];
-                const bool nz = (sm.y >> c) & 1u;
-                const bool p = (sm.x >> c) & 1u;
+                const bool nz = (wm[c >> 5] >> (c & 31)) & 1u;
+                const bool p = (ws[c >> 5] >> (c & 31)) & 1u;
                 part += nz ? (p ? wv : -wv) : 0.0f;
             }
             acc += part;

@@ -63,8 +63,8 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
         if (ly.kind == TN_LAYER_FIRST) { d = g.d; h = g.h; w = g.w; }
         else {
             const tn_dims& s = out[ly.src[0]];
-            const int f = ly.upsample[0] ? 2 : 1;
-            d = s.d * f; h = s.h * f; w = s.w * f;
+            const int f = ly.upsample[0] ? 2 : 1, fz = ly.upsample[0] == 1 ? 2 : 1;
+            d = s.d * fz; h = s.h * f; w = s.w * f;
         }
         if (ly.dil != 1) { set_error("slab forward supports dilation 1"); return TN_EUNSUPPORTED; }
         out[i] = tn_dims{1, ly.c_out, out_extent(d, ly.stride, 1, 1), out_extent(h, ly.stride, 1, 1),
@@ -104,7 +104,7 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
     for (int j = 0; j < nl; ++j) {
         const tn_layer& ly = net->layers[j];
         for (int sgi = 0; sgi < ly.nseg; ++sgi) {
-            const int sides = (ly.stride == 1 || ly.upsample[sgi]) ? 3 : 1;
+            const int sides = (ly.stride == 1 || ly.upsample[sgi] == 1) ? 3 : 1;
             if (ly.kind == TN_LAYER_FIRST) sp.x_halo |= sides;
             else sp.L[ly.src[sgi]].halo |= sides;
         }
@@ -159,8 +159,8 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
                 sd.up = ly.upsample[sgi];
             }
             const tn_slab_layer& s0 = sp.L[ly.src[0]];
-            const int f = ly.upsample[0] ? 2 : 1;
-            cd.Dci = s0.gd * f; cd.Hci = s0.h * f; cd.Wci = s0.w * f;
+            const int f = ly.upsample[0] ? 2 : 1, fz = ly.upsample[0] == 1 ? 2 : 1;
+            cd.Dci = s0.gd * fz; cd.Hci = s0.h * f; cd.Wci = s0.w * f;
             for (int a = 0; a < 3; ++a) { cd.s[a] = ly.stride; cd.p[a] = 1; cd.dl[a] = 1; }
             cd.Do = zb - za; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = o.z0 + za;
             cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;

@@ -64,9 +64,9 @@ def jittered_thresholds(k: int, base: int, seed: int):
     return lo, hi
 
 
-def threshold_base(cin: int, p_a: float, p_w: float = 0.4) -> int:
-    """Quartile of an acc ~ N(0, 27*cin*p_a*p_w): about half the outputs become 0."""
-    return int(round(0.6745 * math.sqrt(27.0 * cin * p_a * p_w)))
+def threshold_base(cin: int, p_a: float, p_w: float = 0.4, taps: int = 27) -> int:
+    """Quartile of an acc ~ N(0, taps*cin*p_a*p_w): about half the outputs become 0."""
+    return int(round(0.6745 * math.sqrt(taps * cin * p_a * p_w)))
 
 
 def ct_volume(shape, seed: int) -> np.ndarray:
@@ -133,3 +133,54 @@ def fcn_params(seed: int = 21):
     pred_b = (0.1 * g.standard_normal(size=(2,))).astype(np.float32)
     return dict(weights=weights, lo=lo, hi=hi, pred_w=pred_w, pred_b=pred_b,
                 t_lo=CT_T_LO, t_hi=CT_T_HI)
+
+
+# NEXT-4: Table 1's 2.5D U-Net (reading R18).  (cin, cout, kernel) of its 14 ternary layers --
+# input recipe only; the topology is stated separately by the oracle and the binding.
+FCN25_WEIGHT_SHAPES = [(15, 32, 3), (32, 64, 3), (64, 64, 3), (64, 128, 3), (128, 128, 3), (128, 256, 3),
+                       (256, 256, 1), (256, 256, 1), (512, 256, 3), (256, 128, 3), (256, 128, 3), (128, 64, 3),
+                       (128, 64, 3), (64, 64, 3)]
+# stack geometry: 15 neighbouring slices of 240 x 176 voxels (Table 1's 236 x 172
+# input rounded up to a multiple of 8 for its three /2 levels); one volume = 138 stacks (the
+# 138-slice ROI of PAPER.md:180)
+STACK_SLICES, STACK_H, STACK_W, ROI_STACKS = 15, 240, 176, 138
+
+
+def fcn25_params(seed: int = 81):
+    """Weights of the 2D layers as [cout][cin][3][3][3] codes with P(0) = 0.6 on the active taps
+    (the middle plane dz = 1 for 3x3 layers, the centre tap for 1x1 layers) and 0 elsewhere
+    (those taps only ever meet the zero padding of one-plane inputs); thresholds from
+    threshold_base with taps = 9 or 1 (p_a = 0.38 for layer 1, else 0.5), jitter seed 100 + i;
+    prediction w ~ N(0, 0.25^2) [2][64], b ~ N(0, 0.1^2) (seed 61)."""
+    weights, lo, hi = [], [], []
+    for i, (cin, cout, k) in enumerate(FCN25_WEIGHT_SHAPES):
+        w = np.zeros((cout, cin, 3, 3, 3), np.int8)
+        act = ternary_codes((cout, cin, k, k), 0.6, seed + i)
+        if k == 3:
+            w[:, :, 1] = act
+        else:
+            w[:, :, 1, 1, 1] = act[:, :, 0, 0]
+        weights.append(w)
+        base = threshold_base(cin, 0.38 if i == 0 else 0.5, taps=k * k)
+        l, h = jittered_thresholds(cout, base, 100 + i)
+        lo.append(l)
+        hi.append(h)
+    g = rng(61)
+    pred_w = (0.25 * g.standard_normal(size=(2, 64))).astype(np.float32)
+    pred_b = (0.1 * g.standard_normal(size=(2,))).astype(np.float32)
+    return dict(weights=weights, lo=lo, hi=hi, pred_w=pred_w, pred_b=pred_b, t_lo=CT_T_LO, t_hi=CT_T_HI)
+
+
+def ct_stacks(n_stacks: int, h: int, w: int, seed: int) -> np.ndarray:
+    """float32 [n_stacks][15][1][h][w]: stack s holds slices s-7 .. s+7 of a CT-like volume of
+    n_stacks slices (ct_volume recipe), zero outside the volume ('a stack of several
+    neighbouring slices (15 in our experiments)' per central slice)."""
+    vol = ct_volume((1, 1, n_stacks, h, w), seed)[0, 0]
+    half = STACK_SLICES // 2
+    out = np.zeros((n_stacks, STACK_SLICES, 1, h, w), np.float32)
+    for s in range(n_stacks):
+        for j in range(STACK_SLICES):
+            z = s + j - half
+            if 0 <= z < n_stacks:
+                out[s, j, 0] = vol[z]
+    return out

@@ -64,7 +64,7 @@ def test_host_validation_before_any_launch(tn):
     assert tn.lib.tn_conv3d_first(ctypes.c_void_p(0x1000), tn.dims(1, 2, 4, 4, 4), 0.0, 1.0,
                                   ctypes.c_void_p(0x1000), 16, g, ctypes.c_void_p(0x1000),
                                   ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), None, None) == tn.TN_ESHAPE
-    assert tn.lib.tn_predict(ctypes.c_void_p(0x1000), tn.dims(1, 64, 4, 4, 4), ctypes.c_void_p(0x1000),
+    assert tn.lib.tn_predict(ctypes.c_void_p(0x1000), tn.dims(1, 65, 4, 4, 4), ctypes.c_void_p(0x1000),
                              ctypes.c_void_p(0x1000), 2, ctypes.c_void_p(0x1000), None) == tn.TN_EUNSUPPORTED
     # empty tensors are a successful no-op
     assert tn.lib.tn_pack_i8(None, tn.dims(1, 16, 0, 4, 4), None, None, None) == tn.TN_OK
@@ -194,3 +194,24 @@ def test_every_fcn_layer_runs_on_the_tensor_core_kernel(tn, vol):
         ups = [u for _, u in segs]
         assert tn.tn_conv_kernel_for(dims, co, tn.geom(s), ups) == tn.TN_KERNEL_TZ, (vol, i + 1)
         ext[i] = tuple((v - 1) // s + 1 for v in e)
+
+
+def test_fcn25_kernel_selection(tn):
+    """Table 1's 2.5D U-Net (reading R18) at 240 x 176: the layers up to 64 channels plan onto the
+    tensor-core kernel (TZ; 15 slice channels padded to 16), the 128 / 256-channel layers (whose
+    filter banks exceed the resident B image) onto popc."""
+    table = tn.fcn25_table()
+    couts = [row[1] for row in table]
+    ext, picks = {}, []
+    for i, (kind, co, s, segs) in enumerate(table):
+        if segs[0][0] < 0:
+            e, dims, ups = (1, 240, 176), [tn.dims(1, 15, 1, 240, 176)], [0]
+        else:
+            src, up = segs[0]
+            z, y, x = ext[src]
+            e = (z, y * 2, x * 2) if up else (z, y, x)
+            dims, ups = [tn.dims(1, couts[sj], *ext[sj]) for sj, _ in segs], [u for _, u in segs]
+        picks.append(tn.tn_conv_kernel_for(dims, co, tn.geom(s), ups))
+        ext[i] = (1,) + tuple((v - 1) // s + 1 for v in e[1:])
+    TZ, P = tn.TN_KERNEL_TZ, tn.TN_KERNEL_POPC
+    assert picks == [TZ, TZ, TZ, P, P, P, P, P, P, P, P, P, TZ, TZ]

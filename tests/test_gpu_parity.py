@@ -718,3 +718,35 @@ def test_fcn_from_float_model_prepared_on_host(tn):
     p = dict(base, weights=weights, lo=lo, hi=hi)
     x = synth.ct_volume((1, 1, 16, 24, 32), seed=78)
     _fcn_compare(tn, x, p)
+
+
+# --------------------------------------------------------------------------- NEXT-4: Table 1's 2.5D U-Net
+@pytest.mark.parametrize("n,h,w", [(3, 48, 64), (2, 240, 176)])
+def test_fcn25_table1_network_matches_oracle(tn, n, h, w):
+    """Table 1's ternary 2.5D U-Net (reading R18) on 15-slice stacks: the multi-channel input
+    ternarised and packed, 2D layers as one-plane 3x3x3 convs (TZ up to 64 channels, popc beyond),
+    stride-2 rows, 2D nearest upsampling (upsample 2) with skip concatenation, the 64-channel last
+    layer with the unfused prediction: every layer bit-exact and the logits within R13."""
+    p = synth.fcn25_params()
+    x = synth.ct_stacks(n + 2, h, w, seed=12)[1:n + 1]
+    net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"],
+                        table=tn.fcn25_table(), c_in=15)
+    ws = net.workspace(x.shape)
+    flag = tn.bad_flag()
+    logits = net(dev(x), ws=ws, d_bad=flag)
+    assert bad_value(flag) == tn.INT64_MAX
+    ref_logits, acts, bad = oracle.fcn25_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"],
+                                                 p["pred_w"], p["pred_b"], want_acts=True)
+    assert bad == -1
+    for i in range(14):
+        view, _ = net.layer_output(x.shape, ws, i)
+        ref, _ = oracle.pack(acts[i])
+        np.testing.assert_array_equal(u32(view), ref, err_msg=f"layer #{i + 1}")
+    got = logits.cpu().numpy()
+    tol = np.maximum(np.abs(ref_logits), _logit_tol(p["pred_w"], p["pred_b"]) / 1e-5) * 1e-5
+    assert np.all(np.abs(got - ref_logits) <= tol)
+    # a non-finite slice value is reported at its flat index through the multi-channel input pack
+    x[1, 4, 0, 3, 5] = np.nan
+    flag = tn.bad_flag()
+    net(dev(x), ws=ws, d_bad=flag)
+    assert bad_value(flag) == np.ravel_multi_index((1, 4, 0, 3, 5), x.shape)

@@ -454,3 +454,21 @@ def test_bench_golden_fcn_logits_are_the_oracles():
         for a, (lo_, hi_) in enumerate(region):
             assert np.all((at[:, 2 + a] >= lo_) & (at[:, 2 + a] < hi_)), (name, a)
         assert np.all(np.isfinite(ref)) and np.all(np.abs(ref) <= bound + 1e-6)
+
+
+
+def test_bench_golden_fcn25_logits_are_the_oracles():
+    """bench.py's Table-1 2.5D gate: the sampled logits of stack 0 recomputed with the oracle
+    (a stack depends only on its own slices); stacks 1-3 checked for range and magnitude."""
+    g = np.load(os.path.join(GOLDEN, "bench_samples.npz"))
+    at, ref = g["fcn25_at"], g["fcn25_ref"]
+    assert at.shape == (512, 5) and set(np.unique(at[:, 0])) <= {0, 1, 2, 3} and np.all(at[:, 2] == 0)
+    p = synth.fcn25_params()
+    x = synth.ct_stacks(synth.ROI_STACKS, synth.STACK_H, synth.STACK_W, seed=300)[:1]
+    lg, _, bad = oracle.fcn25_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"])
+    assert bad == -1
+    s0 = at[:, 0] == 0
+    assert s0.sum() > 50
+    np.testing.assert_array_equal(lg[tuple(at[s0].T)], ref[s0])
+    bound = float(np.abs(p["pred_b"]).max() + np.abs(p["pred_w"]).sum(1).max())
+    assert np.all(np.isfinite(ref)) and np.all(np.abs(ref) <= bound + 1e-6)

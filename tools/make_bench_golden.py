@@ -41,6 +41,30 @@ def fcn_logits(cfg_name, crop=None):
     return logits
 
 
+def fcn25_golden(out):
+    """NEXT-4 (Table 1's 2.5D U-Net, reading R18): sampled logits of the first 4 of the bench's
+    138 stacks (240 x 176); a stack depends only on its own 15 slices, so these need the oracle
+    on 4 stacks only."""
+    p = synth.fcn25_params()
+    x = synth.ct_stacks(synth.ROI_STACKS, synth.STACK_H, synth.STACK_W, seed=300)[:4]
+    lg, _, bad = oracle.fcn25_forward(x, p["t_lo"], p["t_hi"], p["weights"], p["lo"], p["hi"], p["pred_w"],
+                                      p["pred_b"])
+    assert bad == -1
+    g = synth.rng(904)
+    m = 512
+    at = np.stack([g.integers(0, 4, m), g.integers(0, 2, m), np.zeros(m, int), g.integers(0, synth.STACK_H, m),
+                   g.integers(0, synth.STACK_W, m)], 1).astype(np.int32)
+    out["fcn25_at"] = at
+    out["fcn25_ref"] = lg[tuple(at.T)]
+
+
+path = os.path.join(ROOT, "tests", "golden", "bench_samples.npz")
+if "--only-fcn25" in sys.argv:
+    out = dict(np.load(path))
+    fcn25_golden(out)
+    np.savez_compressed(path, **out)
+    print("updated", path)
+    sys.exit(0)
 out = {}
 x0, w0, _, _ = synth.conv_config("C0")
 out["c0_at"] = synth.sample_positions(x0.shape, 16, 512, seed=777)
@@ -72,6 +96,6 @@ for a in range(3):
     loc[:, 2 + a] -= crop[a][0]
 out["fcn_c4_at"] = at
 out["fcn_c4_ref"] = lg[tuple(loc.T)]
-path = os.path.join(ROOT, "tests", "golden", "bench_samples.npz")
+fcn25_golden(out)
 np.savez_compressed(path, **out)
 print("wrote", path)
