@@ -31,6 +31,7 @@ struct Tiling {
     int TX, TY, TZ;                 // output tile
     int BX, BY, BZ;                 // input brick (conv-input coordinates)
     int tiles_x, tiles_y, tiles_z;
+    int a0, a1;                     // kernel planes dz in [a0, a1] that can meet data (2D: only dz = 1)
 };
 
 template <int CW>
@@ -103,9 +104,9 @@ __global__ void __launch_bounds__(kThreads)
 conv_popc_kernel(const ConvDesc cd, const Tiling tl, int Kpad) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int brick_words = (tl.BX * tl.BY * tl.BZ * 2 * CW + 3) & ~3;   // 16-byte aligned
-    const int wt_words = Kpad * 27 * 2 * CW;
+    const int wt_words = kKC * 27 * 2 * CW;                     // one chunk of kKC output channels
     uint32_t* s_brick = smem;                                   // [nseg][brick]
-    uint32_t* s_w = s_brick + cd.nseg * brick_words;            // [nseg][Kpad][27][2CW]
+    uint32_t* s_w = s_brick + cd.nseg * brick_words;            // [nseg][kKC][27][2CW]
     const bool fused = cd.yp != nullptr;
     uint32_t* s_out = s_w + cd.nseg * wt_words;                 // [kTile][2][cwo] (fused only)
 
@@ -115,30 +116,34 @@ conv_popc_kernel(const ConvDesc cd, const Tiling tl, int Kpad) {
     const int tz = t % tl.tiles_z; t /= tl.tiles_z;
     const int n = t;
     const int zo0 = tz * tl.TZ, yo0 = ty * tl.TY, xo0 = tx * tl.TX;
-    const int zi0 = (cd.zo_beg + zo0) * cd.s[0] - cd.p[0];
+    // (2D tiles stage only the one input plane the middle kernel plane reads)
+    const int zi0 = (cd.zo_beg + zo0) * cd.s[0] - cd.p[0] + tl.a0 * cd.dl[0];
     const int yi0 = yo0 * cd.s[1] - cd.p[1];
     const int xi0 = xo0 * cd.s[2] - cd.p[2];
 
-    for (int sgi = 0; sgi < cd.nseg; ++sgi) {
+    for (int sgi = 0; sgi < cd.nseg; ++sgi)
         stage_brick<CW>(s_brick + sgi * brick_words, cd.seg[sgi], cd, n, zi0, yi0, xi0,
                         tl.BX, tl.BY, tl.BZ);
-        // weights: K real rows then zero rows up to Kpad
-        const int real_words = cd.K * 27 * 2 * CW;
-        uint32_t* wdst = s_w + sgi * wt_words;
-        if ((real_words & 3) == 0) {
-            const uint4* wsrc = reinterpret_cast<const uint4*>(cd.seg[sgi].wp);
-            for (int i = threadIdx.x; i < wt_words / 4; i += kThreads)
-                reinterpret_cast<uint4*>(wdst)[i] =
-                    4 * i < real_words ? __ldg(wsrc + i) : make_uint4(0u, 0u, 0u, 0u);
-        } else {
-            for (int i = threadIdx.x; i < wt_words; i += kThreads)
-                wdst[i] = i < real_words ? __ldg(cd.seg[sgi].wp + i) : 0u;
+    // filter banks chunk by chunk of kKC output channels (K real rows, zero rows up to Kpad),
+    // so wide banks (Table 1's 256 x 512 x 27) need only one chunk of shared memory
+    auto stage_weights = [&](int k0) {
+        for (int sgi = 0; sgi < cd.nseg; ++sgi) {
+            const int real_words = min(cd.K - k0, kKC) * 27 * 2 * CW;
+            const uint32_t* wsrc = cd.seg[sgi].wp + static_cast<int64_t>(k0) * 27 * 2 * CW;
+            uint32_t* wdst = s_w + sgi * wt_words;
+            if ((real_words & 3) == 0) {
+                for (int i = threadIdx.x; i < wt_words / 4; i += kThreads)
+                    reinterpret_cast<uint4*>(wdst)[i] = 4 * i < real_words
+                        ? __ldg(reinterpret_cast<const uint4*>(wsrc) + i) : make_uint4(0u, 0u, 0u, 0u);
+            } else {
+                for (int i = threadIdx.x; i < wt_words; i += kThreads) wdst[i] = i < real_words ? __ldg(wsrc + i) : 0u;
+            }
         }
-    }
+    };
+    (void)Kpad;
     if (fused) {
         for (int i = threadIdx.x; i < kTile * 2 * cd.cwo; i += kThreads) s_out[i] = 0u;
     }
-    __syncthreads();
 
     // this thread's voxels
     int boff[kVPT];
@@ -147,17 +152,21 @@ conv_popc_kernel(const ConvDesc cd, const Tiling tl, int Kpad) {
 #pragma unroll
     for (int i = 0; i < kVPT; ++i) {
         const int lin = threadIdx.x + kThreads * i;
+        const bool in_tile = lin < tl.TX * tl.TY * tl.TZ;        // 2D tiles can hold fewer than kTile voxels
         const int ox = lin % tl.TX;
         const int oy = (lin / tl.TX) % tl.TY;
-        const int oz = lin / (tl.TX * tl.TY);
-        boff[i] = ((oz * cd.s[0]) * tl.BY + oy * cd.s[1]) * tl.BX + ox * cd.s[2];
+        const int oz = in_tile ? lin / (tl.TX * tl.TY) : 0;
+        boff[i] = in_tile ? ((oz * cd.s[0]) * tl.BY + oy * cd.s[1]) * tl.BX + ox * cd.s[2] : 0;
         const int zo = zo0 + oz, yo = yo0 + oy, xo = xo0 + ox;
-        valid[i] = zo < cd.Do && yo < cd.Ho && xo < cd.Wo;
+        valid[i] = in_tile && zo < cd.Do && yo < cd.Ho && xo < cd.Wo;
         vox[i] = (((static_cast<int64_t>(n) * cd.Do + zo) * cd.Ho + yo) * cd.Wo + xo);
     }
     const int step_z = cd.dl[0] * tl.BY * tl.BX, step_y = cd.dl[1] * tl.BX, step_x = cd.dl[2];
 
     for (int k0 = 0; k0 < cd.K; k0 += kKC) {
+        if (k0 > 0) __syncthreads();          // everyone is done with the previous chunk
+        stage_weights(k0);
+        __syncthreads();
         int acc[kVPT][kKC];
 #pragma unroll
         for (int i = 0; i < kVPT; ++i)
@@ -166,11 +175,11 @@ conv_popc_kernel(const ConvDesc cd, const Tiling tl, int Kpad) {
 
         for (int sgi = 0; sgi < cd.nseg; ++sgi) {
             const uint32_t* bb = s_brick + sgi * brick_words;
-            const uint32_t* wb = s_w + sgi * wt_words + k0 * 27 * 2 * CW;
+            const uint32_t* wb = s_w + sgi * wt_words;
 #pragma unroll 1
-            for (int tap = 0; tap < 27; ++tap) {
+            for (int tap = 9 * tl.a0; tap < 9 * (tl.a1 + 1); ++tap) {
                 const int a = tap / 9, b = (tap / 3) % 3, e = tap % 3;
-                const int toff = a * step_z + b * step_y + e * step_x;
+                const int toff = (a - tl.a0) * step_z + b * step_y + e * step_x;
                 Words<CW> av[kVPT];
 #pragma unroll
                 for (int i = 0; i < kVPT; ++i) av[i] = lds_words<CW>(bb + (boff[i] + toff) * 2 * CW);
@@ -351,18 +360,23 @@ conv_first_kernel(const FirstDesc fd, const Tiling tl) {
     }
 }
 
-Tiling make_tiling(int Do, int Ho, int Wo, int N, const int* s, const int* dl, int tx_pref) {
+// two_d: one output plane whose only input plane is met by the middle kernel plane (one-plane
+// volumes with pad = dilation in z: Table 1's 2D layers) -> one-plane tiles, 9 taps.
+Tiling make_tiling(int Do, int Ho, int Wo, int N, const int* s, const int* dl, int tx_pref, bool two_d = false) {
     Tiling tl;
     tl.TX = tx_pref;
     while (tl.TX > 4 && tl.TX / 2 >= Wo) tl.TX /= 2;
     int rest = kTile / tl.TX;
-    tl.TY = 8;
+    tl.TY = two_d ? rest : 8;
     while (tl.TY > 1 && tl.TY / 2 >= Ho) tl.TY /= 2;
     if (tl.TY > rest) tl.TY = rest;
     tl.TZ = rest / tl.TY;
+    if (two_d) tl.TZ = 1;
+    tl.a0 = two_d ? 1 : 0;
+    tl.a1 = two_d ? 1 : 2;
     tl.BX = (tl.TX - 1) * s[2] + 2 * dl[2] + 1;
     tl.BY = (tl.TY - 1) * s[1] + 2 * dl[1] + 1;
-    tl.BZ = (tl.TZ - 1) * s[0] + 2 * dl[0] + 1;
+    tl.BZ = two_d ? 1 : (tl.TZ - 1) * s[0] + 2 * dl[0] + 1;
     tl.tiles_x = (Wo + tl.TX - 1) / tl.TX;
     tl.tiles_y = (Ho + tl.TY - 1) / tl.TY;
     tl.tiles_z = (Do + tl.TZ - 1) / tl.TZ;
@@ -372,10 +386,11 @@ Tiling make_tiling(int Do, int Ho, int Wo, int N, const int* s, const int* dl, i
 
 template <int CW>
 cudaError_t launch_popc_cw(const ConvDesc& cd, cudaStream_t st) {
-    const Tiling tl = make_tiling(cd.Do, cd.Ho, cd.Wo, cd.N, cd.s, cd.dl, 16);
+    const bool two_d = cd.Do == 1 && cd.Dci == 1 && cd.zo_beg == 0 && cd.p[0] == cd.dl[0];
+    const Tiling tl = make_tiling(cd.Do, cd.Ho, cd.Wo, cd.N, cd.s, cd.dl, 16, two_d);
     const int Kpad = (cd.K + kKC - 1) / kKC * kKC;
     const int brick_words = (tl.BX * tl.BY * tl.BZ * 2 * CW + 3) & ~3;
-    size_t smem = sizeof(uint32_t) * (static_cast<size_t>(cd.nseg) * (brick_words + Kpad * 27 * 2 * CW));
+    size_t smem = sizeof(uint32_t) * (static_cast<size_t>(cd.nseg) * (brick_words + kKC * 27 * 2 * CW));
     if (cd.yp) smem += sizeof(uint32_t) * kTile * 2 * cd.cwo;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(conv_popc_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -395,6 +410,7 @@ cudaError_t launch_conv_popc(const ConvDesc& cd, cudaStream_t st) {
         case 1: return launch_popc_cw<1>(cd, st);
         case 2: return launch_popc_cw<2>(cd, st);
         case 4: return launch_popc_cw<4>(cd, st);
+        case 8: return launch_popc_cw<8>(cd, st);     // up to 256 channels per segment (Table 1's widest)
         default: return cudaErrorNotSupported;
     }
 }
