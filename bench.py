@@ -277,6 +277,8 @@ def main():
     xd = tn.dims(*x.shape)
     g = tn.geom(1, 1, 1)
     wp = tn.tn_pack_weights(w_d)
+    # the filter bank's tensor-core operand image, built once with the weights (tn_conv_prepare)
+    prep = tn.tn_conv_prepare([(None, xd, 0, wp)], 64, g)
     xp = tn.packed_empty(*x.shape, device=dev)
     yp = tn.packed_empty(1, 64, 64, 128, 128, device=dev)
     yp_host = torch.empty(yp.shape, dtype=torch.int32).pin_memory()
@@ -284,7 +286,7 @@ def main():
 
     def step():
         tn.tn_pack_i8(x_d, xp)
-        tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+        tn.tn_conv3d_requant_prepared(prep, xp, xd, wp, 64, g, lo_d, hi_d, yp)
 
     # ---- parity gate (SPEC.md:485 pattern: no number without a passing check)
     step()
@@ -316,7 +318,7 @@ def main():
             a, c = ev[i]
             a.record(stream)
             tn.tn_pack_i8(x_d, xp)
-            tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+            tn.tn_conv3d_requant_prepared(prep, xp, xd, wp, 64, g, lo_d, hi_d, yp)
             c.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -334,7 +336,7 @@ def main():
         a.record(stream)
         tn.tn_pack_i8(x_d, xp)
         b.record(stream)
-        tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+        tn.tn_conv3d_requant_prepared(prep, xp, xd, wp, 64, g, lo_d, hi_d, yp)
         c.record(stream)
     torch.cuda.synchronize()
     conv_ms = [b.elapsed_time(c) for _, b, c in ev3]
@@ -368,7 +370,7 @@ def main():
         with torch.cuda.stream(streams[b]):
             x_b[b].copy_(x_host, non_blocking=True)
             tn.tn_pack_i8(x_b[b], xp_b[b])
-            tn.tn_conv3d_requant(xp_b[b], xd, wp, 64, g, lo_d, hi_d, yp_b[b])
+            tn.tn_conv3d_requant_prepared(prep, xp_b[b], xd, wp, 64, g, lo_d, hi_d, yp_b[b])
             yh_b[b].copy_(yp_b[b], non_blocking=True)
     tail = torch.cuda.Event()
     tail.record(streams[1])
@@ -398,7 +400,7 @@ def main():
         b = i & 1
         with torch.cuda.stream(streams[b]):
             xpk_b[b].copy_(xh_packed, non_blocking=True)
-            tn.tn_conv3d_requant(xpk_b[b], xd, wp, 64, g, lo_d, hi_d, yp_b[b])
+            tn.tn_conv3d_requant_prepared(prep, xpk_b[b], xd, wp, 64, g, lo_d, hi_d, yp_b[b])
             yh_b[b].copy_(yp_b[b], non_blocking=True)
     tail = torch.cuda.Event()
     tail.record(streams[1])
@@ -412,7 +414,7 @@ def main():
         e2p_ms = float(t.item())
     e2e_packed = {"value": world * e2e_steps * C1_MACS / (e2p_ms / 1e3) / 1e9, "unit": "GMAC/s", "steps": e2e_steps,
                   "h2d_bytes_per_step": int(xh_packed.numel() * 4), "d2h_bytes_per_step": int(yp.numel() * 4),
-                  "step": "H2D of the 2-bit packed input + tn_conv3d_requant + D2H of the packed output",
+                  "step": "H2D of the 2-bit packed input + tn_conv3d_requant_prepared + D2H of the packed output",
                   "pipeline": "double-buffered like e2e"}
 
     # ---- roofline of the dominant kernel (the conv)
@@ -508,7 +510,7 @@ def main():
             "ms_per_step_min": float(np.min(step_ms)), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": C1_WORKLOAD,
-                       "step": "tn_pack_i8 (A1) + tn_conv3d_requant (A2-A4)",
+                       "step": "tn_pack_i8 (A1) + tn_conv3d_requant_prepared (A2-A4; filter bank prepared once with the weights)",
                        "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
                        "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)",
                                        3: "tcgen05 kind::i8 implicit GEMM, taps as UMMA descriptor offsets, "
@@ -649,6 +651,7 @@ def bench_c2(args, tn, torch, dev, stream):
     p = synth.fcn_params(cfg["seed_params"])
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"], device=dev)
     x = torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][0])).to(dev)
+    net.prepare(shape)   # filter-bank operand images, built once (tn_fcn_prepare)
     ws = net.workspace(shape, dev)
     logits = torch.empty((1, 2) + shape[2:], dtype=torch.float32, device=dev)
     net(x, logits=logits, ws=ws)
@@ -687,6 +690,7 @@ def bench_fcn25(args, tn, torch, dist, world, rank, dev, stream):
     del x_all
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"],
                         table=tn.fcn25_table(), device=dev, c_in=15)
+    net.prepare(tuple(x.shape))
     ws = net.workspace(tuple(x.shape), dev)
     logits = torch.empty((x.shape[0], 2, 1, synth.STACK_H, synth.STACK_W), dtype=torch.float32, device=dev)
     net(x, logits=logits, ws=ws)
@@ -835,6 +839,7 @@ def bench_fcn(args, tn, torch, dist, world, rank, dev, stream):
     # single launch over all of them, so partition tails and kernel prologues are paid once
     xb = torch.cat([torch.from_numpy(synth.ct_volume(shape, seed=cfg["seeds"][i])) for i in mine], 0).to(dev)
     bshape = (len(mine),) + tuple(shape[1:])
+    net.prepare(bshape)
     ws = net.workspace(bshape, dev)
     logits = torch.empty((len(mine), 2) + shape[2:], dtype=torch.float32, device=dev)
     net(xb, logits=logits, ws=ws)
@@ -872,6 +877,7 @@ def bench_c4(args, tn, torch, dist, world, rank, dev, stream):
     D, H, W = shape[2:]
     p = synth.fcn_params(cfg["seed_params"])
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"], device=dev)
+    net.prepare(shape)
     z0, z1 = rank * D // world, (rank + 1) * D // world
     vol = synth.ct_volume(shape, seed=cfg["seeds"][0])
     x = torch.from_numpy(np.ascontiguousarray(vol[:, :, z0:z1])).to(dev)

@@ -132,6 +132,37 @@ tn_status tn_conv3d_seg(const tn_segment* segs /*host array*/, int32_t nseg, int
                         tn_geom g, const int32_t* lo, const int32_t* hi, int32_t* y,
                         uint32_t* yp, tn_stream stream);
 
+/* ---- Prepared filter banks (tensor-core kernel) --------------------------- */
+/* The tensor-core conv kernel expands the packed filter bank into its UMMA B
+ * operand image (Eq. 9's w as int8 or FP4 codes) in every
+ * CTA of every launch.  tn_conv_prepare builds that image once, in device
+ * memory, for a conv of these segments / k / g (requant != 0: the packed-output
+ * form; 0: int32 output); the *_prepared calls then copy it instead.
+ *   segs[i].xp may be NULL here (only d, upsample and wp are read); the spatial
+ *   extents only steer the plan, the image is the same for any extents.
+ *   The image is a COPY of the bank at prepare time and is tied to the wp
+ *   pointers: after changing a bank's contents in place, prepare again.  A
+ *   prepared call whose kernel plan differs from the prepared one (other wp
+ *   pointers, segment widths, k, stride, dilation, kernel selector) is still
+ *   correct: it stages the bank as the unprepared call does.
+ *   *out receives a handle (also when the shape has no tensor-core plan:
+ *   tn_conv_prep_bytes is then 0); the call synchronises `stream`.
+ *   Errors: TN_EINVAL (NULL out/segs, bad k/nseg), TN_ESHAPE, TN_ECUDA.     */
+typedef struct tn_conv_prep tn_conv_prep;
+tn_status tn_conv_prepare(const tn_segment* segs /*host array*/, int32_t nseg, int32_t k, tn_geom g,
+                          int32_t requant, tn_conv_prep** out, tn_stream stream);
+int64_t   tn_conv_prep_bytes(const tn_conv_prep* p);   /* device bytes held (0: no image) */
+void      tn_conv_prep_destroy(tn_conv_prep* p);        /* NULL is a no-op; not stream-ordered:
+                                                           no launch using p may be pending */
+/* Same arguments and results as tn_conv3d_requant / tn_conv3d_seg, plus p
+ * (NULL = the unprepared call).                                              */
+tn_status tn_conv3d_requant_prepared(const tn_conv_prep* p, const uint32_t* xp, tn_dims xd,
+                                     const uint32_t* wp, int32_t k, tn_geom g, const int32_t* lo,
+                                     const int32_t* hi, uint32_t* yp, tn_stream stream);
+tn_status tn_conv3d_seg_prepared(const tn_conv_prep* p, const tn_segment* segs, int32_t nseg,
+                                 int32_t k, tn_geom g, const int32_t* lo, const int32_t* hi,
+                                 int32_t* y, uint32_t* yp, tn_stream stream);
+
 /* ---- A7: first layer -- Eq. 6 on the float input fused with a conv from 1
  * channel and the requant epilogue (reading R7).
  * x float [n][1][d][h][w]; wp packed [k][27][2][1]; yp packed.  Domain: NaN/Inf. */
@@ -176,7 +207,17 @@ size_t    tn_fcn_workspace_bytes(const tn_fcn* net, tn_dims xd);
 /* x float [n][c][d][h][w] -> logits float [n][nclass][d][h][w]. */
 tn_status tn_fcn_forward(const tn_fcn* net, const float* x, tn_dims xd, float* logits, void* ws,
                          size_t ws_bytes, int64_t* d_bad, tn_stream stream);
-void      tn_fcn_destroy(tn_fcn* net);
+void      tn_fcn_destroy(tn_fcn* net);   /* also frees the images of tn_fcn_prepare */
+/* Optional: build every tensor-core layer's filter-bank image (tn_conv_prepare)
+ * for inputs of dims xd under the current kernel selector, replacing earlier
+ * ones; later forwards (tn_fcn_forward*, slab variants) copy them instead of
+ * expanding the banks in every CTA.  Forwards of other extents or selectors stay
+ * correct (a layer whose plan differs stages its bank).  Synchronises stream;
+ * not stream-ordered against pending forwards of net.  The images are copies of
+ * the banks at prepare time: prepare again after changing weights in place.
+ * Errors: TN_EINVAL (NULL net), TN_ESHAPE (xd), TN_ECUDA.                     */
+tn_status tn_fcn_prepare(tn_fcn* net, tn_dims xd, tn_stream stream);
+size_t    tn_fcn_prep_bytes(const tn_fcn* net);   /* device bytes the images hold */
 /* The layers [first, last) of tn_fcn_forward only (last = -1: to the end; the
  * prediction runs with the last layer), reading earlier layers' outputs from ws.
  * Calling it for consecutive ranges on one stream is tn_fcn_forward; used to time

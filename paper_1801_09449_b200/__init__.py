@@ -79,6 +79,12 @@ SIGNATURES = {
     "tn_conv3d": (ctypes.c_int, [_P, _D, _P, _I32, _G, _P, _P]),
     "tn_conv3d_requant": (ctypes.c_int, [_P, _D, _P, _I32, _G, _P, _P, _P, _P]),
     "tn_requant": (ctypes.c_int, [_P, _D, _P, _P, _P, _P]),
+    "tn_conv_prepare": (ctypes.c_int, [ctypes.POINTER(tn_segment), _I32, _I32, _G, _I32, ctypes.POINTER(_P), _P]),
+    "tn_conv_prep_bytes": (_I64, [_P]),
+    "tn_conv_prep_destroy": (None, [_P]),
+    "tn_conv3d_requant_prepared": (ctypes.c_int, [_P, _P, _D, _P, _I32, _G, _P, _P, _P, _P]),
+    "tn_conv3d_seg_prepared": (ctypes.c_int, [_P, ctypes.POINTER(tn_segment), _I32, _I32, _G, _P, _P, _P, _P,
+                                              _P]),
     "tn_conv3d_seg": (ctypes.c_int, [ctypes.POINTER(tn_segment), _I32, _I32, _G, _P, _P, _P, _P, _P]),
     "tn_conv3d_first": (ctypes.c_int, [_P, _D, _F, _F, _P, _I32, _G, _P, _P, _P, _P, _P]),
     "tn_predict": (ctypes.c_int, [_P, _D, _P, _P, _I32, _P, _P]),
@@ -87,6 +93,8 @@ SIGNATURES = {
     "tn_fcn_workspace_bytes": (_SZ, [_P, _D]),
     "tn_fcn_forward": (ctypes.c_int, [_P, _P, _D, _P, _P, _SZ, _P, _P]),
     "tn_fcn_destroy": (None, [_P]),
+    "tn_fcn_prepare": (ctypes.c_int, [_P, _D, _P]),
+    "tn_fcn_prep_bytes": (_SZ, [_P]),
     "tn_fcn_forward_range": (ctypes.c_int, [_P, _P, _D, _P, _P, _SZ, _P, _I32, _I32, _P]),
     "tn_fcn_layer_output": (_P, [_P, _D, _P, _I32, ctypes.POINTER(_D)]),
     "tn_set_conv_kernel": (ctypes.c_int, [_I32]),
@@ -248,14 +256,76 @@ def tn_requant(y, lo, hi, yp=None, stream=None):
     return yp
 
 
-def tn_conv3d_seg(segs, k, g: tn_geom, lo=None, hi=None, y=None, yp=None, requant=True, stream=None):
-    """segs: list of (xp, tn_dims, upsample, wp)."""
+class ConvPrep:
+    """A prepared filter bank (tn_conv_prepare): the tensor-core kernel's B image, built once."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    @property
+    def nbytes(self) -> int:
+        return int(lib.tn_conv_prep_bytes(self.handle)) if self.handle else 0
+
+    def close(self):
+        if self.handle and lib is not None:   # lib is None during interpreter shutdown
+            lib.tn_conv_prep_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
+def _seg_array(segs):
     arr = (tn_segment * len(segs))()
     for i, (xp, d, up, wp) in enumerate(segs):
-        arr[i] = tn_segment(xp.data_ptr(), d, int(up), wp.data_ptr())
+        arr[i] = tn_segment(xp.data_ptr() if xp is not None else None, d, int(up), wp.data_ptr())
+    return arr
+
+
+def tn_conv_prepare(segs, k, g: tn_geom, requant=True, stream=None) -> ConvPrep:
+    """segs: list of (xp or None, tn_dims, upsample, wp), as for tn_conv3d_seg."""
+    h = ctypes.c_void_p()
+    _check(lib.tn_conv_prepare(_seg_array(segs), len(segs), k, g, int(bool(requant)), ctypes.byref(h),
+                               _stream(stream)), "tn_conv_prepare")
+    return ConvPrep(h.value)
+
+
+def tn_conv3d_requant_prepared(prep, xp, xd: tn_dims, wp, k, g: tn_geom, lo, hi, yp=None, stream=None):
+    od = conv_out_dims(xd, k, g)
+    yp = packed_empty(od.n, k, od.d, od.h, od.w, xp.device) if yp is None else yp
+    _check(lib.tn_conv3d_requant_prepared(prep.handle if prep is not None else None, _ptr(xp), xd, _ptr(wp), k, g,
+                                          _ptr(lo), _ptr(hi), _ptr(yp), _stream(stream)),
+           "tn_conv3d_requant_prepared")
+    return yp
+
+
+def _seg_out(segs, k, g, y, yp, requant):
     d0, up0 = segs[0][1], segs[0][2]
-    f = 2 if up0 else 1
-    od = conv_out_dims(dims(d0.n, 1, d0.d * f, d0.h * f, d0.w * f), k, g)
+    f, fz = (2 if up0 else 1), (2 if up0 == 1 else 1)   # upsample 2: in-plane only
+    od = conv_out_dims(dims(d0.n, 1, d0.d * fz, d0.h * f, d0.w * f), k, g)
+    dev = segs[0][0].device
+    if requant and yp is None and y is None:
+        yp = packed_empty(od.n, k, od.d, od.h, od.w, dev)
+    elif not requant and y is None and yp is None:
+        y = torch.empty((od.n, od.d, od.h, od.w, k), dtype=torch.int32, device=dev)
+    return y, yp
+
+
+def tn_conv3d_seg_prepared(prep, segs, k, g: tn_geom, lo=None, hi=None, y=None, yp=None, requant=True,
+                           stream=None):
+    y, yp = _seg_out(segs, k, g, y, yp, requant)
+    _check(lib.tn_conv3d_seg_prepared(prep.handle if prep is not None else None, _seg_array(segs), len(segs), k,
+                                      g, _ptr(lo), _ptr(hi), _ptr(y), _ptr(yp), _stream(stream)),
+           "tn_conv3d_seg_prepared")
+    return yp if yp is not None else y
+
+
+def tn_conv3d_seg(segs, k, g: tn_geom, lo=None, hi=None, y=None, yp=None, requant=True, stream=None):
+    """segs: list of (xp, tn_dims, upsample, wp)."""
+    arr = _seg_array(segs)
+    d0, up0 = segs[0][1], segs[0][2]
+    f, fz = (2 if up0 else 1), (2 if up0 == 1 else 1)   # upsample 2: in-plane only
+    od = conv_out_dims(dims(d0.n, 1, d0.d * fz, d0.h * f, d0.w * f), k, g)
     dev = segs[0][0].device
     if requant and yp is None and y is None:
         yp = packed_empty(od.n, k, od.d, od.h, od.w, dev)
@@ -453,6 +523,12 @@ class TernaryFCN:
 
     def workspace_bytes(self, xd: tn_dims) -> int:
         return int(lib.tn_fcn_workspace_bytes(self.handle, xd))
+
+    def prepare(self, x_shape, stream=None) -> int:
+        """tn_fcn_prepare: prebuild every tensor-core layer's filter-bank image for inputs of x_shape;
+        returns the device bytes they hold."""
+        _check(lib.tn_fcn_prepare(self.handle, dims(*x_shape), _stream(stream)), "tn_fcn_prepare")
+        return int(lib.tn_fcn_prep_bytes(self.handle))
 
     def workspace(self, x_shape, device="cuda"):
         nb = self.workspace_bytes(dims(*x_shape))

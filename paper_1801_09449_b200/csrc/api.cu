@@ -301,6 +301,69 @@ tn_status tn_conv3d_seg(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom
     return run_conv(cd, cs(stream), "tn_conv3d_seg");
 }
 
+struct tn_conv_prep {
+    tn::TzPrep* tz;
+};
+
+tn_status tn_conv_prepare(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g, int32_t requant,
+                          tn_conv_prep** out, tn_stream stream) {
+    if (out == nullptr) return fail(TN_EINVAL, "tn_conv_prepare: out is NULL");
+    *out = nullptr;
+    if (segs == nullptr) return fail(TN_EINVAL, "tn_conv_prepare: segs is NULL");
+    if (nseg < 1 || nseg > kMaxSeg) return fail(TN_EINVAL, "nseg must be 1 or 2 (got %d)", nseg);
+    // the activations and outputs are not touched: stand-in pointers for build_conv's checks
+    alignas(16) static const uint32_t dummy[4] = {0u, 0u, 0u, 0u};
+    tn_segment sg[kMaxSeg];
+    for (int i = 0; i < nseg; ++i) {
+        sg[i] = segs[i];
+        if (sg[i].xp == nullptr) sg[i].xp = dummy;
+    }
+    const int32_t* t = reinterpret_cast<const int32_t*>(dummy);
+    int32_t* yo = reinterpret_cast<int32_t*>(const_cast<uint32_t*>(dummy));
+    ConvDesc cd;
+    TN_TRY(build_conv(sg, nseg, k, g, requant ? t : nullptr, requant ? t : nullptr, requant ? nullptr : yo,
+                      requant ? const_cast<uint32_t*>(dummy) : nullptr, &cd, nullptr));
+    tn_conv_prep* p = new tn_conv_prep{nullptr};
+    if (cd.N > 0 && cd.Do > 0 && cd.Ho > 0 && cd.Wo > 0 && pick_kernel(cd, g_conv_kernel) == TN_KERNEL_TZ) {
+        const tn_status st = cuda_status(tz_prepare(cd, g_conv_kernel != TN_KERNEL_TZ8, &p->tz, cs(stream)),
+                                         "tn_conv_prepare");
+        if (st != TN_OK) { delete p; return st; }
+    }
+    *out = p;
+    return TN_OK;
+}
+
+int64_t tn_conv_prep_bytes(const tn_conv_prep* p) {
+    return p ? static_cast<int64_t>(tz_prep_bytes(p->tz)) : 0;
+}
+
+void tn_conv_prep_destroy(tn_conv_prep* p) {
+    if (p == nullptr) return;
+    tz_prep_free(p->tz);
+    delete p;
+}
+
+tn_status tn_conv3d_requant_prepared(const tn_conv_prep* p, const uint32_t* xp, tn_dims xd,
+                                     const uint32_t* wp, int32_t k, tn_geom g, const int32_t* lo,
+                                     const int32_t* hi, uint32_t* yp, tn_stream stream) {
+    TN_TRY(check_dims(xd, "xd"));
+    tn_segment seg{xp, xd, 0, wp};
+    ConvDesc cd;
+    TN_TRY(build_conv(&seg, 1, k, g, lo, hi, nullptr, yp, &cd, nullptr));
+    cd.prep = p ? p->tz : nullptr;
+    return run_conv(cd, cs(stream), "tn_conv3d_requant_prepared");
+}
+
+tn_status tn_conv3d_seg_prepared(const tn_conv_prep* p, const tn_segment* segs, int32_t nseg,
+                                 int32_t k, tn_geom g, const int32_t* lo, const int32_t* hi,
+                                 int32_t* y, uint32_t* yp, tn_stream stream) {
+    if (segs == nullptr) return fail(TN_EINVAL, "segs is NULL");
+    ConvDesc cd;
+    TN_TRY(build_conv(segs, nseg, k, g, lo, hi, y, yp, &cd, nullptr));
+    cd.prep = p ? p->tz : nullptr;
+    return run_conv(cd, cs(stream), "tn_conv3d_seg_prepared");
+}
+
 tn_status tn_conv3d_first(const float* x, tn_dims xd, float t_lo, float t_hi, const uint32_t* wp,
                           int32_t k, tn_geom g, const int32_t* lo, const int32_t* hi,
                           uint32_t* yp, int64_t* d_bad, tn_stream stream) {

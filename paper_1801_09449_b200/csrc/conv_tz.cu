@@ -51,6 +51,7 @@
 #include "tc_ptx.cuh"
 
 #include <algorithm>
+#include <cstring>
 #include <climits>
 #include <vector>
 
@@ -202,6 +203,77 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
     nrows = max(yhi - ylo + 1, 0);
 }
 
+// B image entry u of a plan (the filter bank as the UMMA B operand): MMA m, half h = K-slice
+// j = 2m + h, block b (dz of the block sequence), row k: 16 channels of W[k][chunk][dz][dy][dx]
+// as int8, or 32 FP4 nibbles.  wsrc[sg]: segment sg's packed filter bank [K][27][2][cw] (staged
+// in shared memory by the conv, read from global memory by the prepare kernel).
+template <int K, int NSEG, int STR, bool FIRST, bool F4, int NB>
+__device__ __forceinline__ uint4 bimage_entry(const ConvDesc& cd, const TzPlan& pl, const uint32_t* const* wsrc,
+                                              int u) {
+    constexpr int rows = NB * K;
+    const int row = u % rows;
+    const int j = u / rows;                    // slice index (2m + h)
+    const int b = row / K, k = row - b * K;
+    const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    const int tap = k < cd.K ? pl.sl_tap[j] : -1;    // padded output channels: zero filters
+    if (FIRST) {
+        if (j == 0) {   // byte (dy*3 + dx) = w[k][0][dz][dy][dx]
+            uint32_t wv[4] = {0u, 0u, 0u, 0u};
+            for (int t9 = 0; t9 < 9; ++t9) {
+                const uint32_t* src = wsrc[0] + (k * 27 + dz * 9 + t9) * 2;
+                const uint32_t sb = src[0] & 1u, mb = src[1] & 1u;
+                const uint32_t byte = mb ? (sb ? 0x01u : 0xFFu) : 0u;
+                wv[t9 >> 2] |= byte << (8 * (t9 & 3));
+            }
+            v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+    } else if (F4) {
+        if (tap >= 0) {
+            const int sg = pl.sl_seg[j];
+            const int cw = cd.seg[sg].cw;
+            const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
+            if (cd.seg[sg].c <= 16) {       // [tap a ch 0-15 | tap b ch 0-15]
+                const uint2 a2 = expand16_f4(src[0], src[cw], 0);
+                uint2 b2 = make_uint2(0u, 0u);
+                const int tb = pl.sl_tapb[j];
+                if (tb >= 0) {
+                    const uint32_t* s2 = wsrc[sg] + (k * 27 + dz * 9 + tb) * 2 * cw;
+                    b2 = expand16_f4(s2[0], s2[cw], 0);
+                }
+                v = make_uint4(a2.x, a2.y, b2.x, b2.y);
+            } else {                        // 32 channels 32c .. 32c+31
+                const int c = pl.sl_chunk[j];
+                const uint2 a2 = expand16_f4(src[c], src[cw + c], 0);
+                const uint2 b2 = expand16_f4(src[c], src[cw + c], 16);
+                v = make_uint4(a2.x, a2.y, b2.x, b2.y);
+            }
+        }
+    } else if (tap >= 0) {
+        int c = pl.sl_chunk[j];
+        const int sg = (NSEG > 1 && c >= pl.cch[0]) ? 1 : 0;
+        if (sg) c -= pl.cch[0];
+        const int cw = cd.seg[sg].cw;
+        const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
+        const int word = c >> 1, sh = 16 * (c & 1);
+        v = expand16(src[word], src[cw + word], sh);
+    }
+    return v;
+}
+template <int K, int STR>
+__host__ __device__ constexpr int tz_nb() { return STR == 1 ? (K == 64 ? 3 : 5) : 4; }
+
+// Prepared filter bank (tn_weights_prepare / the FCN at create): the B image built once in global
+// memory, same layout as in shared memory ([j][NB*K][16 B]); the conv then copies it instead of
+// staging and expanding the packed bank in every CTA.
+template <int K, int NSEG, int STR, bool FIRST, bool F4>
+__global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* out) {
+    const uint32_t* wsrc[kMaxSeg] = {cd.seg[0].wp, cd.seg[kMaxSeg - 1].wp};
+    const int total = pl.nmma * 2 * tz_nb<K, STR>() * K;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x)
+        out[u] = bimage_entry<K, NSEG, STR, FIRST, F4, tz_nb<K, STR>()>(cd, pl, wsrc, u);
+}
+
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
 __global__ void __launch_bounds__(tz_threads(K, PRED, CT), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
@@ -267,8 +339,14 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         const uint32_t* wsrc[kMaxSeg];
         uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_a);
         int ofs = 0;
+        const bool prepared = cd.bimg != nullptr;   // (the host matched its plan to this launch's)
+        if (prepared) {
+            for (int i = threadIdx.x; i < pl.b_bytes / 16; i += kZThreads)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_b + 16 * i)), "l"(cd.bimg + i)
+                             : "memory");
+        }
 #pragma unroll
-        for (int sg = 0; sg < NSEG; ++sg) {
+        for (int sg = 0; sg < NSEG && !prepared; ++sg) {
             const int nw = cd.K * 27 * 2 * (FIRST ? 1 : cd.seg[sg].cw);   // words (odd K: not a multiple of 4)
             const int n4 = nw / 4;
             const uint4* g = reinterpret_cast<const uint4*>(cd.seg[sg].wp);
@@ -306,59 +384,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
-        // B image: MMA m, half h = K-slice j = 2m + h, block b (dz of the block
-        // sequence), row k: 16 channels of W[k][chunk][dz][dy][dx] as int8.
-        const int rows = NB * K;
-        const int total = pl.nmma * 2 * rows;
-        for (int u = threadIdx.x; u < total; u += kZThreads) {
-            const int row = u % rows;
-            const int j = u / rows;                    // slice index (2m + h)
-            const int b = row / K, k = row - b * K;
-            const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            const int tap = k < cd.K ? pl.sl_tap[j] : -1;    // padded output channels: zero filters
-            if (FIRST) {
-                if (j == 0) {   // byte (dy*3 + dx) = w[k][0][dz][dy][dx]
-                    uint32_t wv[4] = {0u, 0u, 0u, 0u};
-                    for (int t9 = 0; t9 < 9; ++t9) {
-                        const uint32_t* src = wsrc[0] + (k * 27 + dz * 9 + t9) * 2;
-                        const uint32_t sb = src[0] & 1u, mb = src[1] & 1u;
-                        const uint32_t byte = mb ? (sb ? 0x01u : 0xFFu) : 0u;
-                        wv[t9 >> 2] |= byte << (8 * (t9 & 3));
-                    }
-                    v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                }
-            } else if (F4) {
-                if (tap >= 0) {
-                    const int sg = pl.sl_seg[j];
-                    const int cw = cd.seg[sg].cw;
-                    const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
-                    if (cd.seg[sg].c <= 16) {       // [tap a ch 0-15 | tap b ch 0-15]
-                        const uint2 a2 = expand16_f4(src[0], src[cw], 0);
-                        uint2 b2 = make_uint2(0u, 0u);
-                        const int tb = pl.sl_tapb[j];
-                        if (tb >= 0) {
-                            const uint32_t* s2 = wsrc[sg] + (k * 27 + dz * 9 + tb) * 2 * cw;
-                            b2 = expand16_f4(s2[0], s2[cw], 0);
-                        }
-                        v = make_uint4(a2.x, a2.y, b2.x, b2.y);
-                    } else {                        // 32 channels 32c .. 32c+31
-                        const int c = pl.sl_chunk[j];
-                        const uint2 a2 = expand16_f4(src[c], src[cw + c], 0);
-                        const uint2 b2 = expand16_f4(src[c], src[cw + c], 16);
-                        v = make_uint4(a2.x, a2.y, b2.x, b2.y);
-                    }
-                }
-            } else if (tap >= 0) {
-                int c = pl.sl_chunk[j];
-                const int sg = (NSEG > 1 && c >= pl.cch[0]) ? 1 : 0;
-                if (sg) c -= pl.cch[0];
-                const int cw = cd.seg[sg].cw;
-                const uint32_t* src = wsrc[sg] + (k * 27 + dz * 9 + tap) * 2 * cw;
-                const int word = c >> 1, sh = 16 * (c & 1);
-                v = expand16(src[word], src[cw + word], sh);
-            }
-            *reinterpret_cast<uint4*>(s_b + static_cast<size_t>(j) * rows * 16 + row * 16) = v;
+        // B image (unless a prepared one was copied)
+        if (!prepared) {
+            const int total = pl.nmma * 2 * NB * K;
+            for (int u = threadIdx.x; u < total; u += kZThreads)
+                *reinterpret_cast<uint4*>(s_b + static_cast<size_t>(u) * 16) =
+                    bimage_entry<K, NSEG, STR, FIRST, F4, NB>(cd, pl, wsrc, u);
         }
         if (PRED) {
             for (int i = threadIdx.x; i < cd.nclass; i += kZThreads) s_pred[i] = __ldg(cd.pb + i);
@@ -1366,18 +1397,25 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     return pl.units > 0;
 }
 
+// build_out != nullptr: launch the B-image builder of this plan into build_out instead of the conv
 template <int K>
-static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int grid, size_t smem, cudaStream_t st) {
+static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int grid, size_t smem, cudaStream_t st,
+                               uint4* build_out = nullptr) {
     void (*kern)(ConvDesc, TzPlan) = nullptr;
+    void (*bkern)(ConvDesc, TzPlan, uint4*) = nullptr;
     const bool pred = cd.logits != nullptr;
 #define TZ_PICK(CT_, NSEG_, STR_)                                                                     \
-    if (!pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                      \
+    if (!pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_) {                                    \
         kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, false>                     \
-                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, false>;
+                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, false>;                        \
+        bkern = bimage_build_kernel<K, NSEG_, STR_, false, false>;                                     \
+    }
 #define TZ_PICK4(CT_, NSEG_, STR_)                                                                    \
-    if (pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_)                                       \
+    if (pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_) {                                     \
         kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, true>                      \
-                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, true>;
+                    : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, true>;                         \
+        bkern = bimage_build_kernel<K, NSEG_, STR_, false, true>;                                      \
+    }
     TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(3, 1, 1) TZ_PICK(4, 1, 1)
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
     TZ_PICK(1, 1, 2) TZ_PICK(2, 1, 2) TZ_PICK(3, 1, 2) TZ_PICK(4, 1, 2)
@@ -1387,6 +1425,11 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
 #undef TZ_PICK
 #undef TZ_PICK4
     if (kern == nullptr) return cudaErrorNotSupported;
+    if (build_out != nullptr) {
+        const int total = pl.nmma * 2 * pl.NB * K;
+        bkern<<<(total + 255) / 256, 256, 0, st>>>(cd, pl, build_out);
+        return cudaGetLastError();
+    }
     static void* configured[128] = {nullptr};
     bool done = false;
     for (void* f : configured) done = done || f == reinterpret_cast<void*>(kern);
@@ -1539,9 +1582,86 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
     return cudaSuccess;
 }
 
-static cudaError_t launch_conv_tz_one(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
+// The prepared image: the plan fields and filter-bank identity the B image depends on.
+struct TzPrep {
+    uint4* img;
+    int bytes;
+    int kp, K, f4, s, nseg, NB, nmma;
+    int cch[kMaxSeg], c[kMaxSeg], cw[kMaxSeg];
+    const uint32_t* wp[kMaxSeg];
+    int8_t sl_tap[2 * kZMaxMma], sl_chunk[2 * kZMaxMma], sl_tapb[2 * kZMaxMma], sl_seg[2 * kZMaxMma];
+};
+
+static void prep_key(const ConvDesc& cd, const TzPlan& pl, TzPrep& k) {
+    k.bytes = pl.b_bytes;
+    k.kp = pl.kp; k.K = cd.K; k.f4 = pl.f4; k.s = pl.s; k.nseg = cd.nseg; k.NB = pl.NB; k.nmma = pl.nmma;
+    for (int i = 0; i < kMaxSeg; ++i) {
+        const bool on = i < cd.nseg;
+        k.cch[i] = on ? pl.cch[i] : 0;
+        k.c[i] = on ? cd.seg[i].c : 0;
+        k.cw[i] = on ? cd.seg[i].cw : 0;
+        k.wp[i] = on ? cd.seg[i].wp : nullptr;
+    }
+    for (int j = 0; j < 2 * kZMaxMma; ++j) {
+        const bool on = j < 2 * pl.nmma;
+        k.sl_tap[j] = on ? pl.sl_tap[j] : 0;
+        k.sl_chunk[j] = on ? pl.sl_chunk[j] : 0;
+        k.sl_tapb[j] = on ? pl.sl_tapb[j] : 0;
+        k.sl_seg[j] = on ? pl.sl_seg[j] : 0;
+    }
+}
+
+static bool prep_matches(const TzPrep& p, const ConvDesc& cd, const TzPlan& pl) {
+    TzPrep k{};
+    prep_key(cd, pl, k);
+    if (k.bytes != p.bytes || k.kp != p.kp || k.K != p.K || k.f4 != p.f4 || k.s != p.s || k.nseg != p.nseg ||
+        k.NB != p.NB || k.nmma != p.nmma)
+        return false;
+    for (int i = 0; i < kMaxSeg; ++i)
+        if (k.cch[i] != p.cch[i] || k.c[i] != p.c[i] || k.cw[i] != p.cw[i] || k.wp[i] != p.wp[i]) return false;
+    return std::memcmp(k.sl_tap, p.sl_tap, sizeof k.sl_tap) == 0 &&
+           std::memcmp(k.sl_chunk, p.sl_chunk, sizeof k.sl_chunk) == 0 &&
+           std::memcmp(k.sl_tapb, p.sl_tapb, sizeof k.sl_tapb) == 0 &&
+           std::memcmp(k.sl_seg, p.sl_seg, sizeof k.sl_seg) == 0;
+}
+
+cudaError_t tz_prepare(const ConvDesc& cd0, bool allow_f4, TzPrep** out, cudaStream_t st) {
+    *out = nullptr;
+    if (!dil_ok(cd0)) return cudaSuccess;
+    const ConvDesc cd = dil_class(cd0, 0);
     TzPlan pl{};
-    if (!plan_any(cd, pl, allow_f4)) return cudaErrorNotSupported;
+    if (!plan_any(cd, pl, allow_f4)) return cudaSuccess;
+    int ct = 0;
+    for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
+    TzPrep* p = new TzPrep{};
+    prep_key(cd, pl, *p);
+    cudaError_t e = cudaMalloc(&p->img, pl.b_bytes);
+    if (e != cudaSuccess) { delete p; return e; }
+    switch (pl.kp) {
+        case 16: e = launch_tz_k<16>(cd, pl, ct, 0, 0, st, p->img); break;
+        case 32: e = launch_tz_k<32>(cd, pl, ct, 0, 0, st, p->img); break;
+        case 64: e = launch_tz_k<64>(cd, pl, ct, 0, 0, st, p->img); break;
+        default: e = cudaErrorNotSupported;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // the image is complete before any conv reads it
+    if (e != cudaSuccess) { cudaFree(p->img); delete p; return e; }
+    *out = p;
+    return cudaSuccess;
+}
+
+void tz_prep_free(TzPrep* p) {
+    if (p == nullptr) return;
+    cudaFree(p->img);
+    delete p;
+}
+
+size_t tz_prep_bytes(const TzPrep* p) { return p ? static_cast<size_t>(p->bytes) : 0; }
+
+static cudaError_t launch_conv_tz_one(const ConvDesc& cd0, cudaStream_t st, bool allow_f4) {
+    TzPlan pl{};
+    if (!plan_any(cd0, pl, allow_f4)) return cudaErrorNotSupported;
+    ConvDesc cd = cd0;
+    cd.bimg = (cd.prep != nullptr && prep_matches(*cd.prep, cd, pl)) ? cd.prep->img : nullptr;
     const size_t smem = tz_smem(pl, pl.kp);
     if (g_num_sms_z == 0) {
         int dev = 0;

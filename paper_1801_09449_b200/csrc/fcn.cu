@@ -72,6 +72,50 @@ tn_status plan(const tn_fcn* net, tn_dims xd, std::vector<LayerPlan>& P, size_t*
     return TN_OK;
 }
 
+// The conv descriptor of layer i (anything but a one-channel TN_LAYER_FIRST) over workspace base.
+ConvDesc layer_desc(const tn_fcn* net, const std::vector<LayerPlan>& P, int i, char* base, size_t soff, tn_dims xd,
+                    float* logits) {
+    const tn_layer& ly = net->layers[i];
+    const int L = static_cast<int>(net->layers.size());
+    const tn_dims& o = P[i].out;
+    uint32_t* outp = reinterpret_cast<uint32_t*>(base + P[i].off);
+    ConvDesc cd{};
+    cd.nseg = ly.nseg;
+    cd.N = xd.n;
+    cd.K = ly.c_out;
+    if (ly.kind == TN_LAYER_FIRST) {   // multi-channel input, packed into the workspace at soff
+        SegDesc& sd = cd.seg[0];
+        sd.xp = reinterpret_cast<const uint32_t*>(base + soff); sd.wp = ly.wp[0]; sd.c = xd.c;
+        sd.cw = (xd.c + 31) / 32;
+        sd.D = xd.d; sd.H = xd.h; sd.W = xd.w; sd.zbeg = 0; sd.up = 0;
+    }
+    for (int sgi = 0; sgi < ly.nseg && ly.kind != TN_LAYER_FIRST; ++sgi) {
+        const LayerPlan& sp = P[ly.src[sgi]];
+        SegDesc& sd = cd.seg[sgi];
+        sd.xp = reinterpret_cast<const uint32_t*>(base + sp.off);
+        sd.wp = ly.wp[sgi];
+        sd.c = sp.out.c;
+        sd.cw = (sp.out.c + 31) / 32;
+        sd.D = sp.out.d; sd.H = sp.out.h; sd.W = sp.out.w;
+        sd.zbeg = 0;
+        sd.up = ly.upsample[sgi];
+    }
+    const int f = ly.upsample[0] ? 2 : 1, fz = ly.upsample[0] == 1 ? 2 : 1;
+    cd.Dci = cd.seg[0].D * fz; cd.Hci = cd.seg[0].H * f; cd.Wci = cd.seg[0].W * f;
+    for (int a = 0; a < 3; ++a) { cd.s[a] = ly.stride; cd.p[a] = ly.dil; cd.dl[a] = ly.dil; }
+    cd.Do = o.d; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = 0;
+    cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
+    cd.cwo = (ly.c_out + 31) / 32;
+    if (i == L - 1) {   // A8 fused into the last block's epilogue
+        cd.logits = logits;
+        cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
+        cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
+        cd.no_yp = 1;   // fused prediction: the last layer's packed codes are not stored
+    }
+    cd.prep = i < static_cast<int>(net->prep.size()) ? net->prep[i] : nullptr;
+    return cd;
+}
+
 }  // namespace
 
 extern "C" {
@@ -204,43 +248,14 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
             if (e != cudaSuccess) { set_error("layer %d: %s", i, cudaGetErrorString(e)); return TN_ECUDA; }
             continue;
         }
-        ConvDesc cd{};
-        cd.nseg = ly.nseg;
-        cd.N = xd.n;
-        cd.K = ly.c_out;
         if (ly.kind == TN_LAYER_FIRST) {
             // A7 on a multi-channel float input (PAPER.md:180, 15 neighbouring slices per stack):
             // Eq. 6 + pack (tn_pack_f32's kernel, NaN -> d_bad), then layer 0 as a regular conv
-            uint32_t* xpk = reinterpret_cast<uint32_t*>(base + soff);
-            cudaError_t e = launch_pack_f32(x, xd, net->t_lo, net->t_hi, xpk, d_bad, s);
+            cudaError_t e = launch_pack_f32(x, xd, net->t_lo, net->t_hi, reinterpret_cast<uint32_t*>(base + soff),
+                                            d_bad, s);
             if (e != cudaSuccess) { set_error("input pack: %s", cudaGetErrorString(e)); return TN_ECUDA; }
-            SegDesc& sd = cd.seg[0];
-            sd.xp = xpk; sd.wp = ly.wp[0]; sd.c = xd.c; sd.cw = (xd.c + 31) / 32;
-            sd.D = xd.d; sd.H = xd.h; sd.W = xd.w; sd.zbeg = 0; sd.up = 0;
         }
-        for (int sgi = 0; sgi < ly.nseg && ly.kind != TN_LAYER_FIRST; ++sgi) {
-            const LayerPlan& sp = P[ly.src[sgi]];
-            SegDesc& sd = cd.seg[sgi];
-            sd.xp = reinterpret_cast<const uint32_t*>(base + sp.off);
-            sd.wp = ly.wp[sgi];
-            sd.c = sp.out.c;
-            sd.cw = (sp.out.c + 31) / 32;
-            sd.D = sp.out.d; sd.H = sp.out.h; sd.W = sp.out.w;
-            sd.zbeg = 0;
-            sd.up = ly.upsample[sgi];
-        }
-        const int f = ly.upsample[0] ? 2 : 1, fz = ly.upsample[0] == 1 ? 2 : 1;
-        cd.Dci = cd.seg[0].D * fz; cd.Hci = cd.seg[0].H * f; cd.Wci = cd.seg[0].W * f;
-        for (int a = 0; a < 3; ++a) { cd.s[a] = ly.stride; cd.p[a] = ly.dil; cd.dl[a] = ly.dil; }
-        cd.Do = o.d; cd.Ho = o.h; cd.Wo = o.w; cd.zo_beg = 0;
-        cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
-        cd.cwo = (ly.c_out + 31) / 32;
-        if (i == L - 1) {   // A8 fused into the last block's epilogue
-            cd.logits = logits;
-            cd.lstride = static_cast<int64_t>(o.d) * o.h * o.w;
-            cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;
-            cd.no_yp = 1;   // fused prediction: the last layer's packed codes are not stored
-        }
+        ConvDesc cd = layer_desc(net, P, i, base, soff, xd, logits);
         st = run_conv(cd, s, "tn_fcn_forward");
         if (st != TN_OK) return st;
     }
@@ -251,6 +266,43 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
         if (e != cudaSuccess) { set_error("prediction: %s", cudaGetErrorString(e)); return TN_ECUDA; }
     }
     return TN_OK;
+}
+
+tn_status tn_fcn_prepare(tn_fcn* net, tn_dims xd, tn_stream stream) {
+    if (net == nullptr) { set_error("net is NULL"); return TN_EINVAL; }
+    if (xd.c < 1 || xd.c > 64) { set_error("FCN input needs 1 <= c <= 64 (got %d)", xd.c); return TN_ESHAPE; }
+    if (xd.n < 1 || xd.d < 1 || xd.h < 1 || xd.w < 1) { set_error("FCN input must be non-empty"); return TN_ESHAPE; }
+    std::vector<LayerPlan> P;
+    size_t total = 0, soff = 0;
+    tn_status st = plan(net, xd, P, &total, &soff);
+    if (st != TN_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const bool allow_f4 = tn_get_conv_kernel() != TN_KERNEL_TZ8;
+    const int L = static_cast<int>(net->layers.size());
+    std::vector<TzPrep*> prep(L, nullptr);
+    // an image depends on the channel widths, banks and geometry only: the descriptors' buffer
+    // pointers are never read (stand-in base); the logits pointer only selects the epilogue form
+    alignas(16) static float dummy_logits[4];
+    for (int i = 0; i < L; ++i) {
+        if (net->layers[i].kind == TN_LAYER_FIRST && xd.c == 1) continue;   // dedicated first-layer kernel
+        const ConvDesc cd = layer_desc(net, P, i, reinterpret_cast<char*>(256), soff, xd, dummy_logits);
+        cudaError_t e = tz_prepare(cd, allow_f4, &prep[i], s);
+        if (e != cudaSuccess) {
+            for (TzPrep* q : prep) tz_prep_free(q);
+            set_error("tn_fcn_prepare: layer %d: %s", i, cudaGetErrorString(e));
+            return TN_ECUDA;
+        }
+    }
+    for (TzPrep* q : net->prep) tz_prep_free(q);
+    net->prep.swap(prep);
+    return TN_OK;
+}
+
+size_t tn_fcn_prep_bytes(const tn_fcn* net) {
+    size_t b = 0;
+    if (net != nullptr)
+        for (const TzPrep* q : net->prep) b += tz_prep_bytes(q);
+    return b;
 }
 
 void tn_fcn_destroy(tn_fcn* net) { delete net; }

@@ -166,6 +166,7 @@ tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i,
             cd.yp = outp; cd.y = nullptr; cd.lo = ly.lo; cd.hi = ly.hi;
             cd.cwo = (ly.c_out + 31) / 32;
             cd.halo_lo = halo_lo; cd.halo_hi = halo_hi;
+            cd.prep = i < static_cast<int>(net->prep.size()) ? net->prep[i] : nullptr;
             if (i + 1 == static_cast<int>(net->layers.size())) {
                 cd.logits = logits; cd.lstride = lstride;
                 cd.pw = net->pred_w; cd.pb = net->pred_b; cd.nclass = net->nclass;

@@ -29,6 +29,8 @@ struct SegDesc {
 // planes [zo_beg, zo_beg + Do).  Conv-input ("ci") coordinates are at the
 // resolution after upsampling; the global ci extents Dci/Hci/Wci define the
 // zero padding.
+struct TzPrep;   // conv_tz.cu: a prepared B image
+
 struct ConvDesc {
     SegDesc seg[kMaxSeg];
     int nseg;
@@ -68,6 +70,11 @@ struct ConvDesc {
     // of planes z = zres + j * zstep; Do / Dci / zo_beg then count class planes and Dbuf is the
     // output buffer's depth.  zstep == 0 means 1 (no classes), Dbuf == 0 means Do.
     int zstep, zres, Dbuf;
+    // Prepared filter bank (tensor-core kernel): the B image built once by tz_prepare; used by a
+    // launch whose plan matches the one it was built for (else the bank is staged as usual).
+    // bimg is set by the launcher from prep, never by callers.
+    const TzPrep* prep;
+    const uint4* bimg;
 };
 
 struct FirstDesc {
@@ -131,6 +138,13 @@ int         persistent_grid_cap();
 // The first layer may use the TZ kernel under the current selector (AUTO or TZ).
 bool        first_kernel_tz_allowed();
 cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s, bool allow_f4 = true);
+// Build the B image of cd's filter bank for the plan a launch of cd would use (one small kernel on
+// s, then a synchronize of s).  *out = nullptr (and cudaSuccess) when cd is not a tensor-core
+// shape.  The image is a copy: it belongs to the bank's contents at prepare time.
+cudaError_t tz_prepare(const ConvDesc& cd, bool allow_f4, TzPrep** out, cudaStream_t s);
+void        tz_prep_free(TzPrep* p);
+// bytes of device memory the image holds (0 for nullptr)
+size_t      tz_prep_bytes(const TzPrep* p);
 
 }  // namespace tn
 
@@ -143,6 +157,10 @@ struct tn_fcn {
     const float* pred_w;
     const float* pred_b;
     int nclass;
+    std::vector<tn::TzPrep*> prep;   // tn_fcn_prepare: per-layer B images (nullptr: none)
+    ~tn_fcn() {
+        for (tn::TzPrep* p : prep) tn::tz_prep_free(p);
+    }
 };
 
 namespace tn {

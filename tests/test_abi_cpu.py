@@ -72,6 +72,24 @@ def test_host_validation_before_any_launch(tn):
     assert tn.lib.tn_set_conv_kernel(tn.TN_KERNEL_AUTO) == tn.TN_OK
 
 
+def test_conv_prepare_host_logic(tn):
+    """tn_conv_prepare validation, and a shape only the popc kernel covers: a handle holding no image,
+    made without touching the device (no GPU here)."""
+    g = tn.geom()
+    h = ctypes.c_void_p()
+    seg = (tn.tn_segment * 1)(tn.tn_segment(None, tn.dims(1, 128, 4, 5, 6), 0, 0x1000))
+    assert tn.lib.tn_conv_prepare(seg, 1, 16, g, 1, None, None) == tn.TN_EINVAL
+    assert tn.lib.tn_conv_prepare(None, 1, 16, g, 1, ctypes.byref(h), None) == tn.TN_EINVAL
+    assert tn.lib.tn_conv_prepare(seg, 3, 16, g, 1, ctypes.byref(h), None) == tn.TN_EINVAL
+    assert tn.lib.tn_conv_prepare(seg, 1, 0, g, 1, ctypes.byref(h), None) == tn.TN_EINVAL
+    assert h.value is None
+    assert tn.lib.tn_conv_prepare(seg, 1, 16, g, 1, ctypes.byref(h), None) == tn.TN_OK   # C = 128: popc
+    assert h.value is not None and tn.lib.tn_conv_prep_bytes(h) == 0
+    tn.lib.tn_conv_prep_destroy(h)
+    tn.lib.tn_conv_prep_destroy(None)
+    assert tn.lib.tn_conv_prep_bytes(None) == 0
+
+
 def test_fcn_create_validation_and_workspace(tn):
     P = ctypes.c_void_p(0x1000)
     table = tn.fcn_table()

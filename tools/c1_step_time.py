@@ -14,8 +14,15 @@ fw = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 fr = torch.zeros(32 << 20, dtype=torch.int64, device="cuda")
 def flush():
     fw.zero_(); fr.sum()
+prep = tn.tn_conv_prepare([(None, xd, 0, wp)], 64, g)
 def sep():
     tn.tn_pack_i8(xd_, xp); tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+def sep_prep():
+    tn.tn_pack_i8(xd_, xp); tn.tn_conv3d_requant_prepared(prep, xp, xd, wp, 64, g, lo_d, hi_d, yp)
+def conv():
+    tn.tn_conv3d_requant(xp, xd, wp, 64, g, lo_d, hi_d, yp)
+def conv_prep():
+    tn.tn_conv3d_requant_prepared(prep, xp, xd, wp, 64, g, lo_d, hi_d, yp)
 import threading, time
 stop = threading.Event()
 period = float(sys.argv[1]) / 1e3 if len(sys.argv) > 1 else 0.0
@@ -29,7 +36,8 @@ if period > 0:
             pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
             time.sleep(period)
     threading.Thread(target=poll, daemon=True).start()
-for name, fn in (("step", sep), ("step", sep)):
+for name, fn in (("step", sep), ("step_prep", sep_prep), ("conv", conv), ("conv_prep", conv_prep),
+                 ("step", sep), ("step_prep", sep_prep)):
     for _ in range(3): fn()
     ts = []
     for _ in range(20):

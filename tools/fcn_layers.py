@@ -1,5 +1,5 @@
 """Per-layer and whole-forward device times of one FCN config (BASELINE configs[2..4]).
-usage: python tools/fcn_layers.py {C2|C3|C4} [reps]
+usage: python tools/fcn_layers.py {C2|C3|C4} [reps] [prep]   (prep: tn_fcn_prepare first)
 Whole forward: eager stream launches (tn_fcn_forward) and one CUDA graph of `reps` forwards.
 Per layer: a CUDA graph of `reps` back-to-back tn_fcn_forward_range(i, i+1) launches, timed
 with events around one replay (no host launch gaps in the number)."""
@@ -15,6 +15,8 @@ cfg = synth.CONFIGS[name]
 p = synth.fcn_params(cfg["seed_params"])
 net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
 x = torch.cat([torch.from_numpy(synth.ct_volume(cfg["vol_shape"], seed=s)) for s in cfg["seeds"]], 0).cuda()
+if len(sys.argv) > 3 and sys.argv[3] == "prep":
+    print("prepared images:", net.prepare(tuple(x.shape)), "bytes")
 ws = net.workspace(tuple(x.shape))
 logits = torch.empty((x.shape[0], 2) + tuple(x.shape[2:]), dtype=torch.float32, device="cuda")
 net(x, logits=logits, ws=ws)
