@@ -199,6 +199,7 @@ static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st
 }
 
 tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where) {
+    NvtxRange nv(where);
     if (cd.N == 0 || cd.Do == 0 || cd.Ho == 0 || cd.Wo == 0) return TN_OK;
     const int mode = g_conv_kernel;
     if (cd.logits != nullptr) {

@@ -231,6 +231,7 @@ tn_status tn_fcn_forward_range(const tn_fcn* net, const float* x, tn_dims xd, fl
     char* base = static_cast<char*>(ws);
     const int L = static_cast<int>(net->layers.size());
     for (int i = first; i < last; ++i) {
+        NvtxRange nv("fcn layer", i + 1);   // Table 1 numbering (#1 .. #L)
         const tn_layer& ly = net->layers[i];
         uint32_t* outp = reinterpret_cast<uint32_t*>(base + P[i].off);
         const tn_dims& o = P[i].out;

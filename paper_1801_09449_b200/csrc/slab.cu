@@ -120,6 +120,7 @@ tn_status make_slab_plan(const tn_fcn* net, tn_dims g, int z0, int z1, SlabPlan&
 tn_status run_slab_layer(const tn_fcn* net, const SlabPlan& sp, char* ws, int i, int64_t* d_bad, cudaStream_t s,
                          float* logits, int64_t lstride, uint32_t* halo_lo = nullptr, uint32_t* halo_hi = nullptr,
                          int za = 0, int zb = -1) {
+    NvtxRange nv("slab layer", i + 1);
     {
         const tn_layer& ly = net->layers[i];
         const tn_slab_layer& o = sp.L[i];
@@ -191,6 +192,7 @@ tn_status nccl_status(ncclResult_t r, const char* where) {
 // receives my first plane as its upper halo only if it reads that side: both ranks derive the
 // same plan, so a send is posted exactly when the peer posts the matching receive).
 tn_status exchange_halo(tn_comm* c, char* buf, int64_t plane_bytes, int planes, int sides, cudaStream_t s) {
+    NvtxRange nv("halo exchange");
     const size_t pb = static_cast<size_t>(plane_bytes);
     ncclResult_t r = ncclGroupStart();
     if (r != ncclSuccess) return nccl_status(r, "ncclGroupStart");

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cstddef>
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/tn.h"
 
@@ -170,6 +172,20 @@ tn_status run_conv(ConvDesc& cd, cudaStream_t st, const char* where);
 
 // Host-side error text.
 void set_error(const char* fmt, ...);
+
+// NVTX range over a host scope (SURVEY.md §5 tracing): "tn <what>" or "tn <what> <i>" for
+// per-layer ranges; visible to nsys / ncu --nvtx, a no-op without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* what, int i = -1) {
+        char b[96];
+        if (i >= 0) std::snprintf(b, sizeof b, "tn %s %d", what, i);
+        else std::snprintf(b, sizeof b, "tn %s", what);
+        nvtxRangePushA(b);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 inline int out_extent(int len, int s, int p, int dl) {
     int span = len + 2 * p - 2 * dl - 1;

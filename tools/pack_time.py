@@ -1,31 +1,25 @@
-"""Time tn_pack_i8 on C1 codes (1x64x64x128x128): CUDA graph of 10 x (L2 flush + pack) minus
-10 x flush, so host launch latency is not in the number."""
+"""C1's A1 pack (tn_pack_i8, 1x64x64x128x128 int8 -> 2-bit planes) timed alone with a cold L2:
+device time per launch (events), and the HBM rate on its algorithmic bytes (64 MiB + 16 MiB)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
 import paper_1801_09449_b200 as tn
-x, w, lo, hi = synth.conv_config("C1")
-if len(sys.argv) > 1:   # optional shape override: N C D H W
-    x = synth.ternary_codes(tuple(map(int, sys.argv[1:6])), 0.5, seed=10)
-xd = torch.from_numpy(x).cuda()
-xp = tn.tn_pack_i8(xd)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-st = torch.cuda.Stream()
-def graph(with_pack):
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=st):
-        for _ in range(10):
-            flush.zero_()
-            if with_pack:
-                tn.lib.tn_pack_i8(tn._ptr(xd), tn.dims(*x.shape), tn._ptr(xp), None, tn._stream(None))
-    return g
-def run(g):
-    g.replay(); torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) * 1e3 / 10
-ga, gb = graph(True), graph(False)
-us = run(ga) - run(gb)
-nb = x.size + x.size // x.shape[1] * 8 * ((x.shape[1] + 31) // 32)
-print(f"pack {x.shape}: {us:.1f} us  {nb / us / 1e3:.0f} GB/s (flush-subtracted)")
+x, _, _, _ = synth.conv_config("C1")
+xd_ = torch.from_numpy(x).cuda()
+xp = tn.packed_empty(*x.shape)
+fw = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+fr = torch.zeros(32 << 20, dtype=torch.int64, device="cuda")
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+for _ in range(3):
+    tn.tn_pack_i8(xd_, xp)
+ts = []
+for _ in range(reps):
+    fw.zero_(); fr.sum()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); tn.tn_pack_i8(xd_, xp); b.record()
+    torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b))
+nb = x.size + xp.numel() * 4
+print(f"pack median {np.median(ts) * 1e3:.2f} us  min {np.min(ts) * 1e3:.2f} us  "
+      f"{nb / (np.median(ts) * 1e-3) / 1e9:.0f} GB/s", flush=True)
