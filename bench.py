@@ -420,16 +420,22 @@ def main():
     # ---- roofline of the dominant kernel (the conv)
     conv_avg_s = float(np.mean(conv_ms)) / 1e3
     kernel = tn.tn_conv_kernel_for([xd], 64, g)
+    operands = tn.tn_conv_operands_for([xd], 64, g)      # 4 = FP4 E2M1 (kind::mxf4), 8 = int8
     uses_tc = kernel == tn.TN_KERNEL_TZ
     clocks = clk.summary()
     if uses_tc:
         bf16 = peaks.get("bf16_tflops", 1590.0)
-        peak = 2.0 * bf16          # int8 dense = 2 x bf16 dense (nominal 4.5 vs 2.25 PFLOP/s)
+        # dense peaks as multiples of the measured bf16 one (the guide's nominal ratios):
+        # int8 = 2x (4.5 vs 2.25 PFLOP/s), fp4 = 4x (9 vs 2.25)
+        ratio = FP4_PER_BF16 if operands == 4 else 2.0
+        peak = ratio * bf16
         achieved = 2.0 * C1_MACS / conv_avg_s / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TOPS (fp4 e2m1)" if operands == 4 else "TOPS (int8)",
                 "frac": achieved / peak,
-                "traffic": tn_peaks.get("c1_tz_conv_dram_bytes" if kernel == tn.TN_KERNEL_TZ else "c1_tc_conv_dram_bytes"),
-                "peak_source": "2 x MEASURED_PEAKS.bf16_tflops (int8/bf16 nominal ratio)"}
+                "traffic": tn_peaks.get("c1_tz_conv_dram_bytes"),
+                "peak_source": f"{ratio:g} x MEASURED_PEAKS.bf16_tflops ("
+                               + ("fp4" if operands == 4 else "int8") + "/bf16 nominal ratio)"}
     else:
         popc_per_clk = tn_peaks.get("popc_per_clk_per_sm", 16.0)
         mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -508,12 +514,18 @@ def main():
             "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps, "ms_per_step_median": float(np.median(step_ms)),
             "ms_per_step_min": float(np.min(step_ms)), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "vs_baseline": None,
+            "dtype": "fp4-e2m1 products, f32 accumulation (integer-exact)" if operands == 4 else "int8 -> int32",
+            "data": "synthetic",
             "config": {"workload": C1_WORKLOAD,
                        "step": "tn_pack_i8 (A1) + tn_conv3d_requant_prepared (A2-A4; filter bank prepared once with the weights)",
-                       "operands": "2-bit ternary sign/mask bitplanes, int32 accumulation",
+                       "operands": "2-bit ternary sign/mask bitplanes in HBM, expanded on chip to "
+                                   + ("FP4 E2M1 (f32 accumulation, exact below 2^24)" if operands == 4 else
+                                      "int8 (int32 accumulation)"),
                        "conv_kernel": {1: "popc (CUDA cores, Eq. 9 XOR/AND/POPC)",
-                                       3: "tcgen05 kind::i8 implicit GEMM, taps as UMMA descriptor offsets, "
+                                       3: "tcgen05 " + ("kind::mxf4 (ternary codes as exact FP4 E2M1, unit "
+                                                        "scales)" if operands == 4 else "kind::i8")
+                                          + " implicit GEMM, taps as UMMA descriptor offsets, "
                                           "kernel planes merged along N (conv_tz)"}.get(kernel, "?"),
                        "l2": "between timed steps, outside the events: a 256 MiB buffer is zeroed and another "
                              "256 MiB buffer read, so L2 (126 MB) is cold and holds no dirty lines when a step "

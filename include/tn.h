@@ -360,6 +360,9 @@ tn_status tn_set_grid_cap(int32_t max_ctas);
  * arguments would run under the current selection; -1 if the call is invalid
  * (or a forced tensor-core kernel does not cover the shape).  Host only.      */
 int32_t   tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);
+/* Operand format of that call on the tensor-core kernel: 8 = int8 (kind::i8),
+ * 4 = FP4 E2M1 (kind::mxf4, NEXT-2); 0 if it would not run on TN_KERNEL_TZ.     */
+int32_t   tn_conv_operands_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,7 @@ SIGNATURES = {
     "tn_ternarize_weights": (ctypes.c_int, [_P, _I32, _I32, ctypes.c_float, _P, _P, _P]),
     "tn_fold_thresholds": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.c_float, _I32, _I32, _P, _P, _P]),
     "tn_conv_kernel_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
+    "tn_conv_operands_for": (_I32, [ctypes.POINTER(tn_segment), _I32, _I32, _G]),
     "tn_comm_unique_id": (ctypes.c_int, [_P]),
     "tn_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_P)]),
     "tn_comm_destroy": (None, [_P]),
@@ -403,6 +404,15 @@ def tn_conv_kernel_for(seg_dims, k, g: tn_geom, upsample=None) -> int:
     for i, (d, up) in enumerate(zip(seg_dims, upsample)):
         arr[i] = tn_segment(None, d, int(up), None)
     return int(lib.tn_conv_kernel_for(arr, len(seg_dims), int(k), g))
+
+
+def tn_conv_operands_for(seg_dims, k, g: tn_geom, upsample=None) -> int:
+    """Tensor-core operand format (8 = int8, 4 = FP4; 0 = not on the tensor-core kernel)."""
+    upsample = upsample or [0] * len(seg_dims)
+    arr = (tn_segment * len(seg_dims))()
+    for i, (d, up) in enumerate(zip(seg_dims, upsample)):
+        arr[i] = tn_segment(None, d, int(up), None)
+    return int(lib.tn_conv_operands_for(arr, len(seg_dims), int(k), g))
 
 
 # ----------------------------------------------------------------------------- the FCN

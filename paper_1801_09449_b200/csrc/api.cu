@@ -421,6 +421,21 @@ tn_status tn_set_grid_cap(int32_t max_ctas) {
     return TN_OK;
 }
 
+int32_t tn_conv_operands_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g) {
+    if (tn_conv_kernel_for(segs, nseg, k, g) != TN_KERNEL_TZ) return 0;
+    ConvDesc cd;
+    uint32_t* dummy = reinterpret_cast<uint32_t*>(static_cast<uintptr_t>(256));
+    static const int32_t zero = 0;
+    tn_segment tmp[kMaxSeg];
+    for (int i = 0; i < nseg && i < kMaxSeg; ++i) {
+        tmp[i] = segs[i];
+        if (tmp[i].xp == nullptr) tmp[i].xp = dummy;
+        if (tmp[i].wp == nullptr) tmp[i].wp = dummy;
+    }
+    if (build_conv(tmp, nseg, k, g, &zero, &zero, nullptr, dummy, &cd, nullptr) != TN_OK) return 0;
+    return conv_tz_uses_f4(cd, g_conv_kernel != TN_KERNEL_TZ8) ? 4 : 8;
+}
+
 int32_t tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g) {
     if (segs == nullptr) return -1;
     // a dummy output pointer: only the shape logic of build_conv is used here

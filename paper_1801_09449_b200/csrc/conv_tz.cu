@@ -107,7 +107,7 @@ constexpr int kZMmaWarps = 2;
 // register budget allows (the fused-prediction variants need more registers).
 // Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
 // strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
-__host__ __device__ constexpr int tz_exp_warps(int, bool pred, int ct) { return (pred || ct == 2) ? 8 : 12; }
+__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct) { return (pred || ct == 2) ? 8 : (k == 64 ? 9 : 12); }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
 // (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
 __host__ __device__ constexpr int tz_epi_groups(int, bool, int) { return 2; }
@@ -260,18 +260,25 @@ __device__ __forceinline__ uint4 bimage_entry(const ConvDesc& cd, const TzPlan& 
     }
     return v;
 }
-template <int K, int STR>
-__host__ __device__ constexpr int tz_nb() { return STR == 1 ? (K == 64 ? 3 : 5) : 4; }
+// K = 64 at stride 1 splits wrapping MMAs over four TMEM blocks (the five-block rotated B image
+// would not fit shared memory next to the int8 operands), except with FP4 operands of one
+// C <= 64 segment, whose rotated image (92 KB) fits: three blocks, no split, two tiles per strip.
+__host__ __device__ constexpr bool tz_split(int K, int STR, bool F4, int CT) {
+    return STR == 1 && K == 64 && !(F4 && CT <= 4);
+}
+template <int K, int STR, bool F4, int CT>
+__host__ __device__ constexpr int tz_nb() { return STR == 1 ? (tz_split(K, STR, F4, CT) ? 3 : 5) : 4; }
 
 // Prepared filter bank (tn_weights_prepare / the FCN at create): the B image built once in global
 // memory, same layout as in shared memory ([j][NB*K][16 B]); the conv then copies it instead of
 // staging and expanding the packed bank in every CTA.
-template <int K, int NSEG, int STR, bool FIRST, bool F4>
+template <int K, int CT, int NSEG, int STR, bool FIRST, bool F4>
 __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* out) {
     const uint32_t* wsrc[kMaxSeg] = {cd.seg[0].wp, cd.seg[kMaxSeg - 1].wp};
-    const int total = pl.nmma * 2 * tz_nb<K, STR>() * K;
+    constexpr int NB = tz_nb<K, STR, F4, CT>();
+    const int total = pl.nmma * 2 * NB * K;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x)
-        out[u] = bimage_entry<K, NSEG, STR, FIRST, F4, tz_nb<K, STR>()>(cd, pl, wsrc, u);
+        out[u] = bimage_entry<K, NSEG, STR, FIRST, F4, NB>(cd, pl, wsrc, u);
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
@@ -295,10 +302,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // columns 480..511): exact (f32 accumulation of integers < 2^24), half the
     // shared-memory bytes per MAC and twice the int8 MMA rate.  C = 16 segments
     // hold two consecutive positions per 16-byte row (taps dx, dx+1 in one K-half).
-    constexpr bool SPLIT = STR == 1 && K == 64;
+    constexpr bool SPLIT = tz_split(K, STR, F4, CT);
     constexpr int RO = STR == 1 ? (SPLIT ? 4 : 3) : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
-    constexpr int NB = STR == 1 ? (SPLIT ? 3 : 5) : 4;
+    constexpr int NB = tz_nb<K, STR, F4, CT>();
     constexpr int CWO = (K + 31) / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     // [B image][A ring][staging ring][FIRST code planes][wpad]: during setup the packed filter
@@ -1028,7 +1035,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     // K <= 32: the whole tile's accumulators go to registers first and the block is
                     // re-initialised and handed back to the MMA issuer at once, so the next MMAs into
                     // it overlap this tile's requant / stores.  K = 64: chunk by chunk (registers).
-                    constexpr bool EARLY = K <= 32;
+                    constexpr bool EARLY = K <= 32 || (!SPLIT && STR == 1);
                     constexpr int NCH = EARLY ? K / 16 : 1;
                     int accs[NCH][16];
                     auto reinit = [&](int c) {            // the output that reuses the block starts at -hi
@@ -1216,7 +1223,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         cd.Ho != out_extent(cd.Hci, pl.s, pl.dil, pl.dil) || cd.Wo != out_extent(cd.Wci, pl.s, pl.dil, pl.dil))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    const bool split = pl.s == 1 && pl.kp == 64;
+    const bool split = tz_split(pl.kp, pl.s, f4, ct);
     pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
@@ -1408,13 +1415,13 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     if (!pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_) {                                    \
         kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, false>                     \
                     : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, false>;                        \
-        bkern = bimage_build_kernel<K, NSEG_, STR_, false, false>;                                     \
+        bkern = bimage_build_kernel<K, CT_, NSEG_, STR_, false, false>;                                     \
     }
 #define TZ_PICK4(CT_, NSEG_, STR_)                                                                    \
     if (pl.f4 && ct == CT_ && cd.nseg == NSEG_ && pl.s == STR_) {                                     \
         kern = pred ? conv_tz_kernel<K, CT_, NSEG_, STR_, (K <= 32), false, true>                      \
                     : conv_tz_kernel<K, CT_, NSEG_, STR_, false, false, true>;                         \
-        bkern = bimage_build_kernel<K, NSEG_, STR_, false, true>;                                      \
+        bkern = bimage_build_kernel<K, CT_, NSEG_, STR_, false, true>;                                      \
     }
     TZ_PICK(1, 1, 1) TZ_PICK(2, 1, 1) TZ_PICK(3, 1, 1) TZ_PICK(4, 1, 1)
     TZ_PICK(2, 2, 1) TZ_PICK(3, 2, 1) TZ_PICK(4, 2, 1)
@@ -1522,13 +1529,16 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
 static bool plan_any(const ConvDesc& cd, TzPlan& pl, bool allow_f4) {
     const bool allow_any_f4 = allow_f4;
     // Measured (tools/conv_time.py, configs[3] layer shapes): FP4 wins for stride-1
-    // layers with K <= 32 (#4 -10 %, #10 -21 %, #12 -23 %, #13 -2 %); at C = K = 64 the
-    // FP4 kernel is bound by shared-memory operand bandwidth (10 KB per 96-cycle MMA)
-    // and only 4 % faster, and at stride 2 with C = 32 it is slower.
+    // layers with K <= 32 (#4 -10 %, #10 -21 %, #12 -23 %, #13 -2 %) and at stride 2
+    // with C = 32 it is slower.
     int c_tot = 0;
     for (int i = 0; i < cd.nseg; ++i) c_tot += cd.seg[i].c;
     // C > 64 (the 64 + 64 -> 64 decoder block) only fits with FP4 operands (half the B bytes)
-    allow_f4 = allow_f4 && ((cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16)) || c_tot > 64);
+    // K in 33..64 at stride 1 with C <= 64: FP4 without the split (five-block rotated B image,
+    // two tiles per strip, half the halo rows per output): C1's conv 82.9 -> 75.3 us
+    const bool f4_k64 = cd.K > 32 && cd.s[0] == 1 && c_tot <= 64;
+    static const bool force_f4 = getenv("TN_TZ_FORCE_F4") != nullptr;   // (experiments)
+    allow_f4 = allow_f4 && ((cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16)) || c_tot > 64 || f4_k64 || force_f4);
     if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, pl.kp) <= 227 * 1024)
         return true;
     pl = TzPlan{};
