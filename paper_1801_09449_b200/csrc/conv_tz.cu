@@ -107,7 +107,12 @@ constexpr int kZMmaWarps = 2;
 // register budget allows (the fused-prediction variants need more registers).
 // Measured (configs[3] layers): 12 expander warps win for one-chunk and four-chunk
 // strips, 8 for two-chunk strips (#12, #13) and the fused-prediction variant.
-__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct) { return (pred || ct == 2) ? 8 : (k == 64 ? 9 : 12); }
+#ifndef TN_EXP64
+#define TN_EXP64 9   // expander warps at K = 64 (20 warps in all: 96 registers per thread)
+#endif
+__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct) {
+    return (pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12);
+}
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
 // (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
 __host__ __device__ constexpr int tz_epi_groups(int, bool, int) { return 2; }
@@ -431,17 +436,17 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
 
     if (warp < kZEpiWarps) {
         // ---- initialise this warp's TMEM blocks (its quadrant, its tiles, all RO blocks)
+        // (K = 16: -hi, see the epilogue's REGT; K >= 32: zero, -hi is added in the requant)
         const int q = warp & 3, g = warp >> 2;
-        int iv[K];
+        int iv[16];
 #pragma unroll
-        for (int k = 0; k < K; ++k) iv[k] = s_nhi[k];
+        for (int k = 0; k < 16; ++k) iv[k] = K == 16 ? s_nhi[k] : 0;
         for (int t = 0; t < T; ++t)
             if (t % kZEpiGroups == g)
             for (int b = 0; b < RO; ++b)
 #pragma unroll
                 for (int c = 0; c < K; c += 16)
-                    tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (t * RO + b) * K + c,
-                              *reinterpret_cast<const int(*)[16]>(iv + c));
+                    tmem_st16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + (t * RO + b) * K + c, iv);
         if (F4 && g == 0) {   // unit block scales (UE8M0 0x7F = 2^0) in columns 480..511
             int sf[16];
 #pragma unroll
@@ -1009,11 +1014,14 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 // of nlo = (acc_k > lo_k) = ((lo-hi) - d < 0).  F4: f32 accumulators start at 0.5 - hi
                 // and lmh = lo - hi + 1, so d and lmh - d are never zero (acc integer): no
                 // sign-of-zero ambiguity.  Returns sign bits (low 16) and mask bits (high 16).
-                auto requant16 = [&](const int* acc, const int* lmh) {
+                auto requant16 = [&](const int* acc, const int* lmh, const int* nh) {
                     uint32_t nhi = 0u, nlo = 0u;
 #pragma unroll
                     for (int i = 15; i >= 0; --i) {
-                        const int d = acc[i];
+                        // K >= 32: the block started at zero, so d = acc + (-hi) here (F4: + 0.5 - hi)
+                        const int d = REGT ? acc[i]
+                                           : (F4 ? __float_as_int(__int_as_float(acc[i]) + __int_as_float(nh[i]))
+                                                 : acc[i] + nh[i]);
                         nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
                         const int e = F4 ? __float_as_int(__int_as_float(lmh[i]) - __int_as_float(d)) : lmh[i] - d;
                         nlo = __funnelshift_l(static_cast<uint32_t>(e), nlo, 1);
@@ -1038,18 +1046,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     constexpr bool EARLY = K <= 32 || (!SPLIT && STR == 1);
                     constexpr int NCH = EARLY ? K / 16 : 1;
                     int accs[NCH][16];
-                    auto reinit = [&](int c) {            // the output that reuses the block starts at -hi
-                        if constexpr (REGT) {
-                            tmem_st16(taddr + c, r_nhi);
-                        } else {
-                            int nhv[16];
-#pragma unroll
-                            for (int i4 = 0; i4 < 4; ++i4) {
-                                const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
-                                nhv[4 * i4] = h4.x; nhv[4 * i4 + 1] = h4.y; nhv[4 * i4 + 2] = h4.z; nhv[4 * i4 + 3] = h4.w;
-                            }
-                            tmem_st16(taddr + c, nhv);
-                        }
+                    // the output that reuses the block starts at -hi (K = 16, thresholds in registers)
+                    // or at zero (K >= 32: no threshold loads and no value registers before the
+                    // hand-back; the requant adds -hi)
+                    auto reinit = [&](int c) {
+                        if constexpr (REGT) tmem_st16(taddr + c, r_nhi);
+                        else tmem_st16_fill(taddr + c, 0);
                     };
                     if constexpr (EARLY) {
 #pragma unroll
@@ -1068,7 +1070,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             tmem_ld16(taddr + c, accs[0]);
                             tmem_wait_ld();
                         }
-                        int lmh[16];
+                        int lmh[16], nh[16];
                         if constexpr (REGT) {
 #pragma unroll
                             for (int i = 0; i < 16; ++i) lmh[i] = r_lmh[i];
@@ -1077,10 +1079,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             for (int i4 = 0; i4 < 4; ++i4) {
                                 const int4 l4 = *reinterpret_cast<const int4*>(s_lmh + c + 4 * i4);
                                 lmh[4 * i4] = l4.x; lmh[4 * i4 + 1] = l4.y; lmh[4 * i4 + 2] = l4.z; lmh[4 * i4 + 3] = l4.w;
+                                const int4 h4 = *reinterpret_cast<const int4*>(s_nhi + c + 4 * i4);
+                                nh[4 * i4] = h4.x; nh[4 * i4 + 1] = h4.y; nh[4 * i4 + 2] = h4.z; nh[4 * i4 + 3] = h4.w;
                             }
                         }
                         if (fused) {
-                            const uint32_t bits = requant16(acc, lmh);
+                            const uint32_t bits = requant16(acc, lmh, nh);
                             const int w = c >> 5, sh = c & 31;
                             const uint32_t sb = (bits & 0xFFFFu) << sh, mb = (bits >> 16) << sh;
                             if (sh == 0) { sbits[w] = sb; mbits[w] = mb; }

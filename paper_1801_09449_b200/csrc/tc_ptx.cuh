@@ -213,6 +213,13 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const int (&v)[16]) {
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+// 16 columns of one value (one source register for all 16 operands)
+__device__ __forceinline__ void tmem_st16_fill(uint32_t taddr, int v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint64_t umma_desc_lbo(uint32_t saddr, uint32_t lbo) { return umma_desc(saddr, lbo, 128); }
 

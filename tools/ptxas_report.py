@@ -1,10 +1,11 @@
-"""Registers and spills of every conv_tz_kernel instantiation (nvcc -Xptxas -v on conv_tz.cu)."""
+"""Registers and spills of every conv_tz_kernel instantiation (nvcc -Xptxas -v on conv_tz.cu).
+usage: python tools/ptxas_report.py [source.cu] [extra nvcc flags, e.g. -DTN_EXP64=8]"""
 import re, subprocess, sys, os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = os.path.join(ROOT, "paper_1801_09449_b200", "csrc", sys.argv[1] if len(sys.argv) > 1 else "conv_tz.cu")
 r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                     "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-                    "-Xptxas", "-v", "-c", src, "-o", "/tmp/ptxas_report.o"], capture_output=True, text=True)
+                    "-Xptxas", "-v", "-c", src, "-o", "/tmp/ptxas_report.o"] + sys.argv[2:], capture_output=True, text=True)
 cur = None
 info = {}
 for line in r.stderr.splitlines():
