@@ -687,15 +687,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             } else if constexpr (CS == 32) {
                                 uint2 w = make_uint2(0u, 0u);
                                 if (ok) w = lds64(src);
-                                const uint2 e0 = expand16_f4(w.x, w.y, 0), e1 = expand16_f4(w.x, w.y, 16);
-                                sts128(dst, make_uint4(e0.x, e0.y, e1.x, e1.y));
+                                sts128(dst, expand32_f4(w.x, w.y));
                             } else {
                                 uint4 w = make_uint4(0u, 0u, 0u, 0u);
                                 if (ok) w = lds128(src);
-                                const uint2 e0 = expand16_f4(w.x, w.z, 0), e1 = expand16_f4(w.x, w.z, 16);
-                                const uint2 e2 = expand16_f4(w.y, w.w, 0), e3 = expand16_f4(w.y, w.w, 16);
-                                sts128(dst, make_uint4(e0.x, e0.y, e1.x, e1.y));
-                                sts128(dst + pl.REG, make_uint4(e2.x, e2.y, e3.x, e3.y));
+                                sts128(dst, expand32_f4(w.x, w.z));
+                                sts128(dst + pl.REG, expand32_f4(w.y, w.w));
                             }
                         }
                     }

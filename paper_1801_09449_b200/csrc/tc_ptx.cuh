@@ -72,6 +72,29 @@ __device__ __forceinline__ uint2 expand16_f4_c16(uint32_t s, uint32_t m) {
     const uint32_t hi = __byte_perm(0x22200200u, 0u, y) | __byte_perm(0x88800800u, 0u, y >> 16);
     return make_uint2(lo, hi);
 }
+// All 32 lanes of a sign / mask word pair -> 32 FP4 nibbles (16 bytes; word w = lanes 8w..8w+7).
+// The bytes of m and of the negative set nn go two per register into 16-bit lanes, are spread
+// to selector nibbles together, and each output word is two PRMTs (39 instructions instead of
+// the 60 of two expand16_f4 calls).
+__device__ __forceinline__ uint4 expand32_f4(uint32_t s, uint32_t m) {
+    const uint32_t nn = m & ~s;
+    uint32_t a = m & 0x00FF00FFu, b = (m >> 8) & 0x00FF00FFu;       // m bytes 0|2, 1|3
+    uint32_t c = nn & 0x00FF00FFu, d = (nn >> 8) & 0x00FF00FFu;     // nn bytes 0|2, 1|3
+    a = (a | (a << 4)) & 0x0F0F0F0Fu;
+    b = (b | (b << 4)) & 0x0F0F0F0Fu;
+    c = (c | (c << 4)) & 0x0F0F0F0Fu;
+    d = (d | (d << 4)) & 0x0F0F0F0Fu;
+    a = (a | (a << 2)) & 0x33333333u;
+    b = (b | (b << 2)) & 0x33333333u;
+    c = (c | (c << 2)) & 0x33333333u;
+    d = (d | (d << 2)) & 0x33333333u;
+    uint4 r;
+    r.x = __byte_perm(0x22200200u, 0u, a) | __byte_perm(0x88800800u, 0u, c);
+    r.y = __byte_perm(0x22200200u, 0u, b) | __byte_perm(0x88800800u, 0u, d);
+    r.z = __byte_perm(0x22200200u, 0u, a >> 16) | __byte_perm(0x88800800u, 0u, c >> 16);
+    r.w = __byte_perm(0x22200200u, 0u, b >> 16) | __byte_perm(0x88800800u, 0u, d >> 16);
+    return r;
+}
 __device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t sfa, uint32_t sfb) {
     asm volatile(
