@@ -348,7 +348,13 @@ tn_status tn_fold_thresholds(const float* alpha, const float* gamma, const float
  *   TN_KERNEL_TZ8   like AUTO, with the TZ kernel restricted to int8 operands
  * TN_KERNEL_AUTO picks TZ, else POPC per shape.  Host, process-wide.  (Value 2,
  * a retired second tensor-core kernel, is rejected with TN_EINVAL.)           */
-enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TZ = 3, TN_KERNEL_TZ8 = 4 };
+enum { TN_KERNEL_AUTO = 0, TN_KERNEL_POPC = 1, TN_KERNEL_TZ = 3, TN_KERNEL_TZ8 = 4, TN_KERNEL_WIDE = 5 };
+/* TN_KERNEL_WIDE is not a selector: tn_conv_kernel_for reports it for the wide
+ * one-plane layers of Table 1 (reading R18: D = 1, C a multiple of 64 per segment
+ * with C or K beyond 64, K <= 256, stride 1 / 2, pad 1, optional [up2d | skip]
+ * segments), which AUTO and TZ run on a tcgen05 kernel with FP4 operands whose
+ * filter bank streams from a prepared image (tn_conv_prepare / tn_fcn_prepare;
+ * an unprepared call builds one per call).                                    */
 tn_status tn_set_conv_kernel(int32_t which);
 int32_t   tn_get_conv_kernel(void);
 /* Upper bound on the CTAs of the persistent tensor-core conv grids (0 = one per
@@ -356,7 +362,7 @@ int32_t   tn_get_conv_kernel(void);
  * small cap to give each CTA long runs of output planes.  Host, process-wide;
  * TN_EINVAL if max_ctas < 0.                                                  */
 tn_status tn_set_grid_cap(int32_t max_ctas);
-/* Which kernel (TN_KERNEL_POPC or _TZ) a tn_conv3d_seg call with these
+/* Which kernel (TN_KERNEL_POPC, _TZ or _WIDE) a tn_conv3d_seg call with these
  * arguments would run under the current selection; -1 if the call is invalid
  * (or a forced tensor-core kernel does not cover the shape).  Host only.      */
 int32_t   tn_conv_kernel_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g);

@@ -24,6 +24,7 @@ INT64_MAX = (1 << 63) - 1
 TN_OK, TN_EINVAL, TN_ESHAPE, TN_EALIGN, TN_EUNSUPPORTED, TN_EDOMAIN, TN_ECUDA, TN_ENCCL = range(8)
 TN_LAYER_FIRST, TN_LAYER_CONV = 1, 2
 TN_KERNEL_AUTO, TN_KERNEL_POPC, TN_KERNEL_TZ, TN_KERNEL_TZ8 = 0, 1, 3, 4
+TN_KERNEL_WIDE = 5   # reported by tn_conv_kernel_for for the wide one-plane layers (not a selector)
 _STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ESHAPE", 3: "TN_EALIGN", 4: "TN_EUNSUPPORTED",
            5: "TN_EDOMAIN", 6: "TN_ECUDA", 7: "TN_ENCCL"}
 

@@ -184,6 +184,8 @@ static int pick_kernel(const ConvDesc& cd, int mode) {
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ || mode == TN_KERNEL_TZ8) &&
         conv_tz_supported(cd, mode != TN_KERNEL_TZ8))
         return TN_KERNEL_TZ;
+    // the wide one-plane layers (FP4 operands only: not under TZ8)
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ) && conv_wide_supported(cd)) return TN_KERNEL_WIDE;
     // TZ8 = AUTO with int8 TZ operands (falls back like AUTO)
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_POPC || mode == TN_KERNEL_TZ8) && cd.logits == nullptr)
         return TN_KERNEL_POPC;
@@ -193,6 +195,12 @@ static int pick_kernel(const ConvDesc& cd, int mode) {
 static cudaError_t launch_kernel(int kernel, const ConvDesc& cd, cudaStream_t st) {
     switch (kernel) {
         case TN_KERNEL_TZ: return launch_conv_tz(cd, st, g_conv_kernel != TN_KERNEL_TZ8);
+        case TN_KERNEL_WIDE: {
+            const uint4* img = nullptr;
+            unsigned mask = 0x1FFu;
+            if (!tz_prep_wide(cd.prep, cd, &img, &mask)) img = nullptr;
+            return launch_conv_wide(cd, img, mask, st);
+        }
         case TN_KERNEL_POPC: return launch_conv_popc(cd, st);
     }
     return cudaErrorNotSupported;
@@ -325,7 +333,8 @@ tn_status tn_conv_prepare(const tn_segment* segs, int32_t nseg, int32_t k, tn_ge
     TN_TRY(build_conv(sg, nseg, k, g, requant ? t : nullptr, requant ? t : nullptr, requant ? nullptr : yo,
                       requant ? const_cast<uint32_t*>(dummy) : nullptr, &cd, nullptr));
     tn_conv_prep* p = new tn_conv_prep{nullptr};
-    if (cd.N > 0 && cd.Do > 0 && cd.Ho > 0 && cd.Wo > 0 && pick_kernel(cd, g_conv_kernel) == TN_KERNEL_TZ) {
+    const int pk = cd.N > 0 && cd.Do > 0 && cd.Ho > 0 && cd.Wo > 0 ? pick_kernel(cd, g_conv_kernel) : -1;
+    if (pk == TN_KERNEL_TZ || pk == TN_KERNEL_WIDE) {
         const tn_status st = cuda_status(tz_prepare(cd, g_conv_kernel != TN_KERNEL_TZ8, &p->tz, cs(stream)),
                                          "tn_conv_prepare");
         if (st != TN_OK) { delete p; return st; }
@@ -422,7 +431,9 @@ tn_status tn_set_grid_cap(int32_t max_ctas) {
 }
 
 int32_t tn_conv_operands_for(const tn_segment* segs, int32_t nseg, int32_t k, tn_geom g) {
-    if (tn_conv_kernel_for(segs, nseg, k, g) != TN_KERNEL_TZ) return 0;
+    const int32_t kern = tn_conv_kernel_for(segs, nseg, k, g);
+    if (kern == TN_KERNEL_WIDE) return 4;
+    if (kern != TN_KERNEL_TZ) return 0;
     ConvDesc cd;
     uint32_t* dummy = reinterpret_cast<uint32_t*>(static_cast<uintptr_t>(256));
     static const int32_t zero = 0;

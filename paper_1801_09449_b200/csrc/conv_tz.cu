@@ -1597,6 +1597,8 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t st, bool allow_f4) {
 struct TzPrep {
     uint4* img;
     int bytes;
+    int wide;              // 1: an image of the wide one-plane kernel (conv_wide.cu) for tapmask
+    unsigned tapmask;
     int kp, K, f4, s, nseg, NB, nmma;
     int cch[kMaxSeg], c[kMaxSeg], cw[kMaxSeg];
     const uint32_t* wp[kMaxSeg];
@@ -1623,6 +1625,7 @@ static void prep_key(const ConvDesc& cd, const TzPlan& pl, TzPrep& k) {
 }
 
 static bool prep_matches(const TzPrep& p, const ConvDesc& cd, const TzPlan& pl) {
+    if (p.wide) return false;
     TzPrep k{};
     prep_key(cd, pl, k);
     if (k.bytes != p.bytes || k.kp != p.kp || k.K != p.K || k.f4 != p.f4 || k.s != p.s || k.nseg != p.nseg ||
@@ -1641,7 +1644,18 @@ cudaError_t tz_prepare(const ConvDesc& cd0, bool allow_f4, TzPrep** out, cudaStr
     if (!dil_ok(cd0)) return cudaSuccess;
     const ConvDesc cd = dil_class(cd0, 0);
     TzPlan pl{};
-    if (!plan_any(cd, pl, allow_f4)) return cudaSuccess;
+    if (!plan_any(cd, pl, allow_f4)) {
+        if (!allow_f4 || !conv_wide_supported(cd0)) return cudaSuccess;
+        // the wide one-plane kernel: its image and the filter bank's active taps
+        TzPrep* p = new TzPrep{};
+        p->wide = 1;
+        p->K = cd0.K; p->s = cd0.s[0]; p->nseg = cd0.nseg;
+        for (int i = 0; i < cd0.nseg; ++i) { p->c[i] = cd0.seg[i].c; p->wp[i] = cd0.seg[i].wp; }
+        cudaError_t e = wide_prepare(cd0, &p->img, &p->bytes, &p->tapmask, st);
+        if (e != cudaSuccess) { delete p; return e == cudaErrorNotSupported ? cudaSuccess : e; }
+        *out = p;
+        return cudaSuccess;
+    }
     int ct = 0;
     for (int i = 0; i < cd.nseg; ++i) ct += pl.cch[i];
     TzPrep* p = new TzPrep{};
@@ -1667,6 +1681,15 @@ void tz_prep_free(TzPrep* p) {
 }
 
 size_t tz_prep_bytes(const TzPrep* p) { return p ? static_cast<size_t>(p->bytes) : 0; }
+
+bool tz_prep_wide(const TzPrep* p, const ConvDesc& cd, const uint4** img, unsigned* tapmask) {
+    if (p == nullptr || !p->wide || p->K != cd.K || p->s != cd.s[0] || p->nseg != cd.nseg) return false;
+    for (int i = 0; i < cd.nseg; ++i)
+        if (p->c[i] != cd.seg[i].c || p->wp[i] != cd.seg[i].wp) return false;
+    *img = p->img;
+    *tapmask = p->tapmask;
+    return true;
+}
 
 static cudaError_t launch_conv_tz_one(const ConvDesc& cd0, cudaStream_t st, bool allow_f4) {
     TzPlan pl{};

@@ -145,6 +145,14 @@ cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s, bool allow_f4 = t
 // shape.  The image is a copy: it belongs to the bank's contents at prepare time.
 cudaError_t tz_prepare(const ConvDesc& cd, bool allow_f4, TzPrep** out, cudaStream_t s);
 void        tz_prep_free(TzPrep* p);
+// The wide one-plane layers (conv_wide.cu): C or K beyond 64 (C % 64 == 0 per segment, K <= 256),
+// D = 1, stride 1 / 2 with pad 1, FP4 operands.  img / tapmask from a prepared image (tz_prepare
+// makes one when the tap-offset kernel does not take the layer), or nullptr: built per call.
+bool        conv_wide_supported(const ConvDesc& cd);
+cudaError_t wide_prepare(const ConvDesc& cd, uint4** img, int* bytes, unsigned* tapmask, cudaStream_t s);
+cudaError_t launch_conv_wide(const ConvDesc& cd, const uint4* img, unsigned tapmask, cudaStream_t s);
+// a prepared wide image matching cd (same banks, widths, K, stride)
+bool        tz_prep_wide(const TzPrep* p, const ConvDesc& cd, const uint4** img, unsigned* tapmask);
 // bytes of device memory the image holds (0 for nullptr)
 size_t      tz_prep_bytes(const TzPrep* p);
 

@@ -217,10 +217,11 @@ def test_every_fcn_layer_runs_on_the_tensor_core_kernel(tn, vol):
 def test_fcn25_kernel_selection(tn):
     """Table 1's 2.5D U-Net (reading R18) at 240 x 176: the layers up to 64 channels plan onto the
     tensor-core kernel (TZ; 15 slice channels padded to 16), the 128 / 256-channel layers (whose
-    filter banks exceed the resident B image) onto popc."""
+    filter banks exceed the resident B image) onto the wide one-plane tensor-core kernel, with
+    FP4 operands; under TZ8 (int8 operands only) those fall back to popc."""
     table = tn.fcn25_table()
     couts = [row[1] for row in table]
-    ext, picks = {}, []
+    ext, picks, args = {}, [], []
     for i, (kind, co, s, segs) in enumerate(table):
         if segs[0][0] < 0:
             e, dims, ups = (1, 240, 176), [tn.dims(1, 15, 1, 240, 176)], [0]
@@ -230,6 +231,13 @@ def test_fcn25_kernel_selection(tn):
             e = (z, y * 2, x * 2) if up else (z, y, x)
             dims, ups = [tn.dims(1, couts[sj], *ext[sj]) for sj, _ in segs], [u for _, u in segs]
         picks.append(tn.tn_conv_kernel_for(dims, co, tn.geom(s), ups))
+        args.append((dims, co, tn.geom(s), ups))
         ext[i] = (1,) + tuple((v - 1) // s + 1 for v in e[1:])
-    TZ, P = tn.TN_KERNEL_TZ, tn.TN_KERNEL_POPC
-    assert picks == [TZ, TZ, TZ, P, P, P, P, P, P, P, P, P, TZ, TZ]
+    TZ, W = tn.TN_KERNEL_TZ, tn.TN_KERNEL_WIDE
+    assert picks == [TZ, TZ, TZ, W, W, W, W, W, W, W, W, W, TZ, TZ]
+    assert [tn.tn_conv_operands_for(d, co, g, u) for d, co, g, u in args[3:12]] == [4] * 9
+    try:
+        tn.tn_set_conv_kernel(tn.TN_KERNEL_TZ8)
+        assert [tn.tn_conv_kernel_for(d, co, g, u) for d, co, g, u in args[3:12]] == [tn.TN_KERNEL_POPC] * 9
+    finally:
+        tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)
