@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -56,6 +57,8 @@ struct WPlan {
     int N;                 // MMA N (output channels per group, 64 or 128)
     int ngroup;            // output-channel groups (ceil(K / N))
     int T;                 // tiles per strip
+    int nbuf;              // TMEM accumulator buffers of T * N columns (2: a unit's epilogue overlaps
+                           // the next unit's MMAs; 1: more tiles per strip, fewer halo rows and B bytes)
     int NT, nstrip, Po, RS, REG, nph;
     int nchunk;            // 64-channel chunks over both segments
     int chunk0[kMaxSeg];   // first chunk of each segment
@@ -228,8 +231,8 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
             };
             int64_t g = 0, ui = 0;
             for (int64_t u = u_beg; u < u_end; ++u, ++ui) {
-                const int buf = static_cast<int>(ui & 1);
-                if (ui >= 2) mbar_wait(acc_empty + buf, static_cast<uint32_t>((ui / 2 - 1) & 1));
+                const int buf = static_cast<int>(ui % pl.nbuf);
+                if (ui >= pl.nbuf) mbar_wait(acc_empty + buf, static_cast<uint32_t>((ui / pl.nbuf - 1) & 1));
                 tc_fence_after();
                 const uint32_t d0 = tmem + buf * (T * N);
                 for (int q = 0; q < pl.nchunk; ++q, ++g) {
@@ -258,8 +261,8 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
         int64_t ui = 0;
         for (int64_t u = u_beg; u < u_end; ++u, ++ui) {
             const WUnit wu = w_unit(u, pl);
-            const int buf = static_cast<int>(ui & 1);
-            mbar_wait(acc_full + buf, static_cast<uint32_t>((ui / 2) & 1));
+            const int buf = static_cast<int>(ui % pl.nbuf);
+            mbar_wait(acc_full + buf, static_cast<uint32_t>((ui / pl.nbuf) & 1));
             tc_fence_after();
             const int Tv = min(T, pl.NT - wu.strip * T);
             for (int t = 0; t < Tv; ++t) {
@@ -436,8 +439,12 @@ bool plan_wide(const ConvDesc& cd, unsigned tapmask, WPlan& pl) {
         pl.ntap = 1;
     }
     pl.b_bytes = pl.ntap * 2 * pl.N * 16;
-    // TMEM: two accumulator buffers of T * N columns below the scale columns (480..511)
-    const int tmax = 240 / pl.N;
+    // TMEM: nbuf accumulator buffers of T * N columns below the scale columns (480..511).  One
+    // buffer of more tiles when the layer has few chunks per unit and many halo rows per tile
+    // (the expanders and the B stream, not the MMAs, would bound it); TN_WIDE_NBUF overrides.
+    static const char* env_nbuf = getenv("TN_WIDE_NBUF");
+    pl.nbuf = env_nbuf ? std::max(1, std::min(2, atoi(env_nbuf))) : (pl.N == 128 ? 1 : 2);
+    const int tmax = (pl.nbuf == 2 ? 240 : 480) / pl.N;
     int tstart = std::min(tmax, pl.NT);
     while (tstart > 1 && static_cast<int64_t>(cd.N) * ((pl.NT + tstart - 1) / tstart) * pl.ngroup < w_num_sms())
         --tstart;
