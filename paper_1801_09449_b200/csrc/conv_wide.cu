@@ -23,8 +23,8 @@
 // thread with a 1-D bulk copy into a two-slot ring.  Accumulators live in two TMEM buffers, so
 // a unit's epilogue overlaps the next unit's MMAs.
 //
-// Warp roles: 0-3 epilogue (TMEM lane quadrant = warp), 4-11 expanders, 12 MMA issuer (and TMEM
-// allocation), 13 B loader.
+// Warp roles: 0-7 epilogue (TMEM lane quadrant = warp % 4, column half = warp / 4), 8-15
+// expanders, 16 MMA issuer (and TMEM allocation), 17 B loader.
 #include "tn_internal.cuh"
 
 #include <algorithm>
@@ -42,12 +42,12 @@ struct TzPrep;   // conv_tz.cu
 
 namespace {
 
-constexpr int kWEpiWarps = 4;
+constexpr int kWEpiWarps = 8;                         // two per TMEM lane quadrant (column halves)
 constexpr int kWExpWarps = 8;
 constexpr int kWExpThreads = kWExpWarps * 32;
-constexpr int kWMmaWarp = kWEpiWarps + kWExpWarps;   // 12
-constexpr int kWLoadWarp = kWMmaWarp + 1;              // 13
-constexpr int kWThreads = (kWLoadWarp + 1) * 32;       // 448
+constexpr int kWMmaWarp = kWEpiWarps + kWExpWarps;   // 16
+constexpr int kWLoadWarp = kWMmaWarp + 1;              // 17
+constexpr int kWThreads = (kWLoadWarp + 1) * 32;       // 576
 constexpr int kWMaxA = 4;                              // A ring slots
 constexpr int kWB = 2;                                 // B ring slots
 constexpr int kWMaxN = 128;
@@ -104,8 +104,10 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
     constexpr int NW = N / 32;                                 // output words per position (sign or mask)
     uint8_t* s_b = smem;                                       // [kWB][b_bytes]
     uint8_t* s_a = s_b + kWB * pl.b_bytes;                     // [nslot][phase][2][REG]
-    int* s_hi = reinterpret_cast<int*>(s_a + pl.nslot * pl.slot_bytes);   // [ngroup * N]
-    int* s_lo = s_hi + pl.ngroup * N;
+    // per channel, as f32 bits: nh = 0.5 - hi and lmh = lo - hi + 1 (exact: |hi|, |lo| <= 2^20);
+    // with d = acc + nh (never zero for integer acc): acc >= hi <=> d > 0, acc > lo <=> lmh - d < 0
+    int* s_hi = reinterpret_cast<int*>(s_a + pl.nslot * pl.slot_bytes);   // [ngroup * N] nh
+    int* s_lo = s_hi + pl.ngroup * N;                                      // [ngroup * N] lmh
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_lo + pl.ngroup * N);
     uint64_t* a_full = bars;                                   // [kWMaxA]
     uint64_t* a_free = a_full + kWMaxA;
@@ -119,15 +121,15 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
     const int Kp = pl.ngroup * N;
 
     for (int k = threadIdx.x; k < Kp; k += kWThreads) {
-        int h = 1 << 30, l = -(1 << 30);                      // padded channels: always 0
+        int h = 1 << 20, l = -(1 << 20);                      // padded channels: always 0
         if (fused && k < cd.K) { h = clamp_threshold(__ldg(cd.hi + k)); l = clamp_threshold(__ldg(cd.lo + k)); }
-        s_hi[k] = h;
-        s_lo[k] = l;
+        s_hi[k] = __float_as_int(0.5f - static_cast<float>(h));
+        s_lo[k] = __float_as_int(static_cast<float>(l - h + 1));
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWMaxA; ++i) { mbar_init(a_full + i, kWExpThreads); mbar_init(a_free + i, 1); }
         for (int i = 0; i < kWB; ++i) { mbar_init(b_full + i, 1); mbar_init(b_free + i, 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, 128); }
+        for (int i = 0; i < 2; ++i) { mbar_init(acc_full + i, 1); mbar_init(acc_empty + i, kWEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kWMmaWarp) {
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
-    if (warp < kWEpiWarps) {   // unit block scales (UE8M0 2^0) for the MMAs, columns 480..511
+    if (warp < 4) {   // unit block scales (UE8M0 2^0) for the MMAs, columns 480..511
         int sf[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) sf[i] = 0x7F7F7F7F;
@@ -256,8 +258,10 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
         }
         __syncwarp();
     } else {
-        // ================= epilogue (warp = TMEM lane quadrant)
-        const uint32_t lane_base = static_cast<uint32_t>(32 * warp) << 16;
+        // ================= epilogue (TMEM lane quadrant warp % 4, output-channel half warp / 4)
+        constexpr int NH = N / 2, NWH = NW / 2;                  // channels / words per half
+        const int qd = warp & 3, hf = warp >> 2;
+        const uint32_t lane_base = static_cast<uint32_t>(32 * qd) << 16;
         int64_t ui = 0;
         for (int64_t u = u_beg; u < u_end; ++u, ++ui) {
             const WUnit wu = w_unit(u, pl);
@@ -266,27 +270,35 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
             tc_fence_after();
             const int Tv = min(T, pl.NT - wu.strip * T);
             for (int t = 0; t < Tv; ++t) {
-                const int qpos = wu.strip * 128 * T + 128 * t + 32 * warp + lane;
+                const int qpos = wu.strip * 128 * T + 128 * t + 32 * qd + lane;
                 const int y = div_po_w(static_cast<uint32_t>(qpos), pl.po_magic);
                 const int x = qpos - y * pl.Po;
                 const bool vpos = x < cd.Wo && y < cd.Ho;
                 const int64_t v = (static_cast<int64_t>(wu.n) * cd.Ho + y) * cd.Wo + x;
-                uint32_t sb[NW], mb[NW];
+                uint32_t sb[NWH > 0 ? NWH : 1], mb[NWH > 0 ? NWH : 1];
 #pragma unroll
-                for (int c = 0; c < N; c += 16) {
+                for (int c = 0; c < NH; c += 16) {
                     int acc[16];
-                    tmem_ld16(tmem + lane_base + buf * (T * N) + t * N + c, acc);
+                    const int cc = hf * NH + c;                  // column / channel within the group
+                    tmem_ld16(tmem + lane_base + buf * (T * N) + t * N + cc, acc);
                     tmem_wait_ld();
-                    const int k0 = wu.grp * N + c;
+                    const int k0 = wu.grp * N + cc;
                     if (fused) {
-                        uint32_t s16 = 0u, m16 = 0u;
+                        uint32_t nhi = 0u, nlo = 0u;
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int a = __float2int_rn(__int_as_float(acc[i]));
-                            const bool pos = a >= s_hi[k0 + i], neg = a <= s_lo[k0 + i];
-                            s16 |= static_cast<uint32_t>(pos) << i;
-                            m16 |= static_cast<uint32_t>(pos || neg) << i;
+                        for (int i4 = 3; i4 >= 0; --i4) {
+                            const int4 h4 = *reinterpret_cast<const int4*>(s_hi + k0 + 4 * i4);
+                            const int4 l4 = *reinterpret_cast<const int4*>(s_lo + k0 + 4 * i4);
+                            const int hv[4] = {h4.x, h4.y, h4.z, h4.w}, lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                            for (int j = 3; j >= 0; --j) {
+                                const float d = __int_as_float(acc[4 * i4 + j]) + __int_as_float(hv[j]);
+                                nhi = __funnelshift_l(static_cast<uint32_t>(__float_as_int(d)), nhi, 1);
+                                nlo = __funnelshift_l(static_cast<uint32_t>(__float_as_int(__int_as_float(lv[j]) - d)),
+                                                      nlo, 1);
+                            }
                         }
+                        const uint32_t s16 = ~nhi & 0xFFFFu, m16 = ~(nhi & nlo) & 0xFFFFu;
                         const int w = c >> 5, sh = c & 31;
                         if (sh == 0) { sb[w] = s16; mb[w] = m16; }
                         else { sb[w] |= s16 << sh; mb[w] |= m16 << sh; }
@@ -298,12 +310,15 @@ __global__ void __launch_bounds__(kWThreads, 1) conv_wide_kernel(const ConvDesc 
                     }
                 }
                 if (fused && vpos) {
-                    uint32_t* dst = cd.yp + v * 2 * cd.cwo + wu.grp * NW;
+                    const int w0 = wu.grp * NW + hf * NWH;        // first output word of this half
+                    uint32_t* dst = cd.yp + v * 2 * cd.cwo + w0;
+                    if constexpr (NH >= 32) {
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        if (wu.grp * NW + w < cd.cwo) {
-                            dst[w] = sb[w];
-                            dst[cd.cwo + w] = mb[w];
+                        for (int w = 0; w < NWH; ++w) {
+                            if (w0 + w < cd.cwo) {
+                                dst[w] = sb[w];
+                                dst[cd.cwo + w] = mb[w];
+                            }
                         }
                     }
                 }
