@@ -181,6 +181,8 @@ namespace tn {
 // shape, else the CUDA-core popc kernel (Eq. 9 as XOR/AND/POPC: any geometry);
 // a forced selector only takes its own kernel.  -1 if nothing covers the shape.
 static int pick_kernel(const ConvDesc& cd, int mode) {
+    // one-plane layers with 64-channel-multiple segments: the wide kernel (no z-merge, 2D strips)
+    if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ) && conv_wide_supported(cd)) return TN_KERNEL_WIDE;
     if ((mode == TN_KERNEL_AUTO || mode == TN_KERNEL_TZ || mode == TN_KERNEL_TZ8) &&
         conv_tz_supported(cd, mode != TN_KERNEL_TZ8))
         return TN_KERNEL_TZ;

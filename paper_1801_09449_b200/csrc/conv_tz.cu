@@ -1644,7 +1644,7 @@ cudaError_t tz_prepare(const ConvDesc& cd0, bool allow_f4, TzPrep** out, cudaStr
     if (!dil_ok(cd0)) return cudaSuccess;
     const ConvDesc cd = dil_class(cd0, 0);
     TzPlan pl{};
-    if (!plan_any(cd, pl, allow_f4)) {
+    if ((allow_f4 && conv_wide_supported(cd0)) || !plan_any(cd, pl, allow_f4)) {
         if (!allow_f4 || !conv_wide_supported(cd0)) return cudaSuccess;
         // the wide one-plane kernel: its image and the filter bank's active taps
         TzPrep* p = new TzPrep{};

@@ -20,8 +20,9 @@
 // The B operand of a chunk -- the taps' N x 64 FP4 weights -- comes from a prepared image in
 // global memory ([group][chunk][active tap][half][N][16 B], built once by tz_prepare, taps whose
 // weights are all zero left out: the 1x1 layers #7/#8 run one MMA per chunk), copied by one
-// thread with a 1-D bulk copy into a two-slot ring.  Accumulators live in two TMEM buffers, so
-// a unit's epilogue overlaps the next unit's MMAs.
+// thread with a 1-D bulk copy into a two-slot ring.  Accumulators: one TMEM buffer of T tiles
+// (or two of fewer tiles, whose epilogue then overlaps the next unit's MMAs).  One-plane layers of
+// 64 channels in and out at stride 1 run here too (no z-merge: more tiles per strip than conv_tz).
 //
 // Warp roles: 0-7 epilogue (TMEM lane quadrant = warp % 4, column half = warp / 4), 8-15
 // expanders, 16 MMA issuer (and TMEM allocation), 17 B loader.
@@ -417,8 +418,8 @@ bool plan_wide(const ConvDesc& cd, unsigned tapmask, WPlan& pl) {
         pl.nchunk += sd.c / 64;
         c_tot += sd.c;
     }
-    // only where the tap-offset kernel does not take the layer (C or K beyond 64 per segment)
-    if (c_tot <= 64 && cd.K <= 64) return false;
+    // 64 channels in and out: stride 1 only (at stride 2 the tap-offset kernel is faster, Table 1 #3)
+    if (c_tot <= 64 && cd.K <= 64 && pl.s != 1) return false;
     if (cd.Ho != out_extent(cd.Hci, pl.s, 1, 1) || cd.Wo != out_extent(cd.Wci, pl.s, 1, 1)) return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
     pl.N = cd.K <= 64 ? 64 : 128;
@@ -455,10 +456,10 @@ bool plan_wide(const ConvDesc& cd, unsigned tapmask, WPlan& pl) {
     }
     pl.b_bytes = pl.ntap * 2 * pl.N * 16;
     // TMEM: nbuf accumulator buffers of T * N columns below the scale columns (480..511).  One
-    // buffer of more tiles when the layer has few chunks per unit and many halo rows per tile
-    // (the expanders and the B stream, not the MMAs, would bound it); TN_WIDE_NBUF overrides.
+    // buffer of more tiles measured faster on every Table-1 layer than two (the expanders and
+    // the B stream bound the layers, and more tiles per strip cut both); TN_WIDE_NBUF overrides.
     static const char* env_nbuf = getenv("TN_WIDE_NBUF");
-    pl.nbuf = env_nbuf ? std::max(1, std::min(2, atoi(env_nbuf))) : (pl.N == 128 ? 1 : 2);
+    pl.nbuf = env_nbuf ? std::max(1, std::min(2, atoi(env_nbuf))) : 1;
     const int tmax = (pl.nbuf == 2 ? 240 : 480) / pl.N;
     int tstart = std::min(tmax, pl.NT);
     while (tstart > 1 && static_cast<int64_t>(cd.N) * ((pl.NT + tstart - 1) / tstart) * pl.ngroup < w_num_sms())

@@ -217,8 +217,9 @@ def test_every_fcn_layer_runs_on_the_tensor_core_kernel(tn, vol):
 def test_fcn25_kernel_selection(tn):
     """Table 1's 2.5D U-Net (reading R18) at 240 x 176: the layers up to 64 channels plan onto the
     tensor-core kernel (TZ; 15 slice channels padded to 16), the 128 / 256-channel layers (whose
-    filter banks exceed the resident B image) onto the wide one-plane tensor-core kernel, with
-    FP4 operands; under TZ8 (int8 operands only) those fall back to popc."""
+    filter banks exceed the resident B image) and the stride-1 64-channel decoder rows #13 / #14 onto
+    the wide one-plane tensor-core kernel, with FP4 operands; under TZ8 (int8 operands only) the
+    wide layers and #13 (128 input channels) fall back to popc, #14 to TZ."""
     table = tn.fcn25_table()
     couts = [row[1] for row in table]
     ext, picks, args = {}, [], []
@@ -234,10 +235,11 @@ def test_fcn25_kernel_selection(tn):
         args.append((dims, co, tn.geom(s), ups))
         ext[i] = (1,) + tuple((v - 1) // s + 1 for v in e[1:])
     TZ, W = tn.TN_KERNEL_TZ, tn.TN_KERNEL_WIDE
-    assert picks == [TZ, TZ, TZ, W, W, W, W, W, W, W, W, W, TZ, TZ]
-    assert [tn.tn_conv_operands_for(d, co, g, u) for d, co, g, u in args[3:12]] == [4] * 9
+    assert picks == [TZ, TZ, TZ, W, W, W, W, W, W, W, W, W, W, W]
+    assert [tn.tn_conv_operands_for(d, co, g, u) for d, co, g, u in args[3:]] == [4] * 11
     try:
         tn.tn_set_conv_kernel(tn.TN_KERNEL_TZ8)
         assert [tn.tn_conv_kernel_for(d, co, g, u) for d, co, g, u in args[3:12]] == [tn.TN_KERNEL_POPC] * 9
+        assert [tn.tn_conv_kernel_for(d, co, g, u) for d, co, g, u in args[12:]] == [tn.TN_KERNEL_POPC, TZ]
     finally:
         tn.tn_set_conv_kernel(tn.TN_KERNEL_AUTO)

@@ -38,6 +38,7 @@ CASES = [
     ((1, 512, 6, 7), 192, 1),       # K not a multiple of 128, C = 512
     ((2, 64, 3, 300), 96, 1),       # wide rows, several strips per plane
     ((1, 256, 12, 16), 256, 2),
+    ((2, 64, 13, 40), 64, 1),       # #14: 64 -> 64 at stride 1 (N = 64, seven tiles per strip)
 ]
 
 
