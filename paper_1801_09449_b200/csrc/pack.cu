@@ -482,6 +482,74 @@ predict_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t tota
     }
 }
 
+// The same sums through per-block quad tables (as the fused tensor-core epilogue): entry
+// (mask nibble | sign nibble << 4) of quad qd and class j is (((t0 w0) + t1 w1) + t2 w2) + t3 w3
+// for the quad's four channels, so b + the quads' entries in ascending order is bit-identical to
+// predict_kernel.  Table layout [qd][entry][class]; persistent grid, one table build per block.
+template <int CW>
+__global__ void __launch_bounds__(256)
+predict_quad_kernel(const uint32_t* __restrict__ tp, int C, int64_t DHW, int64_t total,
+                    const float* __restrict__ w, const float* __restrict__ b, int nclass,
+                    float* __restrict__ logits, int64_t cstride) {
+    extern __shared__ float tab[];                // [8 * CW][256][nclass]
+    __shared__ float sb[kMaxClass];
+    constexpr int NQ = 8 * CW;
+    for (int e = threadIdx.x; e < NQ * 256 * nclass; e += blockDim.x) {
+        const int j = e % nclass, idx = (e / nclass) & 255, qd = e / (256 * nclass);
+        float part = 0.0f;
+        for (int i = 0; i < 4; ++i) {
+            const int c = 4 * qd + i;
+            const float wv = c < C ? __ldg(w + j * C + c) : 0.0f;
+            const bool nz = (idx >> i) & 1, ps = (idx >> (4 + i)) & 1;
+            part += nz ? (ps ? wv : -wv) : 0.0f;
+        }
+        tab[e] = part;
+    }
+    if (threadIdx.x < nclass) sb[threadIdx.x] = b[threadIdx.x];
+    __syncthreads();
+    const int nq = (C + 3) / 4;
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t ws[CW], wm[CW];
+        if constexpr (CW == 1) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(tp) + g);
+            ws[0] = v.x; wm[0] = v.y;
+        } else {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(tp) + g);
+            ws[0] = v.x; ws[1] = v.y; wm[0] = v.z; wm[1] = v.w;
+        }
+        const int64_t n = g / DHW, v = g - n * DHW;
+        if (nclass == 2) {
+            float a0 = sb[0], a1 = sb[1];
+#pragma unroll
+            for (int qd = 0; qd < NQ; ++qd) {
+                if (qd < nq) {
+                    const uint32_t sh = 4 * (qd & 7);
+                    const uint32_t ix = ((wm[qd >> 3] >> sh) & 0xFu) | (((ws[qd >> 3] >> sh) & 0xFu) << 4);
+                    const float2 e2 = *reinterpret_cast<const float2*>(tab + (qd * 256 + ix) * 2);
+                    a0 += e2.x;
+                    a1 += e2.y;
+                }
+            }
+            logits[(n * 2) * cstride + v] = a0;
+            logits[(n * 2 + 1) * cstride + v] = a1;
+        } else {
+            for (int j = 0; j < nclass; ++j) {
+                float a = sb[j];
+#pragma unroll
+                for (int qd = 0; qd < NQ; ++qd) {
+                    if (qd < nq) {
+                        const uint32_t sh = 4 * (qd & 7);
+                        const uint32_t ix = ((wm[qd >> 3] >> sh) & 0xFu) | (((ws[qd >> 3] >> sh) & 0xFu) << 4);
+                        a += tab[(qd * 256 + ix) * nclass + j];
+                    }
+                }
+                logits[(n * nclass + j) * cstride + v] = a;
+            }
+        }
+    }
+}
+
 __global__ void bad_init_kernel(int64_t* d_bad) { *d_bad = LLONG_MAX; }
 
 }  // namespace
@@ -564,6 +632,29 @@ cudaError_t launch_predict(const uint32_t* tp, tn_dims td, const float* w, const
     const int64_t DHW = static_cast<int64_t>(td.d) * td.h * td.w;
     const int64_t total = DHW * td.n;
     if (total == 0) return cudaSuccess;
+    const int cw = (td.c + 31) / 32;
+    if (total >= (1 << 16) && (reinterpret_cast<uintptr_t>(tp) & 15u) == 0 && cw <= 2) {
+        // large tensors: quad tables (bit-identical sums), a persistent grid of 4 blocks per SM
+        static int nsm = 0;
+        if (nsm == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            if (nsm <= 0) nsm = 148;
+        }
+        const size_t smem = static_cast<size_t>(8 * cw) * 256 * nclass * sizeof(float);   // <= 128 KB
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 4 * nsm));
+        if (cw == 1) {
+            cudaFuncSetAttribute(predict_quad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+            predict_quad_kernel<1><<<grid, 256, smem, s>>>(tp, td.c, DHW, total, w, b, nclass, logits,
+                                                           cstride < 0 ? DHW : cstride);
+        } else {
+            cudaFuncSetAttribute(predict_quad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+            predict_quad_kernel<2><<<grid, 256, smem, s>>>(tp, td.c, DHW, total, w, b, nclass, logits,
+                                                           cstride < 0 ? DHW : cstride);
+        }
+        return cudaGetLastError();
+    }
     predict_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
         tp, td.c, DHW, total, w, b, nclass, logits, cstride < 0 ? DHW : cstride);
     return cudaGetLastError();

@@ -399,6 +399,22 @@ def test_predict_matches_oracle(tn):
     assert np.all(np.abs(got - ref) <= tol)
 
 
+@pytest.mark.parametrize("c,nclass", [(64, 2), (16, 2), (33, 3), (64, 8), (7, 1)])
+def test_predict_large_quad_tables(tn, c, nclass):
+    """tn_predict on large tensors (>= 65536 voxels) runs the quad-table kernel: logits within R13
+    of the oracle, and bit-identical to the per-voxel kernel small tensors run (same sum order)."""
+    t = synth.ternary_codes((3, c, 4, 64, 100), 0.5, seed=c)
+    g = synth.rng(c + nclass)
+    w = (0.25 * g.standard_normal((nclass, c))).astype(np.float32)
+    b = (0.1 * g.standard_normal(nclass)).astype(np.float32)
+    ref = oracle.predict(t, w, b)
+    got = tn.tn_predict(tn.tn_pack_i8(dev(t)), c, dev(w), dev(b)).cpu().numpy()
+    tol = np.maximum(np.abs(ref), _logit_tol(w, b) / 1e-5) * 1e-5
+    assert np.all(np.abs(got - ref) <= tol)
+    small = tn.tn_predict(tn.tn_pack_i8(dev(t[:1, :, :1])), c, dev(w), dev(b)).cpu().numpy()   # 6400 voxels
+    np.testing.assert_array_equal(small, got[:1, :, :1])
+
+
 # --------------------------------------------------------------------------- A9 FCN
 def _fcn_compare(tn, x, p, per_layer=True):
     net = tn.TernaryFCN(p["weights"], p["lo"], p["hi"], p["pred_w"], p["pred_b"], p["t_lo"], p["t_hi"])
