@@ -784,6 +784,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         // One lane runs the whole schedule (waits, MMAs, commits are per-thread
         // operations), so no warp-level bookkeeping sits in the per-tile loop.
         if (leader) {
+#ifdef TN_TRACE
+            const long long m_t0 = clock64();
+#endif
             ZWalk wk(pl.units, cd.Do, pl.nstrip);
             int n, strip, zf, zl;
             uint32_t as = 0, as_r = 0;
@@ -794,6 +797,44 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 const int Tv = min(T, pl.NT - strip * T);
                 const int zg0 = cd.zo_beg + zf, zg1 = cd.zo_beg + zl;
                 for (int i = i0; i <= i1; ++i) {
+                    if constexpr (STR == 1 && !SPLIT) {
+                        // steady state, decided without the per-output bookkeeping below (the
+                        // issuing thread is latency-bound): plane i starts output i+1 (its block
+                        // was used before: wait for the epilogue), completes output i-1 (commit)
+                        // and continues output i; all three outputs in the run
+                        const uint32_t u_lo = u_run + static_cast<uint32_t>(i - 1 - zg0);
+                        if (i >= 1 && i + 2 <= cd.Dci && i - 1 >= zg0 && i + 1 <= zg1 && u_lo + 2 >= RO) {
+                            const uint32_t r = u_lo % RO;                // sigma of output i-1
+                            const uint32_t b0 = r == 0 ? 0 : (r == 1 ? 2 : 1);
+                            const uint32_t bl_full = b_lo0 + b0 * K;
+                            const uint32_t un = u_lo + 2;
+                            const int v0 = warp - kZMmaWarp;
+                            const uint32_t wbar = smem_u32(acc_empty + (un % RO) * NU + v0), wpar = ((un / RO) - 1) & 1;
+                            const uint32_t cbar = smem_u32(acc_full + r * NU + v0);
+                            constexpr uint32_t kBarStep = 8 * kZMmaWarps;
+                            const uint32_t idesc = idesc_n(RO * K);
+                            TN_TW(4, warp == kZMmaWarp, mbar_wait(plane_full + as, as_r & 1));
+                            const uint32_t a_slot16 = (as * pl.slot_bytes) >> 4;
+                            int k = 0;
+                            for (int v = v0; v < NU; v += kZMmaWarps, ++k) {   // (units past Tv: empty commit)
+                                TN_TW(5, warp == kZMmaWarp, mbar_wait_addr(wbar + k * kBarStep, wpar));
+                                tc_fence_after();
+                                if (v < Tv) {
+                                    const uint32_t a_t = a_slot16 + v * 128;
+                                    const uint32_t d_tile = tmem_base + v * RO * K;
+                                    TN_TW(1, warp == kZMmaWarp, {
+#pragma unroll
+                                    for (int m = 0; m < NMMA; ++m)
+                                        mma(d_tile, desc64(a_lo[m] + a_t), desc64(bl_full + m * b_mma16), idesc);
+                                    });
+                                }
+                                tc_commit_addr(cbar + k * kBarStep);
+                            }
+                            tc_commit(plane_free + as);
+                            if (++as == static_cast<uint32_t>(pl.nslot)) { as = 0; ++as_r; }
+                            continue;
+                        }
+                    }
                     // outputs touched by plane i: STR 1: z = i-1, i, i+1 (dz = 2, 1, 0);
                     // STR 2: z with 2z-1 <= i <= 2z+1
                     int zlo, zhi;
@@ -864,6 +905,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             TN_TW(5, warp == kZMmaWarp, mbar_wait_addr(wbar + k * kBarStep, wpar));
                             tc_fence_after();
                             const int t1 = min(v + 1, Tv);
+                            TN_TW(1, warp == kZMmaWarp, {
                             for (int t = v; t < t1; ++t) {
                                 const uint32_t a_add = t * 128;
                                 const uint32_t d_tile = tmem_base + t * RO * K;
@@ -871,6 +913,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 for (int m = 0; m < NMMA; ++m)
                                     mma(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc);
                             }
+                            });
                             tc_commit_addr(cbar + k * kBarStep);
                         }
                     } else
@@ -926,6 +969,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }
                 u_run += zl - zf + 1;
             }
+#ifdef TN_TRACE
+            if (warp == kZMmaWarp) atomicAdd(&g_tn_trace[blockIdx.x * 8 + 7], clock64() - m_t0);   // MMA role span
+#endif
         }
         __syncwarp();
     } else {
@@ -1117,9 +1163,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         }
     }
 
-#ifdef TN_TRACE
-    if (threadIdx.x == 0) atomicAdd(&g_tn_trace[blockIdx.x * 8 + 7], clock64() - k_t0);   // epilogue warp 0 done
-#endif
+
     tc_fence_before();
     __syncthreads();
 #ifdef TN_TRACE

@@ -24,7 +24,7 @@ yp = tn.tn_conv3d_requant(xp, tn.dims(*shape), wp, k, tn.geom(s), lo, hi, yp)
 torch.cuda.synchronize()
 rd(buf.ctypes.data, buf.size, 1)
 t = buf.reshape(1024, 8)[:148].astype(np.float64)
-names = ["kernel", "epi release", "exp staged wait", "exp slot wait", "mma plane wait", "mma acc wait",
-         "epi acc wait", "epi done"]
+names = ["kernel", "mma issue (fast path)", "exp staged wait", "exp slot wait", "mma plane wait", "mma acc wait",
+         "epi acc wait", "mma role span"]
 for i, nm in enumerate(names):
     print(f"{nm:16s} mean {t[:, i].mean():10.0f}  max {t[:, i].max():10.0f}  frac {t[:, i].mean() / t[:, 0].mean():.2f}")
