@@ -626,9 +626,11 @@ def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3, t
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(L + 1)]
     ms = np.zeros(L)
     for _ in range(reps):
+        # the host queues all launches while the GPU spins, so no event pair brackets a host gap
+        torch.cuda._sleep(int(2_000_000 * (2.0 + 4.0 * forward_ms)))
         ev[0].record(stream)
         for i in range(L):
-            net.forward_range(x, i, i + 1 if i < L - 1 else -1, logits=logits, ws=ws)
+            net.forward_range(x, i, i + 1 if i < L - 1 else -1, logits=logits, ws=ws, stream=stream)
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
         ms += [ev[i].elapsed_time(ev[i + 1]) for i in range(L)]
@@ -652,7 +654,8 @@ def fcn_roofline(torch, net, x, logits, ws, stream, forward_ms, peaks, reps=3, t
                          "unit": "TMAC/s (fp4 dense)" if dom_t else "GB/s", "frac": dom["frac"], "traffic": None},
             "per_layer": per,
             "peak_source": "fp4 = 4 x MEASURED_PEAKS.bf16_tflops / 2 MAC; HBM = MEASURED_PEAKS.hbm_gbs",
-            "timing": "layers timed one at a time (tn_fcn_forward_range, events between launches); "
+            "timing": "layers timed one at a time (tn_fcn_forward_range, events between launches queued behind a "
+                      "device spin so no host gap falls between events); "
                       "frac uses the whole forward's time"}
 
 

@@ -157,6 +157,8 @@ struct TzPlan {
     int kp;                 // output channels padded to the kernel's K (16 / 32 / 64)
     int dil;                // in-plane dilation (taps dy*dil*Po + dx*dil); z dilation = residue classes
     int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
+    int rstg;               // raster staging (F4, one plain segment, stride 1): the loader copies each packed
+                            // row to pitch Po, so staged voxel = strip row and separators stay zero
 };
 
 // q / Po for 0 <= q with q * Po < 2^32
@@ -403,6 +405,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 *reinterpret_cast<uint4*>(s_b + static_cast<size_t>(u) * 16) =
                     bimage_entry<K, NSEG, STR, FIRST, F4, NB>(cd, pl, wsrc, u);
         }
+        if (pl.rstg) {   // raster staging: separator slots and rows outside the volume stay zero
+            __syncthreads();   // (the unprepared B image was read from the packed bank staged here)
+            uint4* z4 = reinterpret_cast<uint4*>(s_stage);
+            for (int i = threadIdx.x; i < pl.nstage * pl.stage_bytes / 16; i += kZThreads) z4[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
         if (PRED) {
             for (int i = threadIdx.x; i < cd.nclass; i += kZThreads) s_pred[i] = __ldg(cd.pb + i);
             // quad tables: entry (mask nibble | sign nibble << 4) = (((t0 w0) + t1 w1) + t2 w2) + t3 w3
@@ -477,6 +484,24 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
                 for (int i = i0; i <= i1; ++i) {
                     if (st_r > 0) mbar_wait(staged_empty + st, (st_r - 1) & 1);
+                    if constexpr (F4 && NSEG == 1 && STR == 1 && !FIRST) {
+                        if (pl.rstg) {   // one bulk copy per packed row, to its slot of pitch Po
+                            const SegDesc& sd = cd.seg[0];
+                            const int zs = cd.zres + i * zst - sd.zbeg;
+                            const int nrow = (zs >= 0 && zs < sd.D) ? nr[0] : 0;
+                            const uint32_t rb = static_cast<uint32_t>(sd.W) * 8u * sd.cw;
+                            const uint32_t* sp0 = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[0]) * sd.W * 2 * sd.cw;
+                            mbar_arrive_expect_tx(staged_full + st, nrow * rb);
+                            uint8_t* dst = s_stage + st * pl.stage_bytes;
+                            for (int y = 0; y < nrow; ++y) {
+                                TN_ASSERT((y + 1) * pl.Po * 8 * sd.cw <= pl.stage_bytes);
+                                bulk_g2s(dst + y * pl.Po * 8 * sd.cw, sp0 + static_cast<int64_t>(y) * sd.W * 2 * sd.cw, rb,
+                                         staged_full + st);
+                            }
+                            if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
+                            continue;
+                        }
+                    }
                     uint32_t bytes[kMaxSeg];
                     const uint32_t* src[kMaxSeg];
                     uint32_t total = 0;
@@ -639,10 +664,46 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     }
                     asm volatile("bar.sync 1, %0;" ::"r"(kZExpThreads) : "memory");
                 }
+                bool done_rows = false;
+                if constexpr (NSEG == 1 && STR == 1) {
+                    if (pl.rstg) {
+                        // raster staging: strip row r is staged voxel r - rlo (rows [rlo, rhi) hold the
+                        // copied packed rows, separators zero), so a row is one load, the expansion
+                        // and its stores
+                        int rlo = ya[0] * pl.Po - qa;
+                        const int rhi = zok[0] ? rlo + nr[0] * pl.Po : rlo;
+                        const uint32_t nval = static_cast<uint32_t>(rhi - rlo);
+                        const uint32_t sbase = smem_u32(stg) - static_cast<uint32_t>(rlo * BPV);
+                        const uint32_t a0 = smem_u32(slot) + 16;
+#pragma unroll 2
+                        for (int r = et; r < pl.RS; r += kZExpThreads) {
+                            const bool ok = static_cast<uint32_t>(r - rlo) < nval;
+                            const uint32_t dst = a0 + r * 16;
+                            TN_ASSERT(!ok || (sbase + r * BPV >= smem_u32(stg) && sbase + (r + 1) * BPV <= smem_u32(stg) + pl.stage_bytes));
+                            if constexpr (CS == 16) {
+                                uint2 w = make_uint2(0u, 0u);
+                                if (ok) w = lds64(sbase + r * BPV);
+                                const uint2 e = expand16_f4_c16(w.x, w.y);
+                                sts64(dst, e);
+                                sts64(dst - 8, e);
+                            } else if constexpr (CS == 32) {
+                                uint2 w = make_uint2(0u, 0u);
+                                if (ok) w = lds64(sbase + r * BPV);
+                                sts128(dst, expand32_f4(w.x, w.y));
+                            } else {
+                                uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                                if (ok) w = lds128(sbase + r * BPV);
+                                sts128(dst, expand32_f4(w.x, w.z));
+                                sts128(dst + pl.REG, expand32_f4(w.y, w.w));
+                            }
+                        }
+                        done_rows = true;
+                    }
+                }
                 // Row r of the strip = output raster position (y, x) (pitch Po); the plain
                 // segment's staged voxel index L = y * Wp + x (stride 2: phase (py, px) reads
                 // 2L + py * Wp + px) and the row's A address advance incrementally.
-                int r = et;
+                int r = done_rows ? pl.RS : et;
                 int y, x;
                 {
                     const uint32_t tq = static_cast<uint32_t>(qa + r) + two_po;
@@ -1273,6 +1334,13 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.nph = pl.s == 1 ? 1 : 4;
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
     pl.Po = cd.Wo + pl.dil;                    // dil zero separator columns per raster row
+    {   // raster staging: whole packed rows copied to 16-byte aligned slots of pitch Po
+        const int bpv = first || cd.nseg != 1 ? 0 : 8 * cd.seg[0].cw;
+        static const bool no_rstg = getenv("TN_TZ_NO_RSTG") != nullptr;   // A/B switch (measurement)
+        pl.rstg = !no_rstg && f4 && cd.nseg == 1 && pl.s == 1 && !first && pl.dil == 1 && bpv > 0 &&
+                  (cd.seg[0].W * bpv) % 16 == 0;
+        if (pl.rstg && (pl.Po * bpv) % 16) ++pl.Po;    // a second separator column keeps rows aligned
+    }
     pl.qoff = pl.dil * pl.Po + pl.dil;
     pl.yoff = pl.dil + 1;
     const int64_t npo = static_cast<int64_t>(cd.Ho) * pl.Po;
@@ -1393,7 +1461,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                 maxr = std::max(maxr, yhi - ylo + 1);
             }
             pl.seg_off[sg] = off;
-            off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw) + (first ? 0 : 16), 128);   // + alignment head
+            if (pl.rstg) off += round_up(maxr * pl.Po * 8 * sd.cw, 128);                       // rows at pitch Po
+            else off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw) + (first ? 0 : 16), 128);   // + alignment head
             if (first) {   // ternary code planes: maxr + 2 rows of W + 8 bytes (4 zero columns each side)
                 pl.code_pitch = sd.W + 8;
                 pl.code_bytes = round_up((maxr + 2) * pl.code_pitch, 128);
