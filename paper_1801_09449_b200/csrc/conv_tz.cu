@@ -124,6 +124,8 @@ constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
 constexpr int kZMaxSlot = 4;          // A ring
 constexpr int kZMaxStage = 4;         // packed staging ring
 constexpr int kZMaxClass = 8;
+constexpr int kZBiasA = 4096;         // K = 16 accumulator-start MMA: A constants [half][128 rows][16 B]
+constexpr int kZBiasB = 512;          //                                B rows [half][16 rows][16 B]
 
 struct TzPlan {
     int s;                  // stride (1 or 2, all axes)
@@ -157,6 +159,7 @@ struct TzPlan {
     int kp;                 // output channels padded to the kernel's K (16 / 32 / 64)
     int dil;                // in-plane dilation (taps dy*dil*Po + dx*dil); z dilation = residue classes
     int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
+    int bias_bytes;         // K = 16: accumulator-start MMA operands (A constants 4 KB + B rows 512 B)
     int rstg;               // raster staging (F4, one plain segment, stride 1): the loader copies each packed
                             // row to pitch Po, so staged voxel = strip row and separators stay zero
 };
@@ -314,13 +317,19 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     constexpr int NPH = STR == 1 ? 1 : 4;
     constexpr int NB = tz_nb<K, STR, F4, CT>();
     constexpr int CWO = (K + 31) / 32;
+    // K = 16: a new output's accumulator block is started by an MMA (accumulate = 0) of constant A
+    // rows with B rows summing to its start value (-hi; F4: 1/2 - hi), issued just before the
+    // output's first data MMA; the epilogue only loads the block and hands it back
+    constexpr bool BIAS = K == 16;
     extern __shared__ __align__(128) uint8_t smem[];
     // [B image][A ring][staging ring][FIRST code planes][wpad]: during setup the packed filter
     // bank is staged in the contiguous span from the A ring to the end of wpad
     uint8_t* s_b = smem;                                         // [mma][half][NB*K][16]
     uint8_t* s_a = s_b + pl.b_bytes;                             // [slot][phase][chunk][RS][16]
     uint8_t* s_stage = s_a + pl.nslot * pl.slot_bytes;           // [stage] packed rows per segment
-    int* s_nhi = reinterpret_cast<int*>(s_stage + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes + pl.wpad);   // [K] -hi
+    // K = 16: [A constants][B start rows] of the accumulator-start MMA (BIAS, below)
+    uint8_t* s_bias = s_stage + pl.nstage * pl.stage_bytes + 2 * pl.code_bytes + pl.wpad;
+    int* s_nhi = reinterpret_cast<int*>(s_bias + pl.bias_bytes);   // [K] -hi
     int* s_lmh = s_nhi + K;                                      // [K] lo - hi
     float* s_pred = reinterpret_cast<float*>(s_lmh + K);         // [kZMaxClass] bias, then quad tables
     float* s_ptab = s_pred + kZMaxClass;
@@ -350,6 +359,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             lo_r = clamp_threshold(__ldg(cd.lo + threadIdx.x));
             hi_r = clamp_threshold(__ldg(cd.hi + threadIdx.x));
         }
+        if (BIAS) {   // |acc| <= 27 * 16 * CT: thresholds beyond act as "never" / "always"
+            constexpr int M = 27 * 16 * CT + 1;
+            hi_r = max(-M, min(hi_r, M));
+            lo_r = max(-M, min(lo_r, M));
+        }
         const uint32_t* wsrc[kMaxSeg];
         uint32_t* s_wp = reinterpret_cast<uint32_t*>(s_a);
         int ofs = 0;
@@ -375,6 +389,27 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             ofs += (nw + 3) & ~3;
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        if (BIAS) {   // accumulator-start MMA operands: A constants, B rows summing to the start value
+            for (int i = threadIdx.x; i < kZBiasA / 16; i += kZThreads) {
+                const uint32_t c = F4 ? (i < kZBiasA / 32 ? 0x22222222u : 0x77777777u) : 0x01010101u;   // 1.0 | 6.0; int8 1
+                reinterpret_cast<uint4*>(s_bias)[i] = make_uint4(c, c, c, c);
+            }
+            if (threadIdx.x < K) {
+                uint8_t* rb = s_bias + kZBiasA + threadIdx.x * 16;   // half h at + 256 h
+                if (F4) {
+                    const float v = fused ? 0.5f - static_cast<float>(hi_r) : 0.0f;
+                    const float s1 = rintf(v / 3.0f) * 0.5f;         // v = s0 + 6 s1, |s0| <= 3/2
+                    uint8_t r0[16], r1[16];
+                    e2m1_sum_row(v - 6.0f * s1, r0);
+                    e2m1_sum_row(s1, r1);
+                    for (int j = 0; j < 16; ++j) { rb[j] = r0[j]; rb[256 + j] = r1[j]; }
+                } else {
+                    int8_t r0[16], r1[16];
+                    i8_sum_row(fused ? -hi_r : 0, r0, r1);
+                    for (int j = 0; j < 16; ++j) { rb[j] = static_cast<uint8_t>(r0[j]); rb[256 + j] = static_cast<uint8_t>(r1[j]); }
+                }
+            }
+        }
         if (threadIdx.x < K) {
             if (F4) {   // f32 accumulators: acc - hi + 1/2 (exact: |hi|, |lo| <= 2^20, |acc| < 2^12)
                 s_nhi[threadIdx.x] = __float_as_int(fused ? 0.5f - static_cast<float>(hi_r) : 0.0f);
@@ -842,6 +877,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             a_lo[m] = (((a_base + pl.a_off[m]) >> 4) & 0x3FFFu) | ((static_cast<uint32_t>(pl.a_lbo[m]) >> 4) << 16);
         const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | ((b_half >> 4) << 16);
         auto desc64 = [](uint32_t lo) { return (static_cast<uint64_t>(0x4008u) << 32) | lo; };   // SBO 128, v1
+        // accumulator-start MMA (BIAS): A constants (LBO 2048), B start rows (LBO 256), N = K, overwrite
+        const uint64_t bias_a = desc64(((smem_u32(s_bias) >> 4) & 0x3FFFu) | ((2048u >> 4) << 16));
+        const uint64_t bias_b = desc64(((smem_u32(s_bias + kZBiasA) >> 4) & 0x3FFFu) | ((256u >> 4) << 16));
+        auto start_mma = [&](uint32_t d) {
+            if constexpr (F4) tc_mma_mxf4_acc(d, bias_a, bias_b, idesc_n(K), sfa, sfb, 0u);
+            else tc_mma_i8(d, bias_a, bias_b, idesc_n(K), 0u);
+        };
         // One lane runs the whole schedule (waits, MMAs, commits are per-thread
         // operations), so no warp-level bookkeeping sits in the per-tile loop.
         if (leader) {
@@ -883,6 +925,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                                 if (v < Tv) {
                                     const uint32_t a_t = a_slot16 + v * 128;
                                     const uint32_t d_tile = tmem_base + v * RO * K;
+                                    if constexpr (BIAS) start_mma(d_tile + (un % RO) * K);
                                     TN_TW(1, warp == kZMmaWarp, {
 #pragma unroll
                                     for (int m = 0; m < NMMA; ++m)
@@ -908,6 +951,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     uint32_t new_bar[3] = {0, 0, 0}, new_par[3] = {0, 0, 0}, done_bar[3] = {0, 0, 0};
                     uint32_t sgl_d[3] = {0, 0, 0}, sgl_b[3] = {0, 0, 0};
                     bool is_new[3] = {false, false, false}, is_done[3] = {false, false, false};
+                    bool is_first[3] = {false, false, false};    // plane i starts output zlo + j
                     const uint32_t u_lo = u_run + (zlo - zg0);
 #pragma unroll
                     for (int j = 0; j < 3; ++j) {
@@ -917,6 +961,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const uint32_t sg = u % RO;
                             const int first = max(STR * z - 1, 0), last = min(STR * z + 1, cd.Dci - 1);
                             is_new[j] = first == i && u >= static_cast<uint32_t>(RO);
+                            is_first[j] = first == i;
                             new_bar[j] = sg * NU;
                             new_par[j] = ((u / RO) - 1) & 1;
                             is_done[j] = last == i;
@@ -970,6 +1015,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             for (int t = v; t < t1; ++t) {
                                 const uint32_t a_add = t * 128;
                                 const uint32_t d_tile = tmem_base + t * RO * K;
+                                if constexpr (BIAS) start_mma(d_tile + sgl_d[2]);
 #pragma unroll
                                 for (int m = 0; m < NMMA; ++m)
                                     mma(d_tile, desc64(a_pl[m] + a_add), desc64(b_pl[m]), idesc);
@@ -991,6 +1037,11 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                         for (int t = v; t < t1; ++t) {
                         const uint32_t a_add = a_slot16 + t * 128;    // (t * 128 rows * 16 B) >> 4
                         const uint32_t d_tile = tmem_base + t * RO * K;
+                        if constexpr (BIAS) {
+#pragma unroll
+                            for (int j = 0; j < 3; ++j)
+                                if (is_first[j]) start_mma(d_tile + sgl_d[j]);
+                        }
                         if constexpr (SPLIT) {
                             const uint32_t idesc1 = idesc_n(g_n1 * K);
 #pragma unroll
@@ -1044,10 +1095,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         // K = 16: thresholds and the re-init values live in registers
         constexpr bool REGT = K == 16;
-        int r_lmh[16], r_nhi[16];
+        int r_lmh[16];
         if constexpr (REGT) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) { r_lmh[k] = s_lmh[k]; r_nhi[k] = s_nhi[k]; }
+            for (int k = 0; k < 16; ++k) r_lmh[k] = s_lmh[k];
         }
         while (wk.next(n, strip, zf, zl)) {
             const int Tv = min(T, pl.NT - strip * T);
@@ -1153,17 +1204,19 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     // the output that reuses the block starts at -hi (K = 16, thresholds in registers)
                     // or at zero (K >= 32: no threshold loads and no value registers before the
                     // hand-back; the requant adds -hi)
+                    // (K = 16: the accumulator-start MMA re-initialises the block, nothing to store)
                     auto reinit = [&](int c) {
-                        if constexpr (REGT) tmem_st16(taddr + c, r_nhi);
-                        else tmem_st16_fill(taddr + c, 0);
+                        if constexpr (!BIAS) tmem_st16_fill(taddr + c, 0);
                     };
                     if constexpr (EARLY) {
 #pragma unroll
                         for (int ch = 0; ch < NCH; ++ch) tmem_ld16(taddr + 16 * ch, accs[ch]);
                         tmem_wait_ld();
+                        if constexpr (!BIAS) {
 #pragma unroll
-                        for (int ch = 0; ch < NCH; ++ch) reinit(16 * ch);
-                        tmem_wait_st();
+                            for (int ch = 0; ch < NCH; ++ch) reinit(16 * ch);
+                            tmem_wait_st();
+                        }
                         tc_fence_before();
                         mbar_arrive(acc_empty + sgm * NU + v);
                     }
@@ -1262,7 +1315,7 @@ static cudaError_t launch_pdl(void (*kern)(ConvDesc, TzPlan), int grid, int thre
 
 static size_t tz_smem(const TzPlan& pl, int K) {
     return static_cast<size_t>(pl.nslot) * pl.slot_bytes + pl.b_bytes + static_cast<size_t>(pl.nstage) * pl.stage_bytes +
-           2 * static_cast<size_t>(pl.code_bytes) + pl.wpad +
+           2 * static_cast<size_t>(pl.code_bytes) + pl.wpad + pl.bias_bytes +
            2 * K * sizeof(int) + (kZMaxClass + pl.ptab_floats) * sizeof(float) +
            (2 * kZMaxSlot + 2 * kZMaxStage + 2 * kZMaxAcc) * 8 + 16;
 }
@@ -1426,6 +1479,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         if (pl.nmma > kZMaxMma || pl.nmma != (f4 ? nmma_f4 : first ? 1 : (9 * ct + 1) / 2)) return false;   // kernel unrolls
     }
     pl.b_bytes = pl.nmma * 2 * pl.NB * pl.kp * 16;
+    pl.bias_bytes = pl.kp == 16 ? kZBiasA + kZBiasB : 0;
     const int ptab = cd.logits != nullptr ? cd.nclass * (pl.kp / 4) * 256 : 0;
     pl.ptab_floats = ptab;
 

@@ -104,6 +104,45 @@ __device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb)
         : "memory");
 }
+// The same with the accumulate flag (0: D = A x B, overwriting the accumulator).
+__device__ __forceinline__ void tc_mma_mxf4_acc(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+        : "memory");
+}
+// Accumulator-start ("bias") B rows: an MMA of an A tile of constants (E2M1 1.0 in the first
+// 32-element K half, 6.0 in the second; int8: 1 everywhere) with these rows writes v into
+// every accumulator of the row's output channel, so a new output's block is initialised by
+// the tensor core in the MMA stream itself.  E2M1: v = s0 + 6 s1 with s0, s1 sums of 32
+// E2M1 codes (multiples of 1/2, |s1| <= 192: |v| <= 1344); int8: v = sum of 32 int8.
+__device__ __forceinline__ void e2m1_sum_row(float s, uint8_t (&row)[16]) {
+    // 32 nibbles summing to s (a multiple of 1/2, |s| <= 186); element 2j in the low nibble
+    const uint32_t neg = s < 0.0f ? 8u : 0u;
+    int a2 = static_cast<int>(fabsf(s) * 2.0f + 0.25f);      // |s| in halves
+    uint8_t nib[32];
+    int n = 0;
+    for (int j = 0; j < 32; ++j) nib[j] = 0;
+    while (a2 >= 12 && n < 32) { nib[n++] = 7u | neg; a2 -= 12; }        // 6.0
+    // remainder in [0, 6): as one or two E2M1 values
+    const uint8_t first[12] = {0, 1, 2, 3, 4, 4, 5, 5, 6, 6, 6, 6};        // 0 .5 1 1.5 2 2 3 3 4 4 4 4
+    const uint8_t second[12] = {0, 0, 0, 0, 0, 1, 0, 1, 0, 1, 2, 3};       // rest: 2.5 3.5 4.5 5 5.5
+    if (a2 > 0 && n < 32) nib[n++] = first[a2] | (first[a2] ? neg : 0u);
+    if (a2 > 0 && second[a2] && n < 32) nib[n++] = second[a2] | neg;
+    for (int j = 0; j < 16; ++j) row[j] = static_cast<uint8_t>(nib[2 * j] | (nib[2 * j + 1] << 4));
+}
+__device__ __forceinline__ void i8_sum_row(int v, int8_t (&row)[16], int8_t (&row2)[16]) {
+    // 32 int8 summing to v (|v| <= 32 * 127)
+    int rest = v;
+    for (int j = 0; j < 32; ++j) {
+        const int t = max(-127, min(127, rest));
+        (j < 16 ? row[j] : row2[j - 16]) = static_cast<int8_t>(t);
+        rest -= t;
+    }
+}
 // Instruction descriptor for kind::mxf4: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N, K = 64.
 __host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
     return (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
