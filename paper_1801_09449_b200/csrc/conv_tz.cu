@@ -110,14 +110,26 @@ constexpr int kZMmaWarps = 2;
 #ifndef TN_EXP64
 #define TN_EXP64 9   // expander warps at K = 64 (20 warps in all: 96 registers per thread)
 #endif
-__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct) {
-    return (pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12);
+// Plain K = 16 layers (stride 1, not FIRST, no prediction; configs[3] #2, #12): the epilogue is the
+// critical role, so three groups of four epilogue warps and eight expander warps (measured on
+// #2, one 128x256x256 volume: (groups, expanders) = (2, 12) 91.9 us, (2, 8) 90.1, (3, 12) 91.9,
+// (3, 8) 82.1, (3, 6) 85.4, (4, 8) 88.4; the two-segment #13 stays at two groups)
+#ifndef TN_E16
+#define TN_E16 3
+#endif
+#ifndef TN_X16
+#define TN_X16 8
+#endif
+__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct, bool plain) {
+    return (k == 16 && !pred && plain) ? TN_X16 : ((pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12));
 }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
 // (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
-__host__ __device__ constexpr int tz_epi_groups(int, bool, int) { return 2; }
-__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct) {
-    return (4 * tz_epi_groups(k, pred, ct) + tz_exp_warps(k, pred, ct) + kZMmaWarps + 1) * 32;
+__host__ __device__ constexpr int tz_epi_groups(int k, bool pred, int ct, bool plain) {
+    return (k == 16 && !pred && plain && ct == 1) ? TN_E16 : 2;
+}
+__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct, bool plain) {
+    return (4 * tz_epi_groups(k, pred, ct, plain) + tz_exp_warps(k, pred, ct, plain) + kZMmaWarps + 1) * 32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
@@ -292,15 +304,16 @@ __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* o
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
-__global__ void __launch_bounds__(tz_threads(K, PRED, CT), 1)
+__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && !FIRST), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
-    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT) * 32;
-    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT);
+    constexpr bool PLAIN = STR == 1 && !FIRST;
+    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN);
     constexpr int kZEpiWarps = 4 * kZEpiGroups;
     constexpr int kZExpWarp0 = kZEpiWarps;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT);
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(K, PRED, CT);
+    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -610,8 +623,13 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
             const int qa = strip * 128 * T - pl.qoff;
             for (int i = i0; i <= i1; ++i) {
-                TN_TW(2, et == 0, mbar_wait(staged_full + st, st_r & 1));
-                if (as_r > 0) TN_TW(3, et == 0, mbar_wait(plane_free + as, (as_r - 1) & 1));
+                // one warp polls the barriers, the others park on a named barrier (polling
+                // expander warps took ~15 % of the SM's issue slots from the epilogue)
+                if (et < 32) {
+                    TN_TW(2, et == 0, mbar_wait(staged_full + st, st_r & 1));
+                    if (as_r > 0) TN_TW(3, et == 0, mbar_wait(plane_free + as, (as_r - 1) & 1));
+                }
+                asm volatile("bar.sync 2, %0;" ::"r"(kZExpThreads) : "memory");
                 bool zok[kMaxSeg];
                 uint32_t head[kMaxSeg];    // the loader's 16-byte alignment head of each segment's rows
 #pragma unroll
@@ -1401,7 +1419,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct) * 32;
+    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && !first) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1614,7 +1632,7 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
         for (void*& f : configured)
             if (f == nullptr) { f = reinterpret_cast<void*>(kern); break; }
     }
-    return launch_pdl(kern, grid, tz_threads(K, pred && K <= 32, ct), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(K, pred && K <= 32, ct, pl.s == 1), smem, st, cd, pl);
 }
 
 static bool tz_instantiated(const ConvDesc& cd, const TzPlan& pl) {
@@ -1690,7 +1708,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, false), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
