@@ -120,16 +120,45 @@ constexpr int kZMmaWarps = 2;
 #ifndef TN_X16
 #define TN_X16 8
 #endif
-__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct, bool plain) {
-    return (k == 16 && !pred && plain) ? TN_X16 : ((pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12));
+// (groups, expander warps) of the K = 16 layers with the fused prediction (#14: (2, 8) 893 us,
+// (2, 6) 873, (3, 6) 804, (3, 4) 786 per configs[3] batch), of the first layer (#1: (2, 12) 702,
+// (2, 8) 725, (3, 8) 736, (3, 12) 723) and of the two-channel-chunk layers (#13: (2, 8) 820,
+// (2, 12) 801, (3, 6) 906, (2, 6) 923)
+#ifndef TN_EP16
+#define TN_EP16 3
+#endif
+#ifndef TN_XP16
+#define TN_XP16 4
+#endif
+#ifndef TN_EF16
+#define TN_EF16 2
+#endif
+#ifndef TN_XF16
+#define TN_XF16 12
+#endif
+#ifndef TN_E2S
+#define TN_E2S 2
+#endif
+#ifndef TN_X2S
+#define TN_X2S 12
+#endif
+// plain: stride 1 and not FIRST; first: FIRST
+__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct, bool plain, bool first = false) {
+    return k == 16 && first ? TN_XF16
+         : k == 16 && pred && plain && ct == 1 ? TN_XP16
+         : k == 16 && !pred && plain && ct == 2 ? TN_X2S
+         : (k == 16 && !pred && plain) ? TN_X16 : ((pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12));
 }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
 // (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
-__host__ __device__ constexpr int tz_epi_groups(int k, bool pred, int ct, bool plain) {
-    return (k == 16 && !pred && plain && ct == 1) ? TN_E16 : 2;
+__host__ __device__ constexpr int tz_epi_groups(int k, bool pred, int ct, bool plain, bool first = false) {
+    return k == 16 && first ? TN_EF16
+         : k == 16 && pred && plain && ct == 1 ? TN_EP16
+         : k == 16 && !pred && plain && ct == 2 ? TN_E2S
+         : (k == 16 && !pred && plain && ct == 1) ? TN_E16 : 2;
 }
-__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct, bool plain) {
-    return (4 * tz_epi_groups(k, pred, ct, plain) + tz_exp_warps(k, pred, ct, plain) + kZMmaWarps + 1) * 32;
+__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct, bool plain, bool first = false) {
+    return (4 * tz_epi_groups(k, pred, ct, plain, first) + tz_exp_warps(k, pred, ct, plain, first) + kZMmaWarps + 1) * 32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
@@ -304,16 +333,16 @@ __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* o
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
-__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && !FIRST), 1)
+__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && !FIRST, FIRST), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     constexpr bool PLAIN = STR == 1 && !FIRST;
-    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN) * 32;
-    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN);
+    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN, FIRST) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN, FIRST);
     constexpr int kZEpiWarps = 4 * kZEpiGroups;
     constexpr int kZExpWarp0 = kZEpiWarps;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN);
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN, FIRST);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN);
+    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN, FIRST);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -1419,7 +1448,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && !first) * 32;
+    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && !first, first) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1708,7 +1737,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fd.K == 32] = true;
     }
-    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, false), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, false, true), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
