@@ -201,6 +201,7 @@ struct TzPlan {
     int dil;                // in-plane dilation (taps dy*dil*Po + dx*dil); z dilation = residue classes
     int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
     int bias_bytes;         // K = 16: accumulator-start MMA operands (A constants 4 KB + B rows 512 B)
+    int bpv;                // staged bytes per voxel (raster staging)
     int rstg;               // raster staging (F4, one plain segment, stride 1): the loader copies each packed
                             // row to pitch Po, so staged voxel = strip row and separators stay zero
 };
@@ -268,7 +269,7 @@ __device__ __forceinline__ uint4 bimage_entry(const ConvDesc& cd, const TzPlan& 
     const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     const int tap = k < cd.K ? pl.sl_tap[j] : -1;    // padded output channels: zero filters
-    if (FIRST) {
+    if (FIRST && !F4) {
         if (j == 0) {   // byte (dy*3 + dx) = w[k][0][dz][dy][dx]
             uint32_t wv[4] = {0u, 0u, 0u, 0u};
             for (int t9 = 0; t9 < 9; ++t9) {
@@ -333,16 +334,20 @@ __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* o
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
-__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && !FIRST, FIRST), 1)
+__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && (!FIRST || F4), FIRST && !F4), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
-    constexpr bool PLAIN = STR == 1 && !FIRST;
-    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN, FIRST) * 32;
-    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN, FIRST);
+    // FIRST with F4 (FF4): the float input staged in raster rows, Eq. 6 applied per position and
+    // the code fed as a one-channel FP4 segment (the C = 16 F4 path); FIRST alone (FI8): int8 rows
+    // of the position's 9 in-plane taps
+    constexpr bool FF4 = FIRST && F4, FI8 = FIRST && !F4;
+    constexpr bool PLAIN = STR == 1 && !FI8;
+    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN, FI8) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN, FI8);
     constexpr int kZEpiWarps = 4 * kZEpiGroups;
     constexpr int kZExpWarp0 = kZEpiWarps;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN, FIRST);
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN, FI8);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN, FIRST);
+    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN, FI8);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -484,8 +489,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         }
         if (pl.rstg) {   // raster staging: separator slots and rows outside the volume stay zero
             __syncthreads();   // (the unprepared B image was read from the packed bank staged here)
+            // (FF4: a float Eq. 6 maps to 0, the midpoint of t_lo <= t_hi)
+            const uint32_t f = FF4 ? __float_as_uint(0.5f * cd.t_lo + 0.5f * cd.t_hi) : 0u;
             uint4* z4 = reinterpret_cast<uint4*>(s_stage);
-            for (int i = threadIdx.x; i < pl.nstage * pl.stage_bytes / 16; i += kZThreads) z4[i] = make_uint4(0u, 0u, 0u, 0u);
+            for (int i = threadIdx.x; i < pl.nstage * pl.stage_bytes / 16; i += kZThreads) z4[i] = make_uint4(f, f, f, f);
         }
         if (PRED) {
             for (int i = threadIdx.x; i < cd.nclass; i += kZThreads) s_pred[i] = __ldg(cd.pb + i);
@@ -561,19 +568,20 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 for (int sg = 0; sg < NSEG; ++sg) strip_rows(pl, cd, strip, sg, ya[sg], nr[sg]);
                 for (int i = i0; i <= i1; ++i) {
                     if (st_r > 0) mbar_wait(staged_empty + st, (st_r - 1) & 1);
-                    if constexpr (F4 && NSEG == 1 && STR == 1 && !FIRST) {
-                        if (pl.rstg) {   // one bulk copy per packed row, to its slot of pitch Po
+                    if constexpr (F4 && NSEG == 1 && STR == 1) {
+                        if (pl.rstg) {   // one bulk copy per packed (FF4: float) row, to its slot of pitch Po
                             const SegDesc& sd = cd.seg[0];
                             const int zs = cd.zres + i * zst - sd.zbeg;
                             const int nrow = (zs >= 0 && zs < sd.D) ? nr[0] : 0;
-                            const uint32_t rb = static_cast<uint32_t>(sd.W) * 8u * sd.cw;
-                            const uint32_t* sp0 = sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[0]) * sd.W * 2 * sd.cw;
+                            constexpr int kVb = FF4 ? 4 : 8;     // staged bytes per voxel and 32-lane word
+                            const uint32_t rb = static_cast<uint32_t>(sd.W) * kVb * sd.cw;
+                            const char* sp0 = FF4 ? reinterpret_cast<const char*>(cd.xf + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[0]) * sd.W)
+                                                  : reinterpret_cast<const char*>(sd.xp + ((static_cast<int64_t>(n) * sd.D + zs) * sd.H + ya[0]) * sd.W * 2 * sd.cw);
                             mbar_arrive_expect_tx(staged_full + st, nrow * rb);
                             uint8_t* dst = s_stage + st * pl.stage_bytes;
                             for (int y = 0; y < nrow; ++y) {
-                                TN_ASSERT((y + 1) * pl.Po * 8 * sd.cw <= pl.stage_bytes);
-                                bulk_g2s(dst + y * pl.Po * 8 * sd.cw, sp0 + static_cast<int64_t>(y) * sd.W * 2 * sd.cw, rb,
-                                         staged_full + st);
+                                TN_ASSERT((y + 1) * pl.Po * kVb * sd.cw <= pl.stage_bytes);
+                                bulk_g2s(dst + y * pl.Po * kVb * sd.cw, sp0 + static_cast<int64_t>(y) * rb, rb, staged_full + st);
                             }
                             if (++st == static_cast<uint32_t>(pl.nstage)) { st = 0; ++st_r; }
                             continue;
@@ -671,7 +679,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 }
                 const uint8_t* stg = s_stage + st * pl.stage_bytes;
                 uint8_t* slot = s_a + as * pl.slot_bytes;
-                if constexpr (FIRST) {
+                if constexpr (FI8) {
                     // step 1: Eq. 6 on the staged float rows -> int8 codes (zero border of
                     // 4 columns and one row each side); non-finite -> d_bad
                     const SegDesc& sd = cd.seg[0];
@@ -735,7 +743,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 // voxel and plane: its staged words are converted to FP4 in place first
                 // (packed 16 channels and FP4 16 channels are both 8 bytes).
                 constexpr int CS = 16 * CT / NSEG;            // channels per segment (FP4 plans: 16, 32, 64)
-                constexpr int BPV = CS > 32 ? 16 : 8;         // staged bytes per voxel
+                constexpr int BPV = FF4 ? 4 : (CS > 32 ? 16 : 8);   // staged bytes per voxel (FF4: a float)
                 constexpr bool UPC = NSEG == 2 && CS == 16;
                 if constexpr (UPC) {
                     uint2* p0 = reinterpret_cast<uint2*>(const_cast<uint8_t*>(stg) + pl.seg_off[0] + head[0]);
@@ -762,7 +770,21 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             const bool ok = static_cast<uint32_t>(r - rlo) < nval;
                             const uint32_t dst = a0 + r * 16;
                             TN_ASSERT(!ok || (sbase + r * BPV >= smem_u32(stg) && sbase + (r + 1) * BPV <= smem_u32(stg) + pl.stage_bytes));
-                            if constexpr (CS == 16) {
+                            if constexpr (FF4) {
+                                // A7 (reading R7): Eq. 6 with the float32 constants; the code is
+                                // channel 0 of a 16-channel FP4 position (+1 -> 0x2, -1 -> 0xA)
+                                float v = 0.5f * cd.t_lo + 0.5f * cd.t_hi;
+                                if (ok) v = __uint_as_float(lds32(sbase + r * BPV));
+                                const uint32_t c = v > cd.t_hi ? 0x2u : (v < cd.t_lo ? 0xAu : 0u);
+                                if (!isfinite(v) && cd.d_bad != nullptr) {   // (separators hold a finite value)
+                                    const int q = qa + r, y = q / pl.Po, x = q - y * pl.Po;
+                                    atomicMin(reinterpret_cast<long long*>(cd.d_bad),
+                                              static_cast<long long>(static_cast<int64_t>(n) * cd.bad_nstride + cd.bad_base +
+                                                                     ((static_cast<int64_t>(i) - cd.seg[0].zbeg) * cd.seg[0].H + y) * cd.seg[0].W + x));
+                                }
+                                sts64(dst, make_uint2(c, 0u));
+                                sts64(dst - 8, make_uint2(c, 0u));
+                            } else if constexpr (CS == 16) {
                                 uint2 w = make_uint2(0u, 0u);
                                 if (ok) w = lds64(sbase + r * BPV);
                                 const uint2 e = expand16_f4_c16(w.x, w.y);
@@ -1411,12 +1433,12 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     if (first) {   // one float input channel; 9 in-plane taps per 16-byte A row
         const SegDesc& sd = cd.seg[0];
         if (cd.nseg != 1 || pl.s != 1 || sd.up || sd.c != 1 || sd.W % 4 != 0 || cd.K > 32 || cd.logits != nullptr) return false;
+        if (f4 && !(cd.t_lo <= cd.t_hi)) return false;   // FF4 separators: a value Eq. 6 maps to 0
         if ((reinterpret_cast<uintptr_t>(cd.xf) & 15) || (reinterpret_cast<uintptr_t>(sd.wp) & 15)) return false;
         pl.cch[0] = 1;
         ct = 1;
     }
     if (ct > (f4 ? 8 : 4)) return false;   // F4: two 64-channel segments (the 64+64 -> 64 decoder block)
-    if (f4 && first) return false;
     pl.f4 = f4;
     pl.nreg = 0;
     for (int i = 0; i < cd.nseg; ++i) {
@@ -1435,11 +1457,13 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
     pl.Po = cd.Wo + pl.dil;                    // dil zero separator columns per raster row
     {   // raster staging: whole packed rows copied to 16-byte aligned slots of pitch Po
-        const int bpv = first || cd.nseg != 1 ? 0 : 8 * cd.seg[0].cw;
+        const int bpv = cd.nseg != 1 ? 0 : (first ? 4 : 8 * cd.seg[0].cw);   // staged bytes per voxel
         static const bool no_rstg = getenv("TN_TZ_NO_RSTG") != nullptr;   // A/B switch (measurement)
-        pl.rstg = !no_rstg && f4 && cd.nseg == 1 && pl.s == 1 && !first && pl.dil == 1 && bpv > 0 &&
-                  (cd.seg[0].W * bpv) % 16 == 0;
-        if (pl.rstg && (pl.Po * bpv) % 16) ++pl.Po;    // a second separator column keeps rows aligned
+        pl.rstg = (first && f4) ||   // FF4 only stages raster rows
+                  (!no_rstg && f4 && cd.nseg == 1 && pl.s == 1 && !first && pl.dil == 1 && bpv > 0 &&
+                   (cd.seg[0].W * bpv) % 16 == 0);
+        while (pl.rstg && (pl.Po * bpv) % 16) ++pl.Po;   // more separator columns keep rows aligned
+        pl.bpv = bpv;
     }
     pl.qoff = pl.dil * pl.Po + pl.dil;
     pl.yoff = pl.dil + 1;
@@ -1448,7 +1472,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NPo = static_cast<int>(npo);
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
-    const int exp_threads = tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && !first, first) * 32;
+    const int exp_threads =
+        tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && (!first || f4), first && !f4) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1545,7 +1570,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         pl.nstrip = (pl.NT + T - 1) / T;
         pl.RS = 128 * T + (pl.s == 1 ? 2 * pl.qoff : pl.Po + 1);
         pl.REG = round_up((pl.RS + (f4 ? 1 : 0)) * 16, 128);    // F4: a 16-byte guard row first
-        pl.slot_bytes = first ? 128 * T * 16 + 256 : pl.nph * (f4 ? pl.nreg : ct) * pl.REG + 256;
+        pl.slot_bytes = first && !f4 ? 128 * T * 16 + 256 : pl.nph * (f4 ? pl.nreg : ct) * pl.REG + 256;
         // staging: the most rows any strip reads, per segment
         int off = 0;
         for (int sg = 0; sg < cd.nseg; ++sg) {
@@ -1562,15 +1587,15 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
                 maxr = std::max(maxr, yhi - ylo + 1);
             }
             pl.seg_off[sg] = off;
-            if (pl.rstg) off += round_up(maxr * pl.Po * 8 * sd.cw, 128);                       // rows at pitch Po
+            if (pl.rstg) off += round_up(maxr * pl.Po * pl.bpv, 128);                           // rows at pitch Po
             else off += round_up(maxr * sd.W * (first ? 4 : 8 * sd.cw) + (first ? 0 : 16), 128);   // + alignment head
-            if (first) {   // ternary code planes: maxr + 2 rows of W + 8 bytes (4 zero columns each side)
+            if (first && !f4) {   // ternary code planes: maxr + 2 rows of W + 8 bytes (4 zero columns each side)
                 pl.code_pitch = sd.W + 8;
                 pl.code_bytes = round_up((maxr + 2) * pl.code_pitch, 128);
             }
         }
         pl.stage_bytes = off;
-        if (!first) pl.code_bytes = pl.code_pitch = 0;
+        if (!first || f4) pl.code_bytes = pl.code_pitch = 0;
         pl.code_off = 0;
         // packed filter bank staged in the A ring during setup
         int wbytes = 0;
@@ -1709,17 +1734,26 @@ static ConvDesc first_desc(const FirstDesc& fd) {
     return cd;
 }
 
+// FF4 (FP4 operands, raster-staged float rows, one-channel C = 16 path) when it plans, else the
+// int8 9-tap rows
+static bool plan_first(const ConvDesc& cd, TzPlan& pl) {
+    static const bool no_ff4 = getenv("TN_TZ_NO_FF4") != nullptr;   // A/B switch (measurement)
+    if (!no_ff4 && plan_tz(cd, pl, true, true) && tz_smem(pl, pl.kp) <= 227 * 1024) return true;
+    pl = TzPlan{};
+    return plan_tz(cd, pl, true, false) && tz_smem(pl, pl.kp) <= 227 * 1024;
+}
+
 bool conv_tz_first_supported(const FirstDesc& fd) {
     if (fd.K != 16 && fd.K != 32) return false;
     const ConvDesc cd = first_desc(fd);
     TzPlan pl{};
-    return plan_tz(cd, pl, true) && tz_smem(pl, pl.kp) <= 227 * 1024;
+    return plan_first(cd, pl);
 }
 
 cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
     const ConvDesc cd = first_desc(fd);
     TzPlan pl{};
-    if ((fd.K != 16 && fd.K != 32) || !plan_tz(cd, pl, true)) return cudaErrorNotSupported;
+    if ((fd.K != 16 && fd.K != 32) || !plan_first(cd, pl)) return cudaErrorNotSupported;
     const size_t smem = tz_smem(pl, pl.kp);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     if (g_num_sms_z == 0) {
@@ -1730,14 +1764,16 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
     const int cap = persistent_grid_cap() > 0 ? std::min(persistent_grid_cap(), g_num_sms_z) : g_num_sms_z;
     const int grid = static_cast<int>(std::min<int64_t>(pl.units, cap));
     void (*kern)(ConvDesc, TzPlan) =
-        fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true, false> : conv_tz_kernel<32, 1, 1, 1, false, true, false>;
-    static bool configured[2] = {false, false};
-    if (!configured[fd.K == 32]) {
+        pl.f4 ? (fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true, true> : conv_tz_kernel<32, 1, 1, 1, false, true, true>)
+              : (fd.K == 16 ? conv_tz_kernel<16, 1, 1, 1, false, true, false> : conv_tz_kernel<32, 1, 1, 1, false, true, false>);
+    static bool configured[4] = {false, false, false, false};
+    const int ci = (fd.K == 32) + 2 * pl.f4;
+    if (!configured[ci]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        configured[fd.K == 32] = true;
+        configured[ci] = true;
     }
-    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, false, true), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, pl.f4 != 0, !pl.f4), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.

@@ -240,6 +240,11 @@ __device__ __forceinline__ uint4 expand16(uint32_t s, uint32_t m, int sh) {
 }
 
 // Shared-memory loads / stores by 32-bit shared-window address.
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
