@@ -441,20 +441,16 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 const uint32_t c = F4 ? (i < kZBiasA / 32 ? 0x22222222u : 0x77777777u) : 0x01010101u;   // 1.0 | 6.0; int8 1
                 reinterpret_cast<uint4*>(s_bias)[i] = make_uint4(c, c, c, c);
             }
-            if (threadIdx.x < K) {
-                uint8_t* rb = s_bias + kZBiasA + threadIdx.x * 16;   // half h at + 256 h
-                if (F4) {
-                    const float v = fused ? 0.5f - static_cast<float>(hi_r) : 0.0f;
-                    const float s1 = rintf(v / 3.0f) * 0.5f;         // v = s0 + 6 s1, |s0| <= 3/2
-                    uint8_t r0[16], r1[16];
-                    e2m1_sum_row(v - 6.0f * s1, r0);
-                    e2m1_sum_row(s1, r1);
-                    for (int j = 0; j < 16; ++j) { rb[j] = r0[j]; rb[256 + j] = r1[j]; }
-                } else {
-                    int8_t r0[16], r1[16];
-                    i8_sum_row(fused ? -hi_r : 0, r0, r1);
-                    for (int j = 0; j < 16; ++j) { rb[j] = static_cast<uint8_t>(r0[j]); rb[256 + j] = static_cast<uint8_t>(r1[j]); }
-                }
+            // B start rows, one byte per thread: channel k, K half h, byte b
+            for (int i = threadIdx.x; i < K * 32; i += kZThreads) {
+                const int k = i >> 5, h = (i >> 4) & 1, b = i & 15;
+                int hk = 1 << 20;
+                if (fused && k < cd.K) hk = clamp_threshold(__ldg(cd.hi + k));
+                constexpr int M = 27 * 16 * CT + 1;
+                hk = max(-M, min(hk, M));
+                s_bias[kZBiasA + h * 256 + k * 16 + b] =
+                    F4 ? e2m1_start_byte(fused ? 0.5f - static_cast<float>(hk) : 0.0f, h, b)
+                       : i8_start_byte(fused ? -hk : 0, 16 * h + b);
             }
         }
         if (threadIdx.x < K) {
@@ -490,9 +486,15 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         if (pl.rstg) {   // raster staging: separator slots and rows outside the volume stay zero
             __syncthreads();   // (the unprepared B image was read from the packed bank staged here)
             // (FF4: a float Eq. 6 maps to 0, the midpoint of t_lo <= t_hi)
+            // Only the separator slots [W, Po) of each row slot: data slots are always copied before
+            // they are read, and rows outside the volume are never read.
             const uint32_t f = FF4 ? __float_as_uint(0.5f * cd.t_lo + 0.5f * cd.t_hi) : 0u;
-            uint4* z4 = reinterpret_cast<uint4*>(s_stage);
-            for (int i = threadIdx.x; i < pl.nstage * pl.stage_bytes / 16; i += kZThreads) z4[i] = make_uint4(f, f, f, f);
+            const int pitch = pl.Po * pl.bpv, sep = (pl.Po - cd.seg[0].W) * pl.bpv / 4;
+            const int rows = pl.stage_bytes / pitch;
+            for (int i = threadIdx.x; i < pl.nstage * rows * sep; i += kZThreads) {
+                const int stg = i / (rows * sep), rw = (i / sep) % rows, w = i % sep;
+                reinterpret_cast<uint32_t*>(s_stage + stg * pl.stage_bytes + rw * pitch + cd.seg[0].W * pl.bpv)[w] = f;
+            }
         }
         if (PRED) {
             for (int i = threadIdx.x; i < cd.nclass; i += kZThreads) s_pred[i] = __ldg(cd.pb + i);
@@ -1461,7 +1463,8 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         static const bool no_rstg = getenv("TN_TZ_NO_RSTG") != nullptr;   // A/B switch (measurement)
         pl.rstg = (first && f4) ||   // FF4 only stages raster rows
                   (!no_rstg && f4 && cd.nseg == 1 && pl.s == 1 && !first && pl.dil == 1 && bpv > 0 &&
-                   (cd.seg[0].W * bpv) % 16 == 0);
+                   (cd.seg[0].W * bpv) % 16 == 0 && cd.seg[0].W >= 128);   // (narrow rows: one copy per strip
+                                                                             // is faster; configs[0] 8.6 vs 7.7 us)
         while (pl.rstg && (pl.Po * bpv) % 16) ++pl.Po;   // more separator columns keep rows aligned
         pl.bpv = bpv;
     }

@@ -119,29 +119,29 @@ __device__ __forceinline__ void tc_mma_mxf4_acc(uint32_t d_tmem, uint64_t adesc,
 // every accumulator of the row's output channel, so a new output's block is initialised by
 // the tensor core in the MMA stream itself.  E2M1: v = s0 + 6 s1 with s0, s1 sums of 32
 // E2M1 codes (multiples of 1/2, |s1| <= 192: |v| <= 1344); int8: v = sum of 32 int8.
-__device__ __forceinline__ void e2m1_sum_row(float s, uint8_t (&row)[16]) {
-    // 32 nibbles summing to s (a multiple of 1/2, |s| <= 186); element 2j in the low nibble
+// Byte b of K half h of a start row (v = s0 + 6 s1, s1 the multiple of 1/2 nearest v / 6, so
+// |s0| <= 3/2): the half's 32 E2M1 codes are as many 6.0 as fit, then the remainder as one or two
+// codes (2.5 = 2 + .5, 3.5 = 3 + .5, 4.5 = 4 + .5, 5 = 4 + 1, 5.5 = 4 + 1.5); element 2j in the low
+// nibble of byte j.
+__device__ __forceinline__ uint32_t e2m1_start_nibble(float s, int j) {
     const uint32_t neg = s < 0.0f ? 8u : 0u;
-    int a2 = static_cast<int>(fabsf(s) * 2.0f + 0.25f);      // |s| in halves
-    uint8_t nib[32];
-    int n = 0;
-    for (int j = 0; j < 32; ++j) nib[j] = 0;
-    while (a2 >= 12 && n < 32) { nib[n++] = 7u | neg; a2 -= 12; }        // 6.0
-    // remainder in [0, 6): as one or two E2M1 values
-    const uint8_t first[12] = {0, 1, 2, 3, 4, 4, 5, 5, 6, 6, 6, 6};        // 0 .5 1 1.5 2 2 3 3 4 4 4 4
-    const uint8_t second[12] = {0, 0, 0, 0, 0, 1, 0, 1, 0, 1, 2, 3};       // rest: 2.5 3.5 4.5 5 5.5
-    if (a2 > 0 && n < 32) nib[n++] = first[a2] | (first[a2] ? neg : 0u);
-    if (a2 > 0 && second[a2] && n < 32) nib[n++] = second[a2] | neg;
-    for (int j = 0; j < 16; ++j) row[j] = static_cast<uint8_t>(nib[2 * j] | (nib[2 * j + 1] << 4));
+    const int a2 = static_cast<int>(fabsf(s) * 2.0f + 0.25f);   // |s| in halves
+    const int n6 = a2 / 12, rem = a2 - 12 * n6;
+    const uint32_t first = static_cast<uint32_t>(0x666655443210ull >> (4 * rem)) & 0xFu;
+    const uint32_t second = static_cast<uint32_t>(0x321010100000ull >> (4 * rem)) & 0xFu;
+    const uint32_t c = j < n6 ? 7u : (j == n6 ? first : (j == n6 + 1 ? second : 0u));
+    return c ? (c | neg) : 0u;
 }
-__device__ __forceinline__ void i8_sum_row(int v, int8_t (&row)[16], int8_t (&row2)[16]) {
-    // 32 int8 summing to v (|v| <= 32 * 127)
-    int rest = v;
-    for (int j = 0; j < 32; ++j) {
-        const int t = max(-127, min(127, rest));
-        (j < 16 ? row[j] : row2[j - 16]) = static_cast<int8_t>(t);
-        rest -= t;
-    }
+__device__ __forceinline__ uint8_t e2m1_start_byte(float v, int h, int b) {
+    const float s1 = rintf(v / 3.0f) * 0.5f;
+    const float s = h ? s1 : v - 6.0f * s1;
+    return static_cast<uint8_t>(e2m1_start_nibble(s, 2 * b) | (e2m1_start_nibble(s, 2 * b + 1) << 4));
+}
+// Element j of 32 int8 summing to v (|v| <= 32 * 127): 127s first, then the remainder.
+__device__ __forceinline__ uint8_t i8_start_byte(int v, int j) {
+    const int a = v < 0 ? -v : v;
+    const int t = max(0, min(127, a - 127 * j));
+    return static_cast<uint8_t>(static_cast<int8_t>(v < 0 ? -t : t));
 }
 // Instruction descriptor for kind::mxf4: E2M1 x E2M1, UE8M0 scales, K-major, M = 128, N, K = 64.
 __host__ __device__ constexpr uint32_t idesc_mxf4(int n) {
