@@ -142,23 +142,32 @@ constexpr int kZMmaWarps = 2;
 #ifndef TN_X2S
 #define TN_X2S 12
 #endif
-// plain: stride 1 and not FIRST; first: FIRST
-__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct, bool plain, bool first = false) {
-    return k == 16 && first ? TN_XF16
+#ifndef TN_EFF4
+#define TN_EFF4 3    // the FP4 first layer (FF4; #1: (3, 8) 537 us, (2, 8) 613, (3, 12) 605, (3, 4) 657, (4, 4) 658)
+#endif
+#ifndef TN_XFF4
+#define TN_XFF4 8
+#endif
+// plain: stride 1 and not the int8 first layer; first: the int8 first layer; ff4: the FP4 first layer
+__host__ __device__ constexpr int tz_exp_warps(int k, bool pred, int ct, bool plain, bool first = false, bool ff4 = false) {
+    return k == 16 && ff4 ? TN_XFF4
+         : k == 16 && first ? TN_XF16
          : k == 16 && pred && plain && ct == 1 ? TN_XP16
          : k == 16 && !pred && plain && ct == 2 ? TN_X2S
          : (k == 16 && !pred && plain) ? TN_X16 : ((pred || ct == 2) ? 8 : (k == 64 ? TN_EXP64 : 12));
 }
 // epilogue groups of four warps (one per TMEM lane quadrant); group g takes tiles t % groups == g
 // (three groups for K = 16 measured 2 % slower on configs[3]: the SMSPs' issue slots are shared)
-__host__ __device__ constexpr int tz_epi_groups(int k, bool pred, int ct, bool plain, bool first = false) {
-    return k == 16 && first ? TN_EF16
+__host__ __device__ constexpr int tz_epi_groups(int k, bool pred, int ct, bool plain, bool first = false, bool ff4 = false) {
+    return k == 16 && ff4 ? TN_EFF4
+         : k == 16 && first ? TN_EF16
          : k == 16 && pred && plain && ct == 1 ? TN_EP16
          : k == 16 && !pred && plain && ct == 2 ? TN_E2S
          : (k == 16 && !pred && plain && ct == 1) ? TN_E16 : 2;
 }
-__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct, bool plain, bool first = false) {
-    return (4 * tz_epi_groups(k, pred, ct, plain, first) + tz_exp_warps(k, pred, ct, plain, first) + kZMmaWarps + 1) * 32;
+__host__ __device__ constexpr int tz_threads(int k, bool pred, int ct, bool plain, bool first = false, bool ff4 = false) {
+    return (4 * tz_epi_groups(k, pred, ct, plain, first, ff4) + tz_exp_warps(k, pred, ct, plain, first, ff4) + kZMmaWarps + 1) *
+           32;
 }
 constexpr int kZMaxMma = 18;          // ceil(9 taps x 4 chunks / 2)
 constexpr int kZMaxAcc = 32;          // TMEM blocks (RO x T)
@@ -334,20 +343,20 @@ __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* o
 }
 
 template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
-__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && (!FIRST || F4), FIRST && !F4), 1)
+__global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && (!FIRST || F4), FIRST && !F4, FIRST && F4), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // FIRST with F4 (FF4): the float input staged in raster rows, Eq. 6 applied per position and
     // the code fed as a one-channel FP4 segment (the C = 16 F4 path); FIRST alone (FI8): int8 rows
     // of the position's 9 in-plane taps
     constexpr bool FF4 = FIRST && F4, FI8 = FIRST && !F4;
     constexpr bool PLAIN = STR == 1 && !FI8;
-    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN, FI8) * 32;
-    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN, FI8);
+    constexpr int kZExpThreads = tz_exp_warps(K, PRED, CT, PLAIN, FI8, FF4) * 32;
+    constexpr int kZEpiGroups = tz_epi_groups(K, PRED, CT, PLAIN, FI8, FF4);
     constexpr int kZEpiWarps = 4 * kZEpiGroups;
     constexpr int kZExpWarp0 = kZEpiWarps;
-    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN, FI8);
+    constexpr int kZMmaWarp = kZEpiWarps + tz_exp_warps(K, PRED, CT, PLAIN, FI8, FF4);
     constexpr int kZLoadWarp = kZMmaWarp + kZMmaWarps;
-    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN, FI8);
+    constexpr int kZThreads = tz_threads(K, PRED, CT, PLAIN, FI8, FF4);
     // FIRST (A7, reading R7): seg[0] is the float input; the expanders apply Eq. 6
     // and pack each position's 9 in-plane taps (dy, dx) into one 16-byte A row, so
     // a plane is one K-slice (one MMA with a zero-weight second half) and the dz
@@ -1476,7 +1485,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.NT = (pl.NPo + 127) / 128;
     pl.po_magic = static_cast<uint32_t>((0x100000000ull + pl.Po - 1) / pl.Po);
     const int exp_threads =
-        tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && (!first || f4), first && !f4) * 32;
+        tz_exp_warps(pl.kp, cd.logits != nullptr && !first, ct, pl.s == 1 && (!first || f4), first && !f4, first && f4) * 32;
     pl.step_q = exp_threads / pl.Po;
     pl.step_r = exp_threads % pl.Po;
 
@@ -1776,7 +1785,7 @@ cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[ci] = true;
     }
-    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, pl.f4 != 0, !pl.f4), smem, st, cd, pl);
+    return launch_pdl(kern, grid, tz_threads(fd.K, false, 1, pl.f4 != 0, !pl.f4, pl.f4 != 0), smem, st, cd, pl);
 }
 
 // F4 (kind::mxf4) plan if allowed and it fits, else the int8 plan.
