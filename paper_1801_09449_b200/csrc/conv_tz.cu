@@ -1175,8 +1175,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         // K = 16: thresholds and the re-init values live in registers
         constexpr bool REGT = K == 16;
+        constexpr bool LMHR = REGT;   // (thresholds re-read from shared memory per tile: #2 +3 %)
         int r_lmh[16];
-        if constexpr (REGT) {
+        if constexpr (LMHR) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) r_lmh[k] = s_lmh[k];
         }
@@ -1308,7 +1309,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             tmem_wait_ld();
                         }
                         int lmh[16], nh[16];
-                        if constexpr (REGT) {
+                        if constexpr (LMHR) {
 #pragma unroll
                             for (int i = 0; i < 16; ++i) lmh[i] = r_lmh[i];
                         } else {
