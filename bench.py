@@ -753,7 +753,7 @@ def bench_fcn25(args, tn, torch, dist, world, rank, dev, stream):
             "parity": f"passed ({int(sel.sum())} sampled logits of stacks 0-3 vs the oracle's values, R13)",
             "config": f"{synth.ROI_STACKS} stacks of 15 x {synth.STACK_H} x {synth.STACK_W} (one 138-slice ROI), "
                       "Table 1 channels 32-64-128-256, 2D convs (3x3, 1x1 at the lowest level), stride-2 rows "
-                      "for AvgPool2D, nearest x2 Upsample2D; layers above 64 channels run on the popc kernel"}
+                      "for AvgPool2D, nearest x2 Upsample2D; #1-#3 on the TZ tensor-core kernel, #4-#14 on the wide one-plane tensor-core kernel"}
 
 
 def bench_c0(args, tn, torch, dev):
