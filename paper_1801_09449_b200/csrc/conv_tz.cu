@@ -211,6 +211,7 @@ struct TzPlan {
     int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
     int bias_bytes;         // K = 16: accumulator-start MMA operands (A constants 4 KB + B rows 512 B)
     int bpv;                // staged bytes per voxel (raster staging)
+    int onep;               // one-plane volume (Dci = Do = 1): one TMEM block per tile, no z-merge
     int rstg;               // raster staging (F4, one plain segment, stride 1): the loader copies each packed
                             // row to pitch Po, so staged voxel = strip row and separators stay zero
 };
@@ -268,14 +269,15 @@ __device__ __forceinline__ void strip_rows(const TzPlan& pl, const ConvDesc& cd,
 // j = 2m + h, block b (dz of the block sequence), row k: 16 channels of W[k][chunk][dz][dy][dx]
 // as int8, or 32 FP4 nibbles.  wsrc[sg]: segment sg's packed filter bank [K][27][2][cw] (staged
 // in shared memory by the conv, read from global memory by the prepare kernel).
-template <int K, int NSEG, int STR, bool FIRST, bool F4, int NB>
+template <int K, int NSEG, int STR, bool FIRST, bool F4, int NB, bool ONEP = false>
 __device__ __forceinline__ uint4 bimage_entry(const ConvDesc& cd, const TzPlan& pl, const uint32_t* const* wsrc,
                                               int u) {
     constexpr int rows = NB * K;
     const int row = u % rows;
     const int j = u / rows;                    // slice index (2m + h)
     const int b = row / K, k = row - b * K;
-    const int dz = STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
+    // (ONEP: one-plane layers, only the middle kernel plane meets data)
+    const int dz = ONEP ? 1 : STR == 1 ? (2 - (b % 3)) : (b == 0 || b == 2 ? 0 : (b == 1 ? 2 : 1));
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     const int tap = k < cd.K ? pl.sl_tap[j] : -1;    // padded output channels: zero filters
     if (FIRST && !F4) {
@@ -333,16 +335,16 @@ __host__ __device__ constexpr int tz_nb() { return STR == 1 ? (tz_split(K, STR, 
 // Prepared filter bank (tn_weights_prepare / the FCN at create): the B image built once in global
 // memory, same layout as in shared memory ([j][NB*K][16 B]); the conv then copies it instead of
 // staging and expanding the packed bank in every CTA.
-template <int K, int CT, int NSEG, int STR, bool FIRST, bool F4>
+template <int K, int CT, int NSEG, int STR, bool FIRST, bool F4, bool ONEP = false>
 __global__ void bimage_build_kernel(const ConvDesc cd, const TzPlan pl, uint4* out) {
     const uint32_t* wsrc[kMaxSeg] = {cd.seg[0].wp, cd.seg[kMaxSeg - 1].wp};
-    constexpr int NB = tz_nb<K, STR, F4, CT>();
+    constexpr int NB = ONEP ? 1 : tz_nb<K, STR, F4, CT>();
     const int total = pl.nmma * 2 * NB * K;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x)
-        out[u] = bimage_entry<K, NSEG, STR, FIRST, F4, NB>(cd, pl, wsrc, u);
+        out[u] = bimage_entry<K, NSEG, STR, FIRST, F4, NB, ONEP>(cd, pl, wsrc, u);
 }
 
-template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4>
+template <int K, int CT, int NSEG, int STR, bool PRED, bool FIRST, bool F4, bool ONEP = false>
 __global__ void __launch_bounds__(tz_threads(K, PRED, CT, STR == 1 && (!FIRST || F4), FIRST && !F4, FIRST && F4), 1)
 conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // FIRST with F4 (FF4): the float input staged in raster rows, Eq. 6 applied per position and
@@ -368,10 +370,12 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // columns 480..511): exact (f32 accumulation of integers < 2^24), half the
     // shared-memory bytes per MAC and twice the int8 MMA rate.  C = 16 segments
     // hold two consecutive positions per 16-byte row (taps dx, dx+1 in one K-half).
-    constexpr bool SPLIT = tz_split(K, STR, F4, CT);
-    constexpr int RO = STR == 1 ? (SPLIT ? 4 : 3) : 2;
+    // ONEP (one-plane volumes, Table 1's 2D layers): no z-merge -- one TMEM block per tile, the
+    // B image holds the middle kernel plane only, and TMEM fits up to 480 / K tiles per strip
+    constexpr bool SPLIT = !ONEP && tz_split(K, STR, F4, CT);
+    constexpr int RO = ONEP ? 1 : STR == 1 ? (SPLIT ? 4 : 3) : 2;
     constexpr int NPH = STR == 1 ? 1 : 4;
-    constexpr int NB = tz_nb<K, STR, F4, CT>();
+    constexpr int NB = ONEP ? 1 : tz_nb<K, STR, F4, CT>();
     constexpr int CWO = (K + 31) / 32;
     // K = 16: a new output's accumulator block is started by an MMA (accumulate = 0) of constant A
     // rows with B rows summing to its start value (-hi; F4: 1/2 - hi), issued just before the
@@ -490,7 +494,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             const int total = pl.nmma * 2 * NB * K;
             for (int u = threadIdx.x; u < total; u += kZThreads)
                 *reinterpret_cast<uint4*>(s_b + static_cast<size_t>(u) * 16) =
-                    bimage_entry<K, NSEG, STR, FIRST, F4, NB>(cd, pl, wsrc, u);
+                    bimage_entry<K, NSEG, STR, FIRST, F4, NB, ONEP>(cd, pl, wsrc, u);
         }
         if (pl.rstg) {   // raster staging: separator slots and rows outside the volume stay zero
             __syncthreads();   // (the unprepared B image was read from the packed bank staged here)
@@ -980,7 +984,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 const int Tv = min(T, pl.NT - strip * T);
                 const int zg0 = cd.zo_beg + zf, zg1 = cd.zo_beg + zl;
                 for (int i = i0; i <= i1; ++i) {
-                    if constexpr (STR == 1 && !SPLIT) {
+                    if constexpr (STR == 1 && !SPLIT && !ONEP) {
                         // steady state, decided without the per-output bookkeeping below (the
                         // issuing thread is latency-bound): plane i starts output i+1 (its block
                         // was used before: wait for the epilogue), completes output i-1 (commit)
@@ -1048,7 +1052,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                             done_bar[j] = sg * NU;
                             const int dz = i - STR * z + 1;
                             // block holding dz: s1 [2 1 0 ..] -> 2 - dz; s2 [0 2 0 1] -> dz0:0 dz2:1 dz1:3
-                            sgl_b[j] = STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
+                            sgl_b[j] = ONEP ? 0 : STR == 1 ? 2 - dz : (dz == 0 ? 0 : (dz == 2 ? 1 : 3));
                             sgl_d[j] = sg * K;
                         }
                     }
@@ -1067,7 +1071,7 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     if (!SPLIT && full) {
                         // rotation: block position p holds the output with sigma = p
                         const uint32_t r = u_lo % RO;                 // sigma of the lowest output
-                        const uint32_t b0 = STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
+                        const uint32_t b0 = ONEP ? 0 : STR == 1 ? (r == 0 ? 0 : (r == 1 ? 2 : 1)) : (r ? 0 : 1);
                         bl_full = b_lo0 + b0 * K;
                     }
                     TN_TW(4, warp == kZMmaWarp, mbar_wait(plane_full + as, as_r & 1));
@@ -1463,10 +1467,16 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         cd.Ho != out_extent(cd.Hci, pl.s, pl.dil, pl.dil) || cd.Wo != out_extent(cd.Wci, pl.s, pl.dil, pl.dil))
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
-    const bool split = tz_split(pl.kp, pl.s, f4, ct);
-    pl.RO = pl.s == 1 ? (split ? 4 : 3) : 2;
+    // one-plane volumes (Table 1's 2D layers): only the middle kernel plane meets data
+    static const bool no_onep = getenv("TN_TZ_NO_ONEP") != nullptr;   // A/B switch (measurement)
+    // (instantiated: FP4 stride 1 with 1, 2 or 4 chunks -- Table 1's #1 257 -> 219 us and #2 318 -> 205;
+    // the int8 stride-2 #3 measured slower, 142 -> 213 us, and keeps the two-block ring)
+    pl.onep = !no_onep && !first && cd.Dci == 1 && cd.Do == 1 && cd.zo_beg == 0 && pl.dil == 1 && cd.nseg == 1 &&
+              cd.logits == nullptr && f4 && pl.s == 1 && (ct == 1 || ct == 2 || ct == 4);
+    const bool split = !pl.onep && tz_split(pl.kp, pl.s, f4, ct);
+    pl.RO = pl.onep ? 1 : pl.s == 1 ? (split ? 4 : 3) : 2;
     pl.nph = pl.s == 1 ? 1 : 4;
-    pl.NB = pl.s == 1 ? (split ? 3 : 5) : 4;
+    pl.NB = pl.onep ? 1 : pl.s == 1 ? (split ? 3 : 5) : 4;
     pl.Po = cd.Wo + pl.dil;                    // dil zero separator columns per raster row
     {   // raster staging: whole packed rows copied to 16-byte aligned slots of pitch Po
         const int bpv = cd.nseg != 1 ? 0 : (first ? 4 : 8 * cd.seg[0].cw);   // staged bytes per voxel
@@ -1684,6 +1694,14 @@ static cudaError_t launch_tz_k(const ConvDesc& cd, const TzPlan& pl, int ct, int
     TZ_PICK4(1, 1, 2) TZ_PICK4(2, 1, 2) TZ_PICK4(4, 1, 2)
 #undef TZ_PICK
 #undef TZ_PICK4
+    if (pl.onep) {   // one-plane variants (plan_tz sets onep only for these)
+        kern = nullptr;
+        bkern = nullptr;
+        if (pl.f4 && pl.s == 1 && ct == 1) { kern = conv_tz_kernel<K, 1, 1, 1, false, false, true, true>; bkern = bimage_build_kernel<K, 1, 1, 1, false, true, true>; }
+        if (pl.f4 && pl.s == 1 && ct == 2) { kern = conv_tz_kernel<K, 2, 1, 1, false, false, true, true>; bkern = bimage_build_kernel<K, 2, 1, 1, false, true, true>; }
+        if (pl.f4 && pl.s == 1 && ct == 4) { kern = conv_tz_kernel<K, 4, 1, 1, false, false, true, true>; bkern = bimage_build_kernel<K, 4, 1, 1, false, true, true>; }
+        if (pred) kern = nullptr;
+    }
     if (kern == nullptr) return cudaErrorNotSupported;
     if (build_out != nullptr) {
         const int total = pl.nmma * 2 * pl.NB * K;

@@ -209,6 +209,28 @@ def test_conv3d_requant_matches_oracle(tn, kernel, case):
     np.testing.assert_array_equal(u32(tn.tn_requant(y, dev(lo), dev(hi))), ref)
 
 
+# One-plane volumes (D = 1, Table 1's 2D layers, reading R18): the tensor-core kernel's one-plane
+# mode (one TMEM block per tile, the middle kernel plane only, wide strips): FP4 stride 1 with 1, 2
+# and 4 16-channel chunks, int8 stride 2 with 4 chunks; batches so strips and stacks interleave.
+ONEP_CASES = [((3, 16, 1, 40, 36), 16, 1), ((2, 15, 1, 48, 44), 32, 1), ((2, 32, 1, 30, 64), 64, 1),
+              ((2, 64, 1, 24, 40), 64, 1), ((3, 64, 1, 20, 36), 64, 2), ((1, 64, 1, 34, 34), 32, 2),
+              ((4, 32, 1, 9, 13), 16, 1)]
+
+
+@pytest.mark.parametrize("case", ONEP_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}_s{c[2]}")
+def test_conv3d_one_plane_matches_oracle(tn, kernel, case):
+    shape, k, s = case
+    x, w = _case(shape, k, seed=300 + k + s)
+    lo, hi = synth.jittered_thresholds(k, synth.threshold_base(shape[1], 0.5), seed=k + 1)
+    acc = oracle.conv3d(x, w, s, 1, 1)
+    ref, _ = oracle.pack(oracle.requant(acc, lo, hi))
+    xp, wp, xd = tn.tn_pack_i8(dev(x)), tn.tn_pack_weights(dev(w)), tn.dims(*shape)
+    y = run_or_skip(kernel, tn.tn_conv3d, xp, xd, wp, k, tn.geom(s))
+    np.testing.assert_array_equal(y.cpu().numpy(), np.moveaxis(acc, 1, -1))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, xd, wp, k, tn.geom(s), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+
+
 def test_conv3d_requant_sentinel_thresholds(tn, kernel):
     """INT32 sentinel thresholds (always +1 / always -1 / always 0) and lo >= hi through
     the fused epilogues of every conv kernel (no overflow in acc - hi or lo - hi)."""
