@@ -175,7 +175,9 @@ constexpr int kZMaxSlot = 4;          // A ring
 constexpr int kZMaxStage = 4;         // packed staging ring
 constexpr int kZMaxClass = 8;
 constexpr int kZBiasA = 4096;         // K = 16 accumulator-start MMA: A constants [half][128 rows][16 B]
-constexpr int kZBiasB = 512;          //                                B rows [half][16 rows][16 B]
+// B start rows [mma][half][K rows][16 B]: K = 64 FP4 takes two start MMAs (|start| <= 1729.5 > 1344)
+__host__ __device__ constexpr int tz_bias_mmas(int k, bool f4) { return f4 && k == 64 ? 2 : 1; }
+__host__ __device__ constexpr int tz_bias_bytes(int k, bool f4) { return kZBiasA + tz_bias_mmas(k, f4) * k * 32; }
 
 struct TzPlan {
     int s;                  // stride (1 or 2, all axes)
@@ -209,7 +211,7 @@ struct TzPlan {
     int kp;                 // output channels padded to the kernel's K (16 / 32 / 64)
     int dil;                // in-plane dilation (taps dy*dil*Po + dx*dil); z dilation = residue classes
     int qoff, yoff;         // strip start offset dil*Po + dil; raster rows added to keep dividends >= 0
-    int bias_bytes;         // K = 16: accumulator-start MMA operands (A constants 4 KB + B rows 512 B)
+    int bias_bytes;         // accumulator-start MMA operands (A constants 4 KB + B rows), K = 16 or FP4
     int bpv;                // staged bytes per voxel (raster staging)
     int onep;               // one-plane volume (Dci = Do = 1): one TMEM block per tile, no z-merge
     int rstg;               // raster staging (F4, one plain segment, stride 1): the loader copies each packed
@@ -380,7 +382,10 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
     // K = 16: a new output's accumulator block is started by an MMA (accumulate = 0) of constant A
     // rows with B rows summing to its start value (-hi; F4: 1/2 - hi), issued just before the
     // output's first data MMA; the epilogue only loads the block and hands it back
-    constexpr bool BIAS = K == 16;
+    // (K = 32 FP4: #4 194 -> 182 us, #11 225 -> 217; K = 64 FP4 measured slower -- C1's conv 59.4 ->
+    // 61.4 us: its MMA issuer is the busiest role and the two start MMAs add 2 to its 9 per tile)
+    constexpr bool BIAS = K == 16 || (F4 && K == 32);
+    constexpr int NBM = tz_bias_mmas(K, F4);
     extern __shared__ __align__(128) uint8_t smem[];
     // [B image][A ring][staging ring][FIRST code planes][wpad]: during setup the packed filter
     // bank is staged in the contiguous span from the A ring to the end of wpad
@@ -454,16 +459,18 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                 const uint32_t c = F4 ? (i < kZBiasA / 32 ? 0x22222222u : 0x77777777u) : 0x01010101u;   // 1.0 | 6.0; int8 1
                 reinterpret_cast<uint4*>(s_bias)[i] = make_uint4(c, c, c, c);
             }
-            // B start rows, one byte per thread: channel k, K half h, byte b
-            for (int i = threadIdx.x; i < K * 32; i += kZThreads) {
-                const int k = i >> 5, h = (i >> 4) & 1, b = i & 15;
+            // B start rows, one byte per thread: start MMA j, channel k, K half h, byte b (FP4 with two
+            // start MMAs: the first carries up to +-1300 of the start value, the second the rest)
+            for (int i = threadIdx.x; i < NBM * K * 32; i += kZThreads) {
+                const int j = i / (K * 32), k = (i >> 5) % K, h = (i >> 4) & 1, b = i & 15;
                 int hk = 1 << 20;
                 if (fused && k < cd.K) hk = clamp_threshold(__ldg(cd.hi + k));
                 constexpr int M = 27 * 16 * CT + 1;
                 hk = max(-M, min(hk, M));
-                s_bias[kZBiasA + h * 256 + k * 16 + b] =
-                    F4 ? e2m1_start_byte(fused ? 0.5f - static_cast<float>(hk) : 0.0f, h, b)
-                       : i8_start_byte(fused ? -hk : 0, 16 * h + b);
+                const float v = fused ? 0.5f - static_cast<float>(hk) : 0.0f;
+                const float va = NBM == 1 ? v : fmaxf(-1300.0f, fminf(v, 1300.0f));
+                s_bias[kZBiasA + j * K * 32 + h * K * 16 + k * 16 + b] =
+                    F4 ? e2m1_start_byte(j == 0 ? va : v - va, h, b) : i8_start_byte(fused ? -hk : 0, 16 * h + b);
             }
         }
         if (threadIdx.x < K) {
@@ -961,12 +968,16 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
             a_lo[m] = (((a_base + pl.a_off[m]) >> 4) & 0x3FFFu) | ((static_cast<uint32_t>(pl.a_lbo[m]) >> 4) << 16);
         const uint32_t b_lo0 = ((b_base >> 4) & 0x3FFFu) | ((b_half >> 4) << 16);
         auto desc64 = [](uint32_t lo) { return (static_cast<uint64_t>(0x4008u) << 32) | lo; };   // SBO 128, v1
-        // accumulator-start MMA (BIAS): A constants (LBO 2048), B start rows (LBO 256), N = K, overwrite
+        // accumulator-start MMA(s) (BIAS): A constants (LBO 2048), B start rows (LBO 16 K), N = K; the
+        // first overwrites the block
         const uint64_t bias_a = desc64(((smem_u32(s_bias) >> 4) & 0x3FFFu) | ((2048u >> 4) << 16));
-        const uint64_t bias_b = desc64(((smem_u32(s_bias + kZBiasA) >> 4) & 0x3FFFu) | ((256u >> 4) << 16));
+        const uint64_t bias_b = desc64(((smem_u32(s_bias + kZBiasA) >> 4) & 0x3FFFu) | (static_cast<uint32_t>(K) << 16));
         auto start_mma = [&](uint32_t d) {
-            if constexpr (F4) tc_mma_mxf4_acc(d, bias_a, bias_b, idesc_n(K), sfa, sfb, 0u);
-            else tc_mma_i8(d, bias_a, bias_b, idesc_n(K), 0u);
+#pragma unroll
+            for (int j = 0; j < NBM; ++j) {
+                if constexpr (F4) tc_mma_mxf4_acc(d, bias_a, bias_b + j * 2 * K, idesc_n(K), sfa, sfb, j > 0 ? 1u : 0u);
+                else tc_mma_i8(d, bias_a, bias_b, idesc_n(K), 0u);
+            }
         };
         // One lane runs the whole schedule (waits, MMAs, commits are per-thread
         // operations), so no warp-level bookkeeping sits in the per-tile loop.
@@ -1258,8 +1269,9 @@ conv_tz_kernel(const ConvDesc cd, const TzPlan pl) {
                     uint32_t nhi = 0u, nlo = 0u;
 #pragma unroll
                     for (int i = 15; i >= 0; --i) {
-                        // K >= 32: the block started at zero, so d = acc + (-hi) here (F4: + 0.5 - hi)
-                        const int d = REGT ? acc[i]
+                        // int8 K >= 32: the block started at zero, so d = acc + (-hi) here; the
+                        // accumulator-start MMA (BIAS) already started it at -hi (F4: 0.5 - hi)
+                        const int d = (REGT || BIAS) ? acc[i]
                                            : (F4 ? __float_as_int(__int_as_float(acc[i]) + __int_as_float(nh[i]))
                                                  : acc[i] + nh[i]);
                         nhi = __funnelshift_l(static_cast<uint32_t>(d), nhi, 1);
@@ -1574,7 +1586,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         if (pl.nmma > kZMaxMma || pl.nmma != (f4 ? nmma_f4 : first ? 1 : (9 * ct + 1) / 2)) return false;   // kernel unrolls
     }
     pl.b_bytes = pl.nmma * 2 * pl.NB * pl.kp * 16;
-    pl.bias_bytes = pl.kp == 16 ? kZBiasA + kZBiasB : 0;
+    pl.bias_bytes = (pl.kp == 16 || (f4 && pl.kp == 32)) ? tz_bias_bytes(pl.kp, f4) : 0;
     const int ptab = cd.logits != nullptr ? cd.nclass * (pl.kp / 4) * 256 : 0;
     pl.ptab_floats = ptab;
 
