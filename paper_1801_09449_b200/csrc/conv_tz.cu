@@ -123,7 +123,7 @@ constexpr int kZMmaWarps = 2;
 // (groups, expander warps) of the K = 16 layers with the fused prediction (#14: (2, 8) 893 us,
 // (2, 6) 873, (3, 6) 804, (3, 4) 786 per configs[3] batch), of the first layer (#1: (2, 12) 702,
 // (2, 8) 725, (3, 8) 736, (3, 12) 723) and of the two-channel-chunk layers (#13: (2, 8) 820,
-// (2, 12) 801, (3, 6) 906, (2, 6) 923)
+// (2, 12) 801, (3, 12) 782, (2, 16) 869, (1, 16) 1096, (1, 12) 1045, (3, 6) 906, (2, 6) 923)
 #ifndef TN_EP16
 #define TN_EP16 3
 #endif
@@ -137,7 +137,7 @@ constexpr int kZMmaWarps = 2;
 #define TN_XF16 12
 #endif
 #ifndef TN_E2S
-#define TN_E2S 2
+#define TN_E2S 3
 #endif
 #ifndef TN_X2S
 #define TN_X2S 12
