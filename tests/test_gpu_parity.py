@@ -788,3 +788,42 @@ def test_fcn25_table1_network_matches_oracle(tn, n, h, w):
     flag = tn.bad_flag()
     net(dev(x), ws=ws, d_bad=flag)
     assert bad_value(flag) == np.ravel_multi_index((1, 4, 0, 3, 5), x.shape)
+
+
+# Threshold ties (reading R5: +1 iff acc >= hi, -1 iff acc <= lo): sparse filters put most
+# accumulators on 0, +-1, +-2, and the thresholds sit exactly there -- lo = hi, lo = hi - 1,
+# lo > hi, hi = 0 -- so every epilogue's compare (int8 acc - hi, the FP4 f32 start value
+# 1/2 - hi, the K = 16 / 32 accumulator-start MMA, K = 64's zero start) meets its boundary
+# values in bulk.  A compare that takes the sign of an exact zero wrongly fails here.
+TIE_PAIRS = [(-1, 0), (0, 1), (-1, 1), (0, 0), (-2, 0), (0, 2), (1, 0), (-1, -1), (1, 1), (-2, 2), (2, 2), (-2, -2)]
+TIE_CASES = [   # shape, k, stride, pad
+    ((1, 16, 6, 20, 24), 16, 1, 1),
+    ((1, 32, 5, 12, 40), 32, 1, 1),
+    ((1, 64, 4, 10, 16), 64, 1, 1),
+    ((1, 16, 1, 24, 40), 16, 1, 1),    # one plane (one-plane mode on FP4)
+    ((1, 16, 6, 20, 24), 16, 2, 1),
+    ((1, 48, 3, 9, 20), 32, 1, 1),     # ragged channel chunk
+]
+
+
+@pytest.mark.parametrize("case", TIE_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_k{c[1]}_s{c[2]}")
+def test_conv3d_requant_threshold_ties(tn, kernel, case):
+    shape, k, s, p = case
+    seed = zlib.crc32(str(case).encode()) % 1000
+    x = synth.ternary_codes(shape, 0.5, seed=seed)
+    w = synth.ternary_codes((k, shape[1], 3, 3, 3), 1 - 6 / (27 * shape[1]), seed=seed + 1)   # ~6 nonzero taps
+    lo = np.array([TIE_PAIRS[i % len(TIE_PAIRS)][0] for i in range(k)], dtype=np.int32)
+    hi = np.array([TIE_PAIRS[i % len(TIE_PAIRS)][1] for i in range(k)], dtype=np.int32)
+    acc = oracle.conv3d(x, w, s, p)
+    ties = np.mean((acc == hi[None, :, None, None, None]) | (acc == lo[None, :, None, None, None]))
+    assert ties > 0.25, f"the case must put accumulators on the thresholds ({ties:.2f})"
+    ref, _ = oracle.pack(oracle.requant(acc, lo, hi))
+    xp = tn.tn_pack_i8(dev(x))
+    wp = tn.tn_pack_weights(dev(w))
+    yp = run_or_skip(kernel, tn.tn_conv3d_requant, xp, tn.dims(*shape), wp, k, tn.geom(s, p), dev(lo), dev(hi))
+    np.testing.assert_array_equal(u32(yp), ref)
+    # the prepared-bank entry (the bench's and the FCN's path) too
+    segs = [(xp, tn.dims(*shape), 0, wp)]
+    prep = tn.tn_conv_prepare(segs, k, tn.geom(s, p))
+    yp2 = run_or_skip(kernel, tn.tn_conv3d_seg_prepared, prep, segs, k, tn.geom(s, p), lo=dev(lo), hi=dev(hi))
+    np.testing.assert_array_equal(u32(yp2), ref)
