@@ -75,6 +75,9 @@ if __name__ == "__main__":
     if "--trace" in sys.argv:   # profiling build: per-role wait counters (TN_TRACE), libtn_trace.so
         print(build_library(force="--force" in sys.argv, extra=["-DTN_TRACE"],
                             lib_path=os.path.join(HERE, "libtn_trace.so"), obj_dir=os.path.join(HERE, "build_trace")))
+    elif "--ab" in sys.argv:     # measurement A/B switches read from the environment (TN_AB), libtn_ab.so
+        print(build_library(force="--force" in sys.argv, extra=["-DTN_AB"],
+                            lib_path=os.path.join(HERE, "libtn_ab.so"), obj_dir=os.path.join(HERE, "build_ab")))
     elif "--check" in sys.argv:  # device bounds checks (TN_CHECK), libtn_check.so
         print(build_library(force="--force" in sys.argv, extra=["-DTN_CHECK"],
                             lib_path=os.path.join(HERE, "libtn_check.so"), obj_dir=os.path.join(HERE, "build_check")))

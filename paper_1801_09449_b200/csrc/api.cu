@@ -5,6 +5,7 @@
 #include "tn_internal.cuh"
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -15,6 +16,14 @@ static int g_conv_kernel = TN_KERNEL_AUTO;
 static int g_grid_cap = 0;
 
 int persistent_grid_cap() { return g_grid_cap; }
+const char* ab_env(const char* name) {
+#ifdef TN_AB
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 bool first_kernel_tz_allowed() {
     return g_conv_kernel == TN_KERNEL_AUTO || g_conv_kernel == TN_KERNEL_TZ || g_conv_kernel == TN_KERNEL_TZ8;
 }

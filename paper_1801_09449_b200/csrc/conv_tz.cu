@@ -1394,7 +1394,7 @@ int g_num_sms_z = 0;
 // allocation and the shared input planes).  Measured: configs[0] 160 units -> 80 CTAs of two,
 // 7.61 -> 6.92 us per launch; configs[1] / configs[2] unchanged at any limit from 2 to 64 units.
 int tz_grid(int64_t units, int cap) {
-    static const bool no_bal = getenv("TN_TZ_NO_BALANCE") != nullptr;   // A/B switch (measurement)
+    static const bool no_bal = ab_env("TN_TZ_NO_BALANCE") != nullptr;   // A/B switch (measurement)
     const int64_t per = (units + cap - 1) / cap;
     if (no_bal || per > 4) return static_cast<int>(std::min<int64_t>(units, cap));
     return static_cast<int>((units + per - 1) / per);
@@ -1492,7 +1492,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
         return false;
     if (pl.s == 2 && (cd.Hci % 2 || cd.Wci % 2)) return false;
     // one-plane volumes (Table 1's 2D layers): only the middle kernel plane meets data
-    static const bool no_onep = getenv("TN_TZ_NO_ONEP") != nullptr;   // A/B switch (measurement)
+    static const bool no_onep = ab_env("TN_TZ_NO_ONEP") != nullptr;   // A/B switch (measurement)
     // (instantiated: FP4 stride 1 with 1, 2 or 4 chunks -- Table 1's #1 257 -> 219 us and #2 318 -> 205;
     // the int8 stride-2 #3 measured slower, 142 -> 213 us, and keeps the two-block ring)
     pl.onep = !no_onep && !first && cd.Dci == 1 && cd.Do == 1 && cd.zo_beg == 0 && pl.dil == 1 && cd.nseg == 1 &&
@@ -1504,7 +1504,7 @@ static bool plan_tz(const ConvDesc& cd, TzPlan& pl, bool first = false, bool f4 
     pl.Po = cd.Wo + pl.dil;                    // dil zero separator columns per raster row
     {   // raster staging: whole packed rows copied to 16-byte aligned slots of pitch Po
         const int bpv = cd.nseg != 1 ? 0 : (first ? 4 : 8 * cd.seg[0].cw);   // staged bytes per voxel
-        static const bool no_rstg = getenv("TN_TZ_NO_RSTG") != nullptr;   // A/B switch (measurement)
+        static const bool no_rstg = ab_env("TN_TZ_NO_RSTG") != nullptr;   // A/B switch (measurement)
         pl.rstg = (first && f4) ||   // FF4 only stages raster rows
                   (!no_rstg && f4 && cd.nseg == 1 && pl.s == 1 && !first && pl.dil == 1 && bpv > 0 &&
                    (cd.seg[0].W * bpv) % 16 == 0 && cd.seg[0].W >= 128);   // (narrow rows: one copy per strip
@@ -1792,7 +1792,7 @@ static ConvDesc first_desc(const FirstDesc& fd) {
 // FF4 (FP4 operands, raster-staged float rows, one-channel C = 16 path) when it plans, else the
 // int8 9-tap rows
 static bool plan_first(const ConvDesc& cd, TzPlan& pl) {
-    static const bool no_ff4 = getenv("TN_TZ_NO_FF4") != nullptr;   // A/B switch (measurement)
+    static const bool no_ff4 = ab_env("TN_TZ_NO_FF4") != nullptr;   // A/B switch (measurement)
     if (!no_ff4 && plan_tz(cd, pl, true, true) && tz_smem(pl, pl.kp) <= 227 * 1024) return true;
     pl = TzPlan{};
     return plan_tz(cd, pl, true, false) && tz_smem(pl, pl.kp) <= 227 * 1024;
@@ -1843,7 +1843,7 @@ static bool plan_any(const ConvDesc& cd, TzPlan& pl, bool allow_f4) {
     // K in 33..64 at stride 1 with C <= 64: FP4 without the split (five-block rotated B image,
     // two tiles per strip, half the halo rows per output): C1's conv 82.9 -> 75.3 us
     const bool f4_k64 = cd.K > 32 && cd.s[0] == 1 && c_tot <= 64;
-    static const bool force_f4 = getenv("TN_TZ_FORCE_F4") != nullptr;   // (experiments)
+    static const bool force_f4 = ab_env("TN_TZ_FORCE_F4") != nullptr;   // (experiments)
     allow_f4 = allow_f4 && ((cd.K <= 32 && !(cd.s[0] == 2 && c_tot > 16)) || c_tot > 64 || f4_k64 || force_f4);
     if (allow_f4 && plan_tz(cd, pl, false, true) && tz_instantiated(cd, pl) && tz_smem(pl, pl.kp) <= 227 * 1024)
         return true;

@@ -458,7 +458,7 @@ bool plan_wide(const ConvDesc& cd, unsigned tapmask, WPlan& pl) {
     // TMEM: nbuf accumulator buffers of T * N columns below the scale columns (480..511).  One
     // buffer of more tiles measured faster on every Table-1 layer than two (the expanders and
     // the B stream bound the layers, and more tiles per strip cut both); TN_WIDE_NBUF overrides.
-    static const char* env_nbuf = getenv("TN_WIDE_NBUF");
+    static const char* env_nbuf = ab_env("TN_WIDE_NBUF");
     pl.nbuf = env_nbuf ? std::max(1, std::min(2, atoi(env_nbuf))) : 1;
     const int tmax = (pl.nbuf == 2 ? 240 : 480) / pl.N;
     int tstart = std::min(tmax, pl.NT);

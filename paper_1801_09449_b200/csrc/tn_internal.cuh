@@ -137,6 +137,9 @@ bool        conv_tz_first_supported(const FirstDesc& fd);
 cudaError_t launch_conv_tz_first(const FirstDesc& fd, cudaStream_t s);
 // tn_set_grid_cap: upper bound on the persistent tensor-core grids (0 = #SMs).
 int         persistent_grid_cap();
+// Measurement A/B switches (TN_TZ_NO_*, TN_WIDE_NBUF): the environment value only in the A/B
+// build (`build.py --ab`, libtn_ab.so, -DTN_AB); the product library ignores the environment.
+const char* ab_env(const char* name);
 // The first layer may use the TZ kernel under the current selector (AUTO or TZ).
 bool        first_kernel_tz_allowed();
 cudaError_t launch_conv_tz(const ConvDesc& cd, cudaStream_t s, bool allow_f4 = true);
